@@ -1,0 +1,155 @@
+/*
+ * ibcuda.h -- C ABI of the B200-native immersed-boundary coupling library
+ * (libibcuda.so, built from paper_2012_06646_b200/csrc/).
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (/root/reference/proj/include/ib/, a header-only C++20 template library).
+ * Each entry point names the reference interface it replaces.  The C++
+ * shim include/ib_b200/ib.hpp re-exposes these as the reference's own
+ * ib:: templates (same names, argument meaning and exceptions); the ctypes
+ * binding paper_2012_06646_b200/_capi.py is what tests and bench.py use.
+ *
+ * Conventions
+ *  - Points are AoS, n x dim doubles (ib::PointSet<D> = vector<array<double,D>>,
+ *    grid.hpp:187-188).  Fields are colexicographic, axis 0 fastest
+ *    (ib::GridField<D>, grid.hpp:85-92).
+ *  - Status codes mirror the reference's exceptions:
+ *      IBC_ERR_INVALID_ARGUMENT <-> std::invalid_argument
+ *      IBC_ERR_LENGTH           <-> std::length_error
+ *      IBC_ERR_ALLOC            <-> std::bad_alloc (workspace construction)
+ *    ibc_last_error() returns the message of the calling thread's last failure.
+ *  - Host-buffer entry points (ibc_spread, ibc_interpolate) are synchronous,
+ *    like the reference calls.  *_device entry points take device pointers,
+ *    enqueue on the context's stream and return immediately; they never
+ *    allocate or synchronize once the workspace/context scratch is sized, so
+ *    they may be captured in a CUDA graph.
+ *  - `workers` is accepted for signature compatibility with the reference and
+ *    ignored: the device decides its own parallelism.
+ *  - Results are deterministic: repeated calls on the same inputs are bitwise
+ *    identical (no floating-point atomics anywhere on the path).
+ */
+#ifndef IBCUDA_H
+#define IBCUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IBC_API_VERSION 1
+
+typedef enum {
+  IBC_OK = 0,
+  IBC_ERR_INVALID_ARGUMENT = 1,
+  IBC_ERR_LENGTH = 2,
+  IBC_ERR_CUDA = 3,
+  IBC_ERR_ALLOC = 4
+} ibc_status;
+
+/* Delta kernels.  The reference ships exactly one: CosineKernel,
+ * phi(r) = (1 + cos(pi r / 2)) / 4 on |r| < 2, support 4 (kernel.hpp:23-36). */
+typedef enum { IBC_KERNEL_COSINE4 = 0 } ibc_kernel;
+
+/* ib::SpreadAlgorithm (spread.hpp:21).  Every algorithm computes the same
+ * operator; on the device all of them run the write-once tiled spread. */
+typedef enum {
+  IBC_SPREAD_SERIAL = 0,
+  IBC_SPREAD_FUSED = 1,
+  IBC_SPREAD_BUFFERED = 2,
+  IBC_SPREAD_OTF = 3
+} ibc_spread_algorithm;
+
+/* ib::StaggeredGrid<D> (grid.hpp:33-83).  Entries past `dim` are ignored. */
+typedef struct {
+  int dim;              /* 1..3 */
+  int extent[3];        /* grid points per axis, >= 1 */
+  double spacing;       /* h > 0 */
+  double staggering[3]; /* alpha in [0, 1) */
+  int periodic[3];      /* 0 / 1 */
+  double origin[3];
+} ibc_grid;
+
+typedef struct ibc_context ibc_context;
+typedef struct ibc_workspace ibc_workspace;
+
+/* Per-kernel-class device times (ms) accumulated while profiling is on. */
+typedef struct {
+  double keys_ms;    /* fused cell-key + radix-histogram kernel      */
+  double sort_ms;    /* digit scan + onesweep passes                 */
+  double rows_ms;    /* row-start table + run count                  */
+  double prep_ms;    /* sorted per-point weight records (spread)     */
+  double spread_ms;  /* write-once tiled spread                      */
+  double interp_ms;  /* interpolation gather                          */
+  uint64_t spread_calls;
+  uint64_t interp_calls;
+} ibc_profile;
+
+int ibc_version(void);
+const char* ibc_last_error(void);
+
+/* Context = device + stream + scratch.  Replaces the reference's implicit
+ * OpenMP team (parallel.hpp:25-36). */
+ibc_status ibc_context_create(int device, ibc_context** out);
+ibc_status ibc_context_destroy(ibc_context* ctx);
+/* cudaStream_t to enqueue on (NULL = the legacy default stream). */
+ibc_status ibc_context_set_stream(ibc_context* ctx, void* stream);
+ibc_status ibc_context_synchronize(ibc_context* ctx);
+ibc_status ibc_context_set_profiling(ibc_context* ctx, int on);
+ibc_status ibc_context_get_profile(ibc_context* ctx, ibc_profile* out); /* synchronizes */
+ibc_status ibc_context_reset_profile(ibc_context* ctx);
+/* Number of device kernels this context has launched so far. */
+uint64_t ibc_context_launches(const ibc_context* ctx);
+
+/* StaggeredGrid<D> constructor validation (grid.hpp:37-60). */
+ibc_status ibc_grid_check(const ibc_grid* grid);
+
+/* ib::SpreadWorkspace<D>(n, grid, b) (spread.hpp:27-56): device buffers sized
+ * once for (point count, grid, sweep width).  b < 0 -> invalid_argument. */
+ibc_status ibc_workspace_create(ibc_context* ctx, size_t n, const ibc_grid* grid,
+                                int sweep_width, ibc_workspace** out);
+ibc_status ibc_workspace_destroy(ibc_workspace* ws);
+ibc_status ibc_workspace_info(const ibc_workspace* ws, size_t* point_count,
+                              size_t* grid_points, int* sweep_width);
+/* Observable results of the most recent spread through `ws` (synchronize):
+ * ws.run_count, ws.keys (sorted), ws.perm, ws.run_keys[0..q) (spread.hpp:33-41). */
+ibc_status ibc_workspace_run_count(ibc_workspace* ws, size_t* q);
+ibc_status ibc_workspace_get_keys(ibc_workspace* ws, uint32_t* host_keys, size_t n);
+ibc_status ibc_workspace_get_perm(ibc_workspace* ws, uint32_t* host_perm, size_t n);
+ibc_status ibc_workspace_get_run_keys(ibc_workspace* ws, uint32_t* host_run_keys, size_t cap,
+                                      size_t* q);
+
+/* Spreading, host buffers.  Replaces ib::spread_serial (spread.hpp:129-131),
+ * ib::spread_fused (:165-168), ib::spread_buffered (:223-226) and
+ * ib::spread_buffered_otf (:309-313) -- selected by `algorithm` with the
+ * reference's argument checks (:60-77, :314).  `ws` is required for FUSED and
+ * BUFFERED (BUFFERED additionally needs sweep_width >= 1 in ws), ignored
+ * otherwise.  out: prod(extent) doubles, fully overwritten. */
+ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                      ibc_spread_algorithm algorithm, const double* points,
+                      const double* values, size_t n_points, size_t n_values,
+                      int sweep_width, ibc_workspace* ws, int workers, double* out);
+
+/* Interpolation, host buffers.  Replaces ib::interpolate (interpolate.hpp:22-24). */
+ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                           const double* field, const double* points, size_t n_points,
+                           int workers, double* out);
+
+/* Device-resident variants (async on the context stream).  `ws` may be NULL
+ * (context scratch is used).  d_out of the spread is fully overwritten. */
+ibc_status ibc_spread_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                             const double* d_points, const double* d_values, size_t n,
+                             ibc_workspace* ws, double* d_out);
+ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                  const double* d_field, const double* d_points, size_t n,
+                                  double* d_out);
+
+/* ib::stats (stats.hpp:9-25): every operation adds n_points * 4^dim. */
+uint64_t ibc_delta_evaluations(void);
+void ibc_reset_delta_evaluations(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IBCUDA_H */

@@ -1,0 +1,71 @@
+"""In-tree build of libibcuda.so (sm_100a) and the test-side native pieces."""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "_lib" / "libibcuda.so"
+SOURCES = ["ibc_kernels.cu", "ibc_api.cu"]
+HEADERS = ["ibc_device.cuh", "ibc_sort.cuh", "ibc_internal.h"]
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+
+def nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_lib(force: bool = False, verbose: bool = False) -> Path:
+    deps = [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "ibcuda.h", Path(__file__)]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    LIB.parent.mkdir(parents=True, exist_ok=True)
+    cmd = [nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", f"-I{CSRC}",
+           *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    return LIB
+
+
+def build_oracle() -> None:
+    """Test infrastructure: the C restatement + (when present) the reference build."""
+    subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
+
+
+def build_cpp_tests() -> Path | None:
+    """C++ drop-in shim test (include/ib_b200/ib.hpp), linked against libibcuda.so."""
+    src = ROOT / "tests" / "cpp" / "shim_test.cpp"
+    if not src.exists():
+        return None
+    out = ROOT / "tests" / "cpp" / "build" / "shim_test"
+    deps = [src, ROOT / "include" / "ib_b200" / "ib.hpp", ROOT / "include" / "ibcuda.h", LIB,
+            ROOT / "oracle" / "ib_oracle.h"]
+    if not _stale(out, deps):
+        return out
+    out.parent.mkdir(parents=True, exist_ok=True)
+    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else (shutil.which("g++") or "g++")
+    cmd = [cxx, "-O2", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{ROOT / 'oracle'}", str(src),
+           "-o", str(out), f"-L{LIB.parent}", "-libcuda", f"-Wl,-rpath,{LIB.parent}",
+           f"-L{ROOT / 'oracle'}", "-loracle", f"-Wl,-rpath,{ROOT / 'oracle'}"]
+    subprocess.run(cmd, check=True)
+    return out

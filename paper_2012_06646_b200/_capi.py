@@ -1,0 +1,154 @@
+"""ctypes binding of the C ABI in include/ibcuda.h (libibcuda.so).
+
+This is the binding a Python caller of the reference-facing boundary would
+add; INTEGRATION.md shows it next to the C++ (include/ib_b200/ib.hpp) one.
+The library is required: there is no CPU fallback, and importing the
+operators without the built extension raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libibcuda.so"
+
+IBC_OK = 0
+IBC_ERR_INVALID_ARGUMENT = 1
+IBC_ERR_LENGTH = 2
+IBC_ERR_CUDA = 3
+IBC_ERR_ALLOC = 4
+
+IBC_KERNEL_COSINE4 = 0
+
+IBC_SPREAD_SERIAL = 0
+IBC_SPREAD_FUSED = 1
+IBC_SPREAD_BUFFERED = 2
+IBC_SPREAD_OTF = 3
+
+
+class IbcGrid(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int),
+        ("extent", C.c_int * 3),
+        ("spacing", C.c_double),
+        ("staggering", C.c_double * 3),
+        ("periodic", C.c_int * 3),
+        ("origin", C.c_double * 3),
+    ]
+
+
+class IbcProfile(C.Structure):
+    _fields_ = [
+        ("keys_ms", C.c_double),
+        ("sort_ms", C.c_double),
+        ("rows_ms", C.c_double),
+        ("prep_ms", C.c_double),
+        ("spread_ms", C.c_double),
+        ("interp_ms", C.c_double),
+        ("spread_calls", C.c_uint64),
+        ("interp_calls", C.c_uint64),
+    ]
+
+
+_vp = C.c_void_p
+_sz = C.c_size_t
+_G = C.POINTER(IbcGrid)
+_st = C.c_int
+
+# name -> (restype, argtypes); every symbol declared in include/ibcuda.h.
+SIGNATURES = {
+    "ibc_version": (C.c_int, []),
+    "ibc_last_error": (C.c_char_p, []),
+    "ibc_context_create": (_st, [C.c_int, C.POINTER(_vp)]),
+    "ibc_context_destroy": (_st, [_vp]),
+    "ibc_context_set_stream": (_st, [_vp, _vp]),
+    "ibc_context_synchronize": (_st, [_vp]),
+    "ibc_context_set_profiling": (_st, [_vp, C.c_int]),
+    "ibc_context_get_profile": (_st, [_vp, C.POINTER(IbcProfile)]),
+    "ibc_context_reset_profile": (_st, [_vp]),
+    "ibc_context_launches": (C.c_uint64, [_vp]),
+    "ibc_grid_check": (_st, [_G]),
+    "ibc_workspace_create": (_st, [_vp, _sz, _G, C.c_int, C.POINTER(_vp)]),
+    "ibc_workspace_destroy": (_st, [_vp]),
+    "ibc_workspace_info": (_st, [_vp, C.POINTER(_sz), C.POINTER(_sz), C.POINTER(C.c_int)]),
+    "ibc_workspace_run_count": (_st, [_vp, C.POINTER(_sz)]),
+    "ibc_workspace_get_keys": (_st, [_vp, _vp, _sz]),
+    "ibc_workspace_get_perm": (_st, [_vp, _vp, _sz]),
+    "ibc_workspace_get_run_keys": (_st, [_vp, _vp, _sz, C.POINTER(_sz)]),
+    "ibc_spread": (_st, [_vp, _G, C.c_int, C.c_int, _vp, _vp, _sz, _sz, C.c_int, _vp, C.c_int, _vp]),
+    "ibc_interpolate": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, C.c_int, _vp]),
+    "ibc_spread_device": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, _vp, _vp]),
+    "ibc_interpolate_device": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, _vp]),
+    "ibc_delta_evaluations": (C.c_uint64, []),
+    "ibc_reset_delta_evaluations": (None, []),
+}
+
+
+class IbError(RuntimeError):
+    """Base of the errors raised through the C ABI."""
+
+
+class InvalidArgument(IbError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class LengthError(IbError, ValueError):
+    """std::length_error in the reference."""
+
+
+class CudaError(IbError):
+    """A CUDA runtime failure inside the library."""
+
+
+class AllocationError(IbError, MemoryError):
+    """std::bad_alloc (workspace construction)."""
+
+
+_ERRORS = {
+    IBC_ERR_INVALID_ARGUMENT: InvalidArgument,
+    IBC_ERR_LENGTH: LengthError,
+    IBC_ERR_CUDA: CudaError,
+    IBC_ERR_ALLOC: AllocationError,
+}
+
+_lib = None
+
+
+def load(path: Path | None = None):
+    """Load libibcuda.so (in-tree build).  Raises if it is missing."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise ImportError(
+            f"{p} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback for the B200 IB operators)")
+    lib = C.CDLL(str(p))
+    for name, (res, args) in SIGNATURES.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status == IBC_OK:
+        return
+    msg = (_lib or load()).ibc_last_error().decode(errors="replace")
+    raise _ERRORS.get(status, IbError)(msg)
+
+
+def make_grid(extents, spacing, staggering, periodic, origin=None) -> IbcGrid:
+    d = len(extents)
+    g = IbcGrid()
+    g.dim = d
+    for a in range(3):
+        g.extent[a] = int(extents[a]) if a < d else 1
+        g.staggering[a] = float(staggering[a]) if a < d else 0.0
+        g.periodic[a] = int(bool(periodic[a])) if a < d else 0
+        g.origin[a] = float(origin[a]) if (origin is not None and a < d) else 0.0
+    g.spacing = float(spacing)
+    return g

@@ -1,0 +1,467 @@
+// ibc_api.cu -- extern "C" boundary (include/ibcuda.h).
+//
+// Argument validation mirrors the reference exactly (same conditions, same
+// messages) so the C++ shim can rethrow the reference's exception types:
+//   StaggeredGrid ctor        grid.hpp:37-60
+//   check_spread_args         spread.hpp:60-66
+//   check_workspace           spread.hpp:68-77
+//   SpreadWorkspace ctor      spread.hpp:43-45
+//   spread_buffered_otf       spread.hpp:314
+//   spread_vector (null ws)   spread.hpp:335,339
+//   interpolate               interpolate.hpp:27-28
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "ibc_internal.h"
+
+struct ibc_context {
+  ibc::Context c;
+};
+struct ibc_workspace {
+  ibc::Workspace w;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_delta_evaluations{0};
+
+struct ApiError {
+  ibc_status status;
+  std::string msg;
+};
+
+[[noreturn]] void invalid(const char* msg) { throw ApiError{IBC_ERR_INVALID_ARGUMENT, msg}; }
+
+template <class F>
+ibc_status guarded(F&& f) {
+  try {
+    f();
+    return IBC_OK;
+  } catch (const ApiError& e) {
+    g_last_error = e.msg;
+    return e.status;
+  } catch (const ibc::CudaError& e) {
+    g_last_error = e.where + ": " + cudaGetErrorString(e.code);
+    return e.code == cudaErrorMemoryAllocation ? IBC_ERR_ALLOC : IBC_ERR_CUDA;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "allocation failed";
+    return IBC_ERR_ALLOC;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return IBC_ERR_CUDA;
+  }
+}
+
+void check_grid(const ibc_grid* g) {
+  if (!g) invalid("grid is null");
+  if (g->dim < 1 || g->dim > 3) invalid("grids are 1-, 2-, or 3-dimensional");
+  if (!(g->spacing > 0.0) || !std::isfinite(g->spacing)) invalid("grid spacing must be positive");
+  uint64_t extended = 1;
+  for (int a = 0; a < g->dim; ++a) {
+    if (g->extent[a] < 1) invalid("grid extent must be >= 1");
+    if (!(g->staggering[a] >= 0.0 && g->staggering[a] < 1.0))
+      invalid("staggering must lie in [0, 1)");
+    extended *= (uint64_t)g->extent[a] + 2;
+    if (extended >= (uint64_t{1} << 32))
+      throw ApiError{IBC_ERR_LENGTH, "extended grid exceeds 32-bit key range"};
+  }
+}
+
+size_t grid_points(const ibc_grid* g) {
+  size_t p = 1;
+  for (int a = 0; a < g->dim; ++a) p *= (size_t)g->extent[a];
+  return p;
+}
+
+void check_kernel(ibc_kernel k) {
+  if (k != IBC_KERNEL_COSINE4) invalid("unsupported kernel support size");
+}
+
+void check_points(size_t n) {
+  if (n > ibc::kMaxPoints) invalid("point count exceeds the device limit of 2^30 - 1");
+}
+
+uint64_t shift_count(int dim) {
+  uint64_t s = 1;
+  for (int a = 0; a < dim; ++a) s *= ibc::kSupport;
+  return s;
+}
+
+void use_device(ibc::Context& c) { IBC_CUDA(cudaSetDevice(c.device)); }
+
+ibc::PointScratch& spread_scratch_for(ibc::Context& c, ibc_workspace* ws, size_t n,
+                                      const ibc::DevGrid& g) {
+  ibc::PointScratch& s = ws ? ws->w.s : c.spread_scratch;
+  if (!ws) s.reserve_points(n, true);
+  else if (s.cap < n) s.reserve_points(n, true);
+  s.reserve_rows(g.nrows);
+  return s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- Context
+namespace ibc {
+cudaEvent_t Context::acquire_event() {
+  if (!event_pool.empty()) {
+    cudaEvent_t e = event_pool.back();
+    event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  IBC_CUDA(cudaEventCreate(&e));
+  return e;
+}
+void Context::prof_begin(int, cudaEvent_t* ev) {
+  *ev = nullptr;
+  if (!profiling) return;
+  *ev = acquire_event();
+  IBC_CUDA(cudaEventRecord(*ev, stream));
+}
+void Context::prof_end(int cls, cudaEvent_t ev) {
+  if (!profiling || !ev) return;
+  cudaEvent_t e = acquire_event();
+  IBC_CUDA(cudaEventRecord(e, stream));
+  pending.push_back({cls, {ev, e}});
+}
+}  // namespace ibc
+
+extern "C" {
+
+int ibc_version(void) { return IBC_API_VERSION; }
+const char* ibc_last_error(void) { return g_last_error.c_str(); }
+
+ibc_status ibc_context_create(int device, ibc_context** out) {
+  return guarded([&] {
+    if (!out) invalid("out is null");
+    int count = 0;
+    IBC_CUDA(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) invalid("no such CUDA device");
+    IBC_CUDA(cudaSetDevice(device));
+    auto* ctx = new ibc_context();
+    ctx->c.device = device;
+    *out = ctx;
+  });
+}
+
+ibc_status ibc_context_destroy(ibc_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->c.device);
+    cudaStreamSynchronize(ctx->c.stream);
+    ctx->c.spread_scratch.release_all();
+    ctx->c.interp_scratch.release_all();
+    for (auto& b : ctx->c.h_stage) b.release();
+    for (auto& p : ctx->c.pending) {
+      cudaEventDestroy(p.second.first);
+      cudaEventDestroy(p.second.second);
+    }
+    for (auto e : ctx->c.event_pool) cudaEventDestroy(e);
+    delete ctx;
+  });
+}
+
+ibc_status ibc_context_set_stream(ibc_context* ctx, void* stream) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    ctx->c.stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+ibc_status ibc_context_synchronize(ibc_context* ctx) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    use_device(ctx->c);
+    IBC_CUDA(cudaStreamSynchronize(ctx->c.stream));
+  });
+}
+
+ibc_status ibc_context_set_profiling(ibc_context* ctx, int on) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    ctx->c.profiling = on != 0;
+  });
+}
+
+ibc_status ibc_context_get_profile(ibc_context* ctx, ibc_profile* out) {
+  return guarded([&] {
+    if (!ctx || !out) invalid("null argument");
+    auto& c = ctx->c;
+    use_device(c);
+    IBC_CUDA(cudaStreamSynchronize(c.stream));
+    for (auto& p : c.pending) {
+      float ms = 0.f;
+      IBC_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+      c.prof_ms[p.first] += ms;
+      c.event_pool.push_back(p.second.first);
+      c.event_pool.push_back(p.second.second);
+    }
+    c.pending.clear();
+    out->keys_ms = c.prof_ms[ibc::kProfKeys];
+    out->sort_ms = c.prof_ms[ibc::kProfSort];
+    out->rows_ms = c.prof_ms[ibc::kProfRows];
+    out->prep_ms = c.prof_ms[ibc::kProfPrep];
+    out->spread_ms = c.prof_ms[ibc::kProfSpread];
+    out->interp_ms = c.prof_ms[ibc::kProfInterp];
+    out->spread_calls = c.spread_calls;
+    out->interp_calls = c.interp_calls;
+  });
+}
+
+ibc_status ibc_context_reset_profile(ibc_context* ctx) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    auto& c = ctx->c;
+    IBC_CUDA(cudaStreamSynchronize(c.stream));
+    for (auto& p : c.pending) {
+      c.event_pool.push_back(p.second.first);
+      c.event_pool.push_back(p.second.second);
+    }
+    c.pending.clear();
+    for (double& v : c.prof_ms) v = 0.0;
+    c.spread_calls = c.interp_calls = 0;
+  });
+}
+
+uint64_t ibc_context_launches(const ibc_context* ctx) { return ctx ? ctx->c.launches : 0; }
+
+ibc_status ibc_grid_check(const ibc_grid* grid) { return guarded([&] { check_grid(grid); }); }
+
+// ---------------------------------------------------------------- Workspace
+ibc_status ibc_workspace_create(ibc_context* ctx, size_t n, const ibc_grid* grid, int sweep_width,
+                                ibc_workspace** out) {
+  return guarded([&] {
+    if (!ctx || !out) invalid("null argument");
+    check_grid(grid);
+    if (sweep_width < 0) invalid("sweep width must be >= 1 (or 0 for none)");
+    check_points(n);
+    use_device(ctx->c);
+    auto* ws = new ibc_workspace();
+    try {
+      ws->w.ctx = &ctx->c;
+      ws->w.point_count = n;
+      ws->w.grid_points = grid_points(grid);
+      ws->w.sweep_width = sweep_width;
+      ws->w.s.reserve_points(n, true);
+      ws->w.s.reserve_rows(ibc::make_devgrid(*grid).nrows);
+    } catch (...) {
+      ws->w.s.release_all();
+      delete ws;
+      throw;
+    }
+    *out = ws;
+  });
+}
+
+ibc_status ibc_workspace_destroy(ibc_workspace* ws) {
+  return guarded([&] {
+    if (!ws) return;
+    cudaSetDevice(ws->w.ctx->device);
+    cudaStreamSynchronize(ws->w.ctx->stream);
+    ws->w.s.release_all();
+    delete ws;
+  });
+}
+
+ibc_status ibc_workspace_info(const ibc_workspace* ws, size_t* point_count, size_t* gp,
+                              int* sweep_width) {
+  return guarded([&] {
+    if (!ws) invalid("workspace is null");
+    if (point_count) *point_count = ws->w.point_count;
+    if (gp) *gp = ws->w.grid_points;
+    if (sweep_width) *sweep_width = ws->w.sweep_width;
+  });
+}
+
+ibc_status ibc_workspace_run_count(ibc_workspace* ws, size_t* q) {
+  return guarded([&] {
+    if (!ws || !q) invalid("null argument");
+    use_device(*ws->w.ctx);
+    *q = ws->w.s.last_n ? ibc::read_run_count(*ws->w.ctx, ws->w.s) : 0;
+  });
+}
+
+static void copy_sorted(ibc_workspace* ws, uint32_t* host, size_t n, bool perm) {
+  if (!ws || (!host && n)) invalid("null argument");
+  auto& s = ws->w.s;
+  if (n != s.last_n) invalid("buffer size differs from the last spread's point count");
+  if (!n) return;
+  use_device(*ws->w.ctx);
+  IBC_CUDA(cudaMemcpyAsync(host, perm ? s.sorted_perm : s.sorted_keys, n * 4,
+                           cudaMemcpyDeviceToHost, ws->w.ctx->stream));
+  IBC_CUDA(cudaStreamSynchronize(ws->w.ctx->stream));
+}
+
+ibc_status ibc_workspace_get_keys(ibc_workspace* ws, uint32_t* host_keys, size_t n) {
+  return guarded([&] { copy_sorted(ws, host_keys, n, false); });
+}
+
+ibc_status ibc_workspace_get_perm(ibc_workspace* ws, uint32_t* host_perm, size_t n) {
+  return guarded([&] { copy_sorted(ws, host_perm, n, true); });
+}
+
+ibc_status ibc_workspace_get_run_keys(ibc_workspace* ws, uint32_t* host, size_t cap, size_t* q) {
+  return guarded([&] {
+    if (!ws || !q) invalid("null argument");
+    auto& s = ws->w.s;
+    use_device(*ws->w.ctx);
+    if (!s.last_n) {
+      *q = 0;
+      return;
+    }
+    const size_t runs = ibc::compute_run_keys(*ws->w.ctx, s);
+    *q = runs;
+    if (!host) return;
+    if (cap < runs) invalid("run key buffer too small");
+    IBC_CUDA(cudaMemcpyAsync(host, s.run_keys.p, runs * 4, cudaMemcpyDeviceToHost,
+                             ws->w.ctx->stream));
+    IBC_CUDA(cudaStreamSynchronize(ws->w.ctx->stream));
+  });
+}
+
+// ---------------------------------------------------------------- Operators
+static void spread_checks(const ibc_grid* grid, ibc_kernel kernel, ibc_spread_algorithm algo,
+                          size_t n_points, size_t n_values, int sweep_width, ibc_workspace* ws) {
+  check_grid(grid);
+  if (n_values != n_points) invalid("one value per point required");
+  check_kernel(kernel);
+  check_points(n_points);
+  switch (algo) {
+    case IBC_SPREAD_SERIAL:
+      break;
+    case IBC_SPREAD_FUSED:
+    case IBC_SPREAD_BUFFERED: {
+      if (!ws)
+        invalid(algo == IBC_SPREAD_FUSED ? "fused spreading needs a workspace"
+                                         : "buffered spreading needs a workspace");
+      if (ws->w.point_count != n_points) invalid("workspace sized for a different point count");
+      if (ws->w.grid_points != grid_points(grid)) invalid("workspace sized for a different grid");
+      if (algo == IBC_SPREAD_BUFFERED && ws->w.sweep_width < 1)
+        invalid("workspace has no sweep buffers");
+      break;
+    }
+    case IBC_SPREAD_OTF:
+      if (sweep_width < 1) invalid("sweep width must be >= 1");
+      break;
+    default:
+      invalid("unknown spreading algorithm");
+  }
+}
+
+ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                      ibc_spread_algorithm algorithm, const double* points, const double* values,
+                      size_t n_points, size_t n_values, int sweep_width, ibc_workspace* ws,
+                      int workers, double* out) {
+  (void)workers;
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    spread_checks(grid, kernel, algorithm, n_points, n_values, sweep_width, ws);
+    if ((!points || !values) && n_points) invalid("null input buffer");
+    if (!out) invalid("null output buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    // Serial/otf own no caller workspace: they run on the context's scratch.
+    ibc_workspace* use_ws =
+        (algorithm == IBC_SPREAD_FUSED || algorithm == IBC_SPREAD_BUFFERED) ? ws : nullptr;
+    ibc::PointScratch& s = spread_scratch_for(c, use_ws, n_points, g);
+    const size_t np = grid_points(grid);
+    c.h_stage[0].ensure(n_points * grid->dim);
+    c.h_stage[1].ensure(n_points);
+    c.h_stage[2].ensure(np);
+    if (n_points) {
+      IBC_CUDA(cudaMemcpyAsync(c.h_stage[0].p, points, n_points * grid->dim * 8,
+                               cudaMemcpyHostToDevice, c.stream));
+      IBC_CUDA(cudaMemcpyAsync(c.h_stage[1].p, values, n_points * 8, cudaMemcpyHostToDevice,
+                               c.stream));
+    }
+    ibc::spread_pipeline(c, g, c.h_stage[0].p, c.h_stage[1].p, n_points, s, c.h_stage[2].p);
+    IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream));
+    IBC_CUDA(cudaStreamSynchronize(c.stream));
+    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim), std::memory_order_relaxed);
+  });
+}
+
+ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                           const double* field, const double* points, size_t n_points,
+                           int workers, double* out) {
+  (void)workers;
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_grid(grid);
+    check_kernel(kernel);
+    check_points(n_points);
+    if (!field) invalid("null field");
+    if (n_points && (!points || !out)) invalid("null point buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    const size_t np = grid_points(grid);
+    c.interp_scratch.reserve_points(n_points, false);
+    c.h_stage[2].ensure(np);
+    c.h_stage[0].ensure(n_points * grid->dim);
+    c.h_stage[3].ensure(n_points);
+    IBC_CUDA(cudaMemcpyAsync(c.h_stage[2].p, field, np * 8, cudaMemcpyHostToDevice, c.stream));
+    if (n_points)
+      IBC_CUDA(cudaMemcpyAsync(c.h_stage[0].p, points, n_points * grid->dim * 8,
+                               cudaMemcpyHostToDevice, c.stream));
+    ibc::interp_pipeline(c, g, c.h_stage[2].p, c.h_stage[0].p, n_points, c.interp_scratch,
+                         c.h_stage[3].p);
+    if (n_points)
+      IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[3].p, n_points * 8, cudaMemcpyDeviceToHost,
+                               c.stream));
+    IBC_CUDA(cudaStreamSynchronize(c.stream));
+    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim), std::memory_order_relaxed);
+  });
+}
+
+ibc_status ibc_spread_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                             const double* d_points, const double* d_values, size_t n,
+                             ibc_workspace* ws, double* d_out) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_grid(grid);
+    check_kernel(kernel);
+    check_points(n);
+    if (ws) {
+      if (ws->w.point_count != n) invalid("workspace sized for a different point count");
+      if (ws->w.grid_points != grid_points(grid)) invalid("workspace sized for a different grid");
+    }
+    if (!d_out) invalid("null output buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    ibc::PointScratch& s = spread_scratch_for(c, ws, n, g);
+    ibc::spread_pipeline(c, g, d_points, d_values, n, s, d_out);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+  });
+}
+
+ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                  const double* d_field, const double* d_points, size_t n,
+                                  double* d_out) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_grid(grid);
+    check_kernel(kernel);
+    check_points(n);
+    auto& c = ctx->c;
+    use_device(c);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    c.interp_scratch.reserve_points(n, false);
+    ibc::interp_pipeline(c, g, d_field, d_points, n, c.interp_scratch, d_out);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+  });
+}
+
+uint64_t ibc_delta_evaluations(void) { return g_delta_evaluations.load(std::memory_order_relaxed); }
+void ibc_reset_delta_evaluations(void) { g_delta_evaluations.store(0, std::memory_order_relaxed); }
+
+}  // extern "C"

@@ -1,0 +1,93 @@
+// ibc_device.cuh -- grid geometry, cell keys and delta weights on the device.
+//
+// Integer results (cells, keys) must be bit-identical to the reference
+// (/root/reference/proj/include/ib/grid.hpp).  The floating-point steps that
+// decide them are therefore written with explicit round-to-nearest intrinsics
+// so nvcc cannot contract them into FMAs: the reference's x86-64 Release build
+// has no FMA (plain -O3, no -march).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ibc {
+
+constexpr int kSupport = 4;  // CosineKernel::support (kernel.hpp:34)
+// The onesweep look-back packs per-digit counts into 30 bits.
+constexpr uint32_t kMaxPoints = (1u << 30) - 1;
+
+// Precomputed, kernel-argument-sized view of ib::StaggeredGrid<D>.
+// Axes past `dim` are padded: extent 1, not periodic, zero strides.
+struct DevGrid {
+  int dim;
+  int n[3];
+  int periodic[3];
+  double h;
+  double alpha[3];
+  double origin[3];
+  double len[3];        // extent * spacing exactly as axis_length (grid.hpp:72)
+  uint64_t kstride[3];  // cell_key strides prod_{b<a} (n_b + 2) (grid.hpp:158-170)
+  uint32_t rowdiv;      // n[0] + 2: key / rowdiv = extended row id
+  uint32_t nrows;       // number of extended rows (prod_{a>=1,a<dim} (n_a + 2))
+  int64_t npts;         // prod(extent)
+  double hd;            // pow(h, dim), computed on the host with std::pow
+  double inv_h;
+};
+
+__device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
+  int r = i % e;
+  if (r < 0) r += e;
+  return r;
+}
+
+// wrap_position (grid.hpp:197-207) + cell_index for even support
+// (grid.hpp:121-130) on one axis.  Returns the cell; *xw gets the wrapped x.
+__device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double* xw) {
+  double w = x;
+  if (g.periodic[a]) {
+    double r = fmod(__dsub_rn(x, g.origin[a]), g.len[a]);
+    if (r < 0.0) r = __dadd_rn(r, g.len[a]);
+    w = __dadd_rn(g.origin[a], r);
+  }
+  *xw = w;
+  const double t = __dsub_rn(__ddiv_rn(__dsub_rn(w, g.origin[a]), g.h), g.alpha[a]);
+  return (int)ceil(t);
+}
+
+// displacement_ratio (support_window.hpp:48-55): (xw - h*(i+alpha) - o) / h.
+__device__ __forceinline__ double displacement(const DevGrid& g, int a, double xw, int c) {
+  const double hp = __dadd_rn(__dmul_rn(g.h, __dadd_rn((double)c, g.alpha[a])), g.origin[a]);
+  return __ddiv_rn(__dsub_rn(xw, hp), g.h);
+}
+
+// cell_key (grid.hpp:158-170) of already-computed (unwrapped) cells.
+__device__ __forceinline__ uint32_t cell_key(const DevGrid& g, const int* c) {
+  uint64_t k = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (a >= g.dim) break;
+    int ca = c[a];
+    if (g.periodic[a]) ca = wrap_cell(ca, g.n[a]);
+    k += (uint64_t)(int64_t)(ca + 1) * g.kstride[a];
+  }
+  return (uint32_t)k;
+}
+
+// Per-axis weights phi(sigma - t) / h for sigma = -2..1 (index sigma + 2) of
+// the 4-point cosine kernel (kernel.hpp:24-36, 64-69).  With u = -t and
+// theta = pi u / 2 the four values are (1-cos), (1+sin), (1+cos), (1-sin)
+// over 4: one sincospi per axis instead of four cos.  |r| >= 2 cut-offs
+// fall out exactly (the terms vanish at the ends of the support).
+__device__ __forceinline__ void cosine_weights(double t, double inv_h, double w[4]) {
+  double s, c;
+  sincospi(-0.5 * t, &s, &c);
+  w[0] = (0.25 * (1.0 - c)) * inv_h;
+  w[1] = (0.25 * (1.0 + s)) * inv_h;
+  w[2] = (0.25 * (1.0 + c)) * inv_h;
+  w[3] = (0.25 * (1.0 - s)) * inv_h;
+}
+
+// Padded axis (a >= dim): only sigma = 0 contributes, with factor 1.
+__device__ __forceinline__ void unit_weights(double w[4]) {
+  w[0] = 0.0; w[1] = 0.0; w[2] = 1.0; w[3] = 0.0;
+}
+
+}  // namespace ibc

@@ -1,0 +1,99 @@
+// ibc_internal.h -- host-side objects behind the C ABI (not installed).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "ibc_device.cuh"
+#include "ibcuda.h"
+
+namespace ibc {
+
+struct CudaError {
+  cudaError_t code;
+  std::string where;
+};
+
+inline void check_cuda(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) throw CudaError{e, where};
+}
+#define IBC_CUDA(x) ::ibc::check_cuda((x), #x)
+
+// Device buffer owned by a workspace or context.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;  // elements
+  void ensure(size_t n) {
+    if (n <= cap && p) return;
+    release();
+    const size_t want = n ? n : 1;
+    IBC_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    cap = want;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+enum ProfClass { kProfKeys = 0, kProfSort, kProfRows, kProfPrep, kProfSpread, kProfInterp, kProfCount };
+
+// Scratch of one key-sort + tiled operator over up to `cap` points.
+struct PointScratch {
+  size_t cap = 0;
+  DevBuf<uint32_t> keys[2], vals[2];
+  DevBuf<uint32_t> hist, base, lookback, counters;
+  DevBuf<uint32_t> rowstart;
+  DevBuf<int> rec_cx;
+  DevBuf<double> rec;         // 12 x cap weight records (spread)
+  DevBuf<uint32_t> run_keys;  // lazily filled
+  DevBuf<uint32_t> block_counts;
+  const uint32_t* sorted_keys = nullptr;
+  const uint32_t* sorted_perm = nullptr;
+  size_t last_n = 0;
+  bool run_keys_valid = false;
+  void reserve_points(size_t n, bool spread);
+  void reserve_rows(size_t nrows);
+  void release_all();
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool profiling = false;
+  uint64_t launches = 0;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double prof_ms[kProfCount] = {0, 0, 0, 0, 0, 0};
+  uint64_t spread_calls = 0, interp_calls = 0;
+  PointScratch spread_scratch;  // spreads without a user workspace
+  PointScratch interp_scratch;  // interpolation
+  DevBuf<double> h_stage[4];    // device staging for host-buffer calls
+  cudaEvent_t acquire_event();
+  void prof_begin(int cls, cudaEvent_t* ev);
+  void prof_end(int cls, cudaEvent_t ev);
+};
+
+struct Workspace {
+  Context* ctx = nullptr;
+  size_t point_count = 0;
+  size_t grid_points = 0;
+  int sweep_width = 0;
+  PointScratch s;
+};
+
+// Pipelines (ibc_kernels.cu).  All enqueue on ctx.stream; no host sync.
+DevGrid make_devgrid(const ibc_grid& g);
+void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points,
+                     const double* d_values, size_t n, PointScratch& s, double* d_out);
+void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field,
+                     const double* d_points, size_t n, PointScratch& s, double* d_out);
+// ws.run_keys on the device; returns q (synchronizes).
+size_t compute_run_keys(Context& ctx, PointScratch& s);
+size_t read_run_count(Context& ctx, PointScratch& s);
+
+}  // namespace ibc

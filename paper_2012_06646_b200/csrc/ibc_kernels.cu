@@ -1,0 +1,559 @@
+// ibc_kernels.cu -- the spread / interpolate hot path for sm_100a.
+//
+// Per operator call:
+//   K1 keys_hist_kernel   wrap -> cell -> 32-bit key per point + the digit
+//                          histograms of every radix pass        (grid.hpp:121-207)
+//   K2 digit_scan + onesweep_pass x P  stable key/index sort     (sort.hpp:17-71)
+//   K3 rowstart_kernel    extended-row start table + run count q (reduce.hpp:36-69)
+//   K4 prep_records_kernel + spread_tiles_kernel  write-once spread
+//                                                                 (spread.hpp:165-216)
+//   K5 interp_kernel      interpolation gather                   (interpolate.hpp:22-58)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ibc_internal.h"
+#include "ibc_sort.cuh"
+
+namespace ibc {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kSpreadThreads = 256;
+constexpr int kMaxPasses = 4;
+constexpr int kCounters = kMaxPasses + 1;  // tile counters + run count q
+
+__device__ __forceinline__ uint32_t lanemask_le() {
+  const int lane = threadIdx.x & 31;
+  return lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+}
+
+// ---------------------------------------------------------------- K1
+__global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const double* __restrict__ X,
+                                                           uint32_t n, uint32_t* __restrict__ keys,
+                                                           uint32_t* __restrict__ hist, int passes) {
+  __shared__ uint32_t sh[kMaxPasses * sort::kRadix];
+  for (int t = threadIdx.x; t < kMaxPasses * sort::kRadix; t += blockDim.x) sh[t] = 0u;
+  __syncthreads();
+  const int D = g.dim;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    int c[3] = {0, 0, 0};
+    for (int a = 0; a < D; ++a) {
+      double xw;
+      c[a] = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
+    }
+    const uint32_t key = cell_key(g, c);
+    keys[i] = key;
+    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * sort::kRadix + ((key >> (8 * p)) & 255u)], 1u);
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < passes * sort::kRadix; t += blockDim.x)
+    if (sh[t]) atomicAdd(&hist[t], sh[t]);
+}
+
+// ---------------------------------------------------------------- K3
+// rowstart[r] = first sorted index whose extended row id is >= r, r in [0, nrows].
+__global__ void __launch_bounds__(kBlock) rowstart_kernel(const uint32_t* __restrict__ sk, uint32_t n,
+                                                          uint32_t rowdiv, uint32_t nrows,
+                                                          uint32_t* __restrict__ rowstart,
+                                                          uint32_t* __restrict__ q_out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  bool head = false;
+  if (i < n) {
+    const uint32_t k = sk[i];
+    const uint32_t row = k / rowdiv;
+    if (i == 0) {
+      for (uint32_t r = 0; r <= row; ++r) rowstart[r] = 0u;
+      head = true;
+    } else {
+      const uint32_t pk = sk[i - 1];
+      const uint32_t prow = pk / rowdiv;
+      for (uint32_t r = prow + 1; r <= row; ++r) rowstart[r] = i;
+      head = pk != k;
+    }
+    if (i == n - 1)
+      for (uint32_t r = row + 1; r <= nrows; ++r) rowstart[r] = n;
+  }
+  const uint32_t hb = __ballot_sync(0xffffffffu, head);
+  if ((threadIdx.x & 31) == 0 && hb) atomicAdd(q_out, (uint32_t)__popc(hb));
+}
+
+// ---------------------------------------------------------------- K4a
+// Sorted per-point weight records for the tiled spread:
+//   rec[k][r]     = G * phi_x(k-2 - t_x)/h     (k = 0..3)
+//   rec[4+k][r]   = phi_y(k-2 - t_y)/h
+//   rec[8+k][r]   = phi_z(k-2 - t_z)/h
+//   rec_cx[r]     = home cell along x (wrapped on periodic axes)
+__global__ void __launch_bounds__(kBlock) prep_records_kernel(DevGrid g, const double* __restrict__ X,
+                                                              const double* __restrict__ G,
+                                                              const uint32_t* __restrict__ perm,
+                                                              uint32_t n, int* __restrict__ rec_cx,
+                                                              double* __restrict__ rec) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t i = __ldg(perm + r);
+  const int D = g.dim;
+  double w[3][4];
+  int c0 = 0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a < D) {
+      double xw;
+      const int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
+      cosine_weights(displacement(g, a, xw, c), g.inv_h, w[a]);
+      if (a == 0) c0 = g.periodic[0] ? wrap_cell(c, g.n[0]) : c;
+    } else {
+      unit_weights(w[a]);
+    }
+  }
+  const double gv = __ldg(G + i);
+  rec_cx[r] = c0;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    rec[(size_t)k * n + r] = w[0][k] * gv;
+    rec[(size_t)(4 + k) * n + r] = w[1][k];
+    rec[(size_t)(8 + k) * n + r] = w[2][k];
+  }
+}
+
+// ---------------------------------------------------------------- K4b
+struct SpreadTiling {
+  int tx, ty, tz;     // target tile extents (tx == n0 when rows are whole)
+  int ntx, nty, ntz;  // tiles per axis
+};
+
+// Write-once spread.  One CTA owns a tile of target rows (all of x, or an x
+// chunk) x ty x tz held in shared memory.  Warp w owns target rows w, w+8, ...
+// and PULLS, in fixed (sigma_z, sigma_y) order, the sorted points of every
+// source row that reaches it; the sorted order makes equal-cell lanes of a
+// 32-point batch contiguous, and those are serialized by their rank in the
+// cell, so shared-memory accumulation needs no atomics and the summation
+// order is fixed (results are bitwise reproducible).  Each grid value is
+// written to HBM exactly once, with coalesced stores.
+__global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
+    DevGrid g, SpreadTiling T, const uint32_t* __restrict__ rowstart,
+    const int* __restrict__ rec_cx, const double* __restrict__ rec, uint32_t n,
+    double* __restrict__ out) {
+  extern __shared__ double s_acc[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  int b = blockIdx.x;
+  const int bx = b % T.ntx;
+  b /= T.ntx;
+  const int by = b % T.nty;
+  const int bz = b / T.nty;
+  const int x0 = bx * T.tx, y0 = by * T.ty, z0 = bz * T.tz;
+  const int rows = T.ty * T.tz;
+  const int cells = rows * T.tx;
+  for (int i = tid; i < cells; i += blockDim.x) s_acc[i] = 0.0;
+  __syncthreads();
+
+  const double* wy = rec + (size_t)4 * n;
+  const double* wz = rec + (size_t)8 * n;
+  const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
+  const int sylo = g.dim >= 2 ? -2 : 0, syhi = g.dim >= 2 ? 1 : 0;
+  const uint32_t le = lanemask_le();
+
+  for (int tr = warp; tr < rows; tr += nwarps) {
+    const int ty = y0 + tr % T.ty, tz = z0 + tr / T.ty;
+    if (ty >= g.n[1] || tz >= g.n[2]) continue;
+    double* acc = s_acc + (size_t)tr * T.tx;
+    for (int sz = szlo; sz <= szhi; ++sz) {
+      int cz = 0;
+      if (g.dim >= 3) {
+        cz = tz - sz;
+        if (g.periodic[2]) cz = wrap_cell(cz, g.n[2]);
+        else if (cz < -1 || cz > g.n[2]) continue;
+      }
+      for (int sy = sylo; sy <= syhi; ++sy) {
+        int cy = 0;
+        if (g.dim >= 2) {
+          cy = ty - sy;
+          if (g.periodic[1]) cy = wrap_cell(cy, g.n[1]);
+          else if (cy < -1 || cy > g.n[1]) continue;
+        }
+        const uint32_t row = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
+                             (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(g.n[1] + 2) : 0u);
+        const uint32_t rb = __ldg(rowstart + row), re = __ldg(rowstart + row + 1);
+        const double* wyc = wy + (size_t)(sy + 2) * n;
+        const double* wzc = wz + (size_t)(sz + 2) * n;
+        for (uint32_t base = rb; base < re; base += 32) {
+          const uint32_t r = base + lane;
+          const bool valid = r < re;
+          int cx = 0x7fffffff;
+          double a = 0.0, gk[4] = {0.0, 0.0, 0.0, 0.0};
+          if (valid) {
+            cx = __ldg(rec_cx + r);
+            a = __ldg(wyc + r) * __ldg(wzc + r);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) gk[k] = __ldg(rec + (size_t)k * n + r);
+          }
+          const int pcx = __shfl_up_sync(0xffffffffu, cx, 1);
+          const bool head = valid && (lane == 0 || pcx != cx);
+          const uint32_t hm = __ballot_sync(0xffffffffu, head);
+          const int rank = valid ? lane - (31 - __clz(hm & le)) : 0;
+          const int maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            int xt = cx + k - 2;
+            bool ok = valid;
+            if (g.periodic[0]) xt = wrap_cell(xt, g.n[0]);
+            else ok = ok && xt >= 0 && xt < g.n[0];
+            xt -= x0;
+            ok = ok && xt >= 0 && xt < T.tx;
+            const double v = gk[k] * a;
+            for (int rr = 0; rr <= maxrank; ++rr) {
+              if (ok && rank == rr) acc[xt] += v;
+              __syncwarp();
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t sy_ = g.n[0], sz_ = (int64_t)g.n[0] * g.n[1];
+  for (int i = tid; i < cells; i += blockDim.x) {
+    const int tr = i / T.tx, xx = i - tr * T.tx;
+    const int ty = y0 + tr % T.ty, tz = z0 + tr / T.ty, x = x0 + xx;
+    if (ty < g.n[1] && tz < g.n[2] && x < g.n[0]) out[tz * sz_ + ty * sy_ + x] = s_acc[i];
+  }
+}
+
+// ---------------------------------------------------------------- K5
+// One thread per point, visited in sorted (cell) order so neighbouring
+// threads gather neighbouring grid values; result stored at the point's
+// input slot.  Summation order over the 4^d support is the reference's
+// colexicographic shift order (interpolate.hpp:42-52).
+__global__ void __launch_bounds__(kBlock) interp_kernel(DevGrid g, const double* __restrict__ field,
+                                                        const double* __restrict__ X,
+                                                        const uint32_t* __restrict__ perm, uint32_t n,
+                                                        double* __restrict__ out) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const uint32_t i = perm ? __ldg(perm + r) : r;
+  const int D = g.dim;
+  constexpr int64_t kInvalid = INT64_MIN / 4;  // support_window.hpp:15-16
+  double w[3][4];
+  int64_t off[3][4];
+  int64_t stride = 1;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (a < D) {
+      double xw;
+      const int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
+      cosine_weights(displacement(g, a, xw, c), g.inv_h, w[a]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int cc = c + k - 2;
+        if (g.periodic[a]) off[a][k] = stride * wrap_cell(cc, g.n[a]);
+        else off[a][k] = (cc < 0 || cc >= g.n[a]) ? kInvalid : stride * cc;
+      }
+      stride *= g.n[a];
+    } else {
+      unit_weights(w[a]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) off[a][k] = 0;
+    }
+  }
+  const int zlo = D >= 3 ? 0 : 2, zhi = D >= 3 ? 3 : 2;
+  const int ylo = D >= 2 ? 0 : 2, yhi = D >= 2 ? 3 : 2;
+  double acc = 0.0;
+#pragma unroll
+  for (int kz = 0; kz < 4; ++kz) {
+    if (kz < zlo || kz > zhi) continue;
+#pragma unroll
+    for (int ky = 0; ky < 4; ++ky) {
+      if (ky < ylo || ky > yhi) continue;
+      const int64_t oyz = off[1][ky] + off[2][kz];
+#pragma unroll
+      for (int kx = 0; kx < 4; ++kx) {
+        const int64_t o = off[0][kx] + oyz;
+        if (o >= 0) {
+          const double wt = (w[0][kx] * w[1][ky]) * w[2][kz];
+          acc += wt * __ldg(field + o);
+        }
+      }
+    }
+  }
+  out[i] = acc * g.hd;
+}
+
+// ---------------------------------------------------------------- run keys
+__global__ void __launch_bounds__(kBlock) head_count_kernel(const uint32_t* __restrict__ sk, uint32_t n,
+                                                            uint32_t* __restrict__ counts) {
+  __shared__ uint32_t s;
+  if (threadIdx.x == 0) s = 0;
+  __syncthreads();
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const bool head = i < n && (i == 0 || sk[i] != sk[i - 1]);
+  const uint32_t hb = __ballot_sync(0xffffffffu, head);
+  if ((threadIdx.x & 31) == 0) atomicAdd(&s, (uint32_t)__popc(hb));
+  __syncthreads();
+  if (threadIdx.x == 0) counts[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(sort::kThreads) block_scan_kernel(uint32_t* counts, uint32_t nb) {
+  __shared__ uint32_t s_warp[sort::kWarps];
+  __shared__ uint32_t s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  for (uint32_t base = 0; base < nb; base += sort::kThreads) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < nb ? counts[i] : 0u;
+    const uint32_t ex = sort::block_exclusive_scan(v, s_warp);
+    const uint32_t carry = s_carry;
+    if (i < nb) counts[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == sort::kThreads - 1) s_carry = carry + ex + v;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) head_write_kernel(const uint32_t* __restrict__ sk, uint32_t n,
+                                                            const uint32_t* __restrict__ offsets,
+                                                            uint32_t* __restrict__ run_keys) {
+  __shared__ uint32_t s_w[kBlock / 32];
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool head = i < n && (i == 0 || sk[i] != sk[i - 1]);
+  const uint32_t hb = __ballot_sync(0xffffffffu, head);
+  if (lane == 0) s_w[warp] = __popc(hb);
+  __syncthreads();
+  uint32_t base = offsets[blockIdx.x];
+  for (int w = 0; w < warp; ++w) base += s_w[w];
+  if (head) run_keys[base + __popc(hb & ((1u << lane) - 1u))] = sk[i];
+}
+
+int key_bits(const DevGrid& g) {
+  uint64_t ext = 1;
+  for (int a = 0; a < g.dim; ++a) ext *= (uint64_t)g.n[a] + 2;
+  const uint64_t max_key = ext - 1;
+  int bits = 1;
+  while (bits < 32 && (max_key >> bits) != 0) ++bits;
+  return bits;
+}
+
+inline unsigned grid_for(size_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+// Keys + stable sort.  Leaves s.sorted_keys / s.sorted_perm.
+void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t n, PointScratch& s) {
+  cudaStream_t st = ctx.stream;
+  const int passes = (key_bits(g) + sort::kRadixBits - 1) / sort::kRadixBits;
+  const size_t tiles = (n + sort::kTile - 1) / sort::kTile;
+  IBC_CUDA(cudaMemsetAsync(s.hist.p, 0, (size_t)kMaxPasses * sort::kRadix * 4, st));
+  IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
+  IBC_CUDA(cudaMemsetAsync(s.lookback.p, 0, (size_t)passes * tiles * sort::kRadix * 4, st));
+
+  cudaEvent_t ev = nullptr;
+  ctx.prof_begin(kProfKeys, &ev);
+  const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock), 148u * 8u));
+  keys_hist_kernel<<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, passes);
+  ++ctx.launches;
+  ctx.prof_end(kProfKeys, ev);
+
+  ctx.prof_begin(kProfSort, &ev);
+  sort::digit_scan<<<passes, sort::kThreads, 0, st>>>(s.hist.p, s.base.p);
+  ++ctx.launches;
+  int src = 0;
+  for (int p = 0; p < passes; ++p) {
+    sort::onesweep_pass<<<(unsigned)tiles, sort::kThreads, 0, st>>>(
+        s.keys[src].p, p == 0 ? nullptr : s.vals[src].p, s.keys[src ^ 1].p, s.vals[src ^ 1].p,
+        (uint32_t)n, 8 * p, s.base.p + (size_t)p * sort::kRadix,
+        s.lookback.p + (size_t)p * tiles * sort::kRadix, s.counters.p + p);
+    ++ctx.launches;
+    src ^= 1;
+  }
+  ctx.prof_end(kProfSort, ev);
+  IBC_CUDA(cudaGetLastError());
+  s.sorted_keys = s.keys[src].p;
+  s.sorted_perm = s.vals[src].p;
+  s.last_n = n;
+  s.run_keys_valid = false;
+}
+
+void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
+  cudaStream_t st = ctx.stream;
+  cudaEvent_t ev = nullptr;
+  ctx.prof_begin(kProfRows, &ev);
+  if (n == 0) {
+    IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)g.nrows + 1) * 4, st));
+  } else {
+    rowstart_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, g.rowdiv,
+                                                            g.nrows, s.rowstart.p,
+                                                            s.counters.p + kMaxPasses);
+    ++ctx.launches;
+  }
+  ctx.prof_end(kProfRows, ev);
+}
+
+SpreadTiling choose_tiling(const DevGrid& g) {
+  // Target tile: whole x rows when they fit (periodic x then wraps inside the
+  // tile), times ty x tz rows, <= 64 KB of doubles in shared memory.
+  SpreadTiling T;
+  const int n0 = g.n[0];
+  T.tx = n0 <= 4096 ? n0 : 2048;
+  const int rows_budget = std::max(1, (64 * 1024 / 8) / T.tx);
+  int ty = 1, tz = 1;
+  if (g.dim >= 3) {
+    if (rows_budget >= 16) { ty = 4; tz = 4; }
+    else if (rows_budget >= 8) { ty = 4; tz = 2; }
+    else if (rows_budget >= 4) { ty = 2; tz = 2; }
+    else if (rows_budget >= 2) { ty = 2; tz = 1; }
+  } else if (g.dim == 2) {
+    ty = std::min(rows_budget, 16);
+  }
+  ty = std::max(1, std::min(ty, g.n[1]));
+  tz = std::max(1, std::min(tz, g.n[2]));
+  T.ty = ty;
+  T.tz = tz;
+  T.ntx = (n0 + T.tx - 1) / T.tx;
+  T.nty = (g.n[1] + ty - 1) / ty;
+  T.ntz = (g.n[2] + tz - 1) / tz;
+  return T;
+}
+
+}  // namespace
+
+DevGrid make_devgrid(const ibc_grid& gi) {
+  DevGrid g{};
+  g.dim = gi.dim;
+  g.h = gi.spacing;
+  g.inv_h = 1.0 / gi.spacing;
+  uint64_t ks = 1;
+  g.npts = 1;
+  for (int a = 0; a < 3; ++a) {
+    if (a < gi.dim) {
+      g.n[a] = gi.extent[a];
+      g.periodic[a] = gi.periodic[a] ? 1 : 0;
+      g.alpha[a] = gi.staggering[a];
+      g.origin[a] = gi.origin[a];
+      g.len[a] = gi.extent[a] * gi.spacing;
+      g.kstride[a] = ks;
+      ks *= (uint64_t)gi.extent[a] + 2;
+      g.npts *= gi.extent[a];
+    } else {
+      g.n[a] = 1;
+      g.periodic[a] = 0;
+      g.alpha[a] = 0.0;
+      g.origin[a] = 0.0;
+      g.len[a] = gi.spacing;
+      g.kstride[a] = 0;
+    }
+  }
+  g.rowdiv = (uint32_t)(g.n[0] + 2);
+  g.nrows = 1;
+  for (int a = 1; a < gi.dim; ++a) g.nrows *= (uint32_t)(g.n[a] + 2);
+  g.hd = std::pow(gi.spacing, (double)gi.dim);
+  return g;
+}
+
+void PointScratch::reserve_points(size_t n, bool spread) {
+  const size_t tiles = (n + sort::kTile - 1) / sort::kTile;
+  for (int b = 0; b < 2; ++b) {
+    keys[b].ensure(n);
+    vals[b].ensure(n);
+  }
+  hist.ensure((size_t)kMaxPasses * sort::kRadix);
+  base.ensure((size_t)kMaxPasses * sort::kRadix);
+  lookback.ensure((size_t)kMaxPasses * std::max<size_t>(tiles, 1) * sort::kRadix);
+  counters.ensure(kCounters);
+  if (spread) {
+    rec_cx.ensure(n);
+    rec.ensure(12 * std::max<size_t>(n, 1));
+  }
+  cap = std::max(cap, n);
+}
+
+void PointScratch::reserve_rows(size_t nrows) { rowstart.ensure(nrows + 1); }
+
+void PointScratch::release_all() {
+  for (int b = 0; b < 2; ++b) {
+    keys[b].release();
+    vals[b].release();
+  }
+  hist.release(); base.release(); lookback.release(); counters.release(); rowstart.release();
+  rec_cx.release(); rec.release(); run_keys.release(); block_counts.release();
+  cap = 0;
+}
+
+void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
+                     size_t n, PointScratch& s, double* d_out) {
+  cudaStream_t st = ctx.stream;
+  if (n > 0) sort_points(ctx, g, d_points, n, s);
+  else {
+    IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
+    s.last_n = 0;
+    s.sorted_keys = s.keys[0].p;
+    s.sorted_perm = s.vals[0].p;
+    s.run_keys_valid = false;
+  }
+  row_table(ctx, g, n, s);
+  cudaEvent_t ev = nullptr;
+  if (n > 0) {
+    ctx.prof_begin(kProfPrep, &ev);
+    prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_points, d_values, s.sorted_perm,
+                                                                (uint32_t)n, s.rec_cx.p, s.rec.p);
+    ++ctx.launches;
+    ctx.prof_end(kProfPrep, ev);
+  }
+  const SpreadTiling T = choose_tiling(g);
+  const size_t smem = (size_t)T.tx * T.ty * T.tz * sizeof(double);
+  static bool attr_set[64] = {};
+  if (!attr_set[ctx.device & 63]) {
+    IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  160 * 1024));
+    attr_set[ctx.device & 63] = true;
+  }
+  ctx.prof_begin(kProfSpread, &ev);
+  const unsigned blocks = (unsigned)((size_t)T.ntx * T.nty * T.ntz);
+  spread_tiles_kernel<<<blocks, kSpreadThreads, smem, st>>>(g, T, s.rowstart.p, s.rec_cx.p, s.rec.p,
+                                                            (uint32_t)n, d_out);
+  ++ctx.launches;
+  ctx.prof_end(kProfSpread, ev);
+  IBC_CUDA(cudaGetLastError());
+  ++ctx.spread_calls;
+}
+
+void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
+                     size_t n, PointScratch& s, double* d_out) {
+  if (n == 0) return;
+  cudaStream_t st = ctx.stream;
+  sort_points(ctx, g, d_points, n, s);
+  cudaEvent_t ev = nullptr;
+  ctx.prof_begin(kProfInterp, &ev);
+  interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
+                                                        (uint32_t)n, d_out);
+  ++ctx.launches;
+  ctx.prof_end(kProfInterp, ev);
+  IBC_CUDA(cudaGetLastError());
+  ++ctx.interp_calls;
+}
+
+size_t read_run_count(Context& ctx, PointScratch& s) {
+  uint32_t q = 0;
+  IBC_CUDA(cudaMemcpyAsync(&q, s.counters.p + kMaxPasses, 4, cudaMemcpyDeviceToHost, ctx.stream));
+  IBC_CUDA(cudaStreamSynchronize(ctx.stream));
+  return q;
+}
+
+size_t compute_run_keys(Context& ctx, PointScratch& s) {
+  const size_t n = s.last_n;
+  const size_t q = read_run_count(ctx, s);
+  if (s.run_keys_valid || n == 0) return q;
+  cudaStream_t st = ctx.stream;
+  const unsigned nb = grid_for(n, kBlock);
+  s.block_counts.ensure(nb);
+  s.run_keys.ensure(std::max<size_t>(q, 1));
+  head_count_kernel<<<nb, kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, s.block_counts.p);
+  block_scan_kernel<<<1, sort::kThreads, 0, st>>>(s.block_counts.p, nb);
+  head_write_kernel<<<nb, kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, s.block_counts.p, s.run_keys.p);
+  ctx.launches += 3;
+  IBC_CUDA(cudaGetLastError());
+  IBC_CUDA(cudaStreamSynchronize(st));
+  s.run_keys_valid = true;
+  return q;
+}
+
+}  // namespace ibc

@@ -1,0 +1,87 @@
+"""Device-resident operators on torch CUDA tensors (HBM in, HBM out).
+
+The hot path the bench measures: inputs already resident, results left on
+the device, everything enqueued on torch's current stream through
+``ibc_spread_device`` / ``ibc_interpolate_device``.  torch is plumbing here
+(allocation, streams, events); the kernels are libibcuda.so's.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+from . import _capi
+from ._capi import InvalidArgument, check, load
+from .ib import Context, SpreadWorkspace, StaggeredGrid
+
+
+def _ptr(t) -> C.c_void_p:
+    return C.c_void_p(int(t.data_ptr()))
+
+
+def _require(t, name, numel=None):
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise InvalidArgument(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float64 or not t.is_contiguous():
+        raise InvalidArgument(f"{name} must be contiguous float64")
+    if numel is not None and t.numel() != numel:
+        raise InvalidArgument(f"{name} has {t.numel()} elements, expected {numel}")
+
+
+class DeviceOperators:
+    """Spread / interpolate on one GPU with a persistent context + workspace."""
+
+    def __init__(self, device: int = 0):
+        self.device = int(device)
+        self.context = Context(self.device)
+        self._ws: dict[tuple, SpreadWorkspace] = {}
+
+    def _sync_stream(self):
+        import torch
+
+        self.context.set_stream(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def workspace(self, n: int, grid: StaggeredGrid) -> SpreadWorkspace:
+        key = (n, grid.point_count())
+        if key not in self._ws:
+            self._ws[key] = SpreadWorkspace(n, grid, 0, context=self.context)
+        return self._ws[key]
+
+    def spread(self, points, values, grid: StaggeredGrid, out=None, workspace=None):
+        """points (n, D) float64 cuda, values (n,) -> out (prod(extent),) float64 cuda."""
+        import torch
+
+        n = points.shape[0] if points.dim() == 2 else points.numel() // grid.dim
+        _require(points, "points", n * grid.dim)
+        _require(values, "values", n)
+        if out is None:
+            out = torch.empty(grid.point_count(), dtype=torch.float64, device=points.device)
+        _require(out, "out", grid.point_count())
+        ws = workspace if workspace is not None else self.workspace(n, grid)
+        self._sync_stream()
+        check(load().ibc_spread_device(self.context.handle, C.byref(grid.c_grid),
+                                       _capi.IBC_KERNEL_COSINE4, _ptr(points), _ptr(values), n,
+                                       ws.handle, _ptr(out)))
+        ws._mark(n)
+        return out
+
+    def interpolate(self, field, points, grid: StaggeredGrid, out=None):
+        """field (prod(extent),) + points (n, D) -> out (n,), all float64 cuda."""
+        import torch
+
+        n = points.shape[0] if points.dim() == 2 else points.numel() // grid.dim
+        _require(field, "field", grid.point_count())
+        _require(points, "points", n * grid.dim)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=points.device)
+        _require(out, "out", n)
+        self._sync_stream()
+        check(load().ibc_interpolate_device(self.context.handle, C.byref(grid.c_grid),
+                                            _capi.IBC_KERNEL_COSINE4, _ptr(field), _ptr(points),
+                                            n, _ptr(out)))
+        return out
+
+    @property
+    def launches(self) -> int:
+        return self.context.launches
