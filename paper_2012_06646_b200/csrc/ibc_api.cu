@@ -405,6 +405,7 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
     const ibc::DevGrid g = ibc::make_devgrid(*grid);
     const size_t np = grid_points(grid);
     c.interp_scratch.reserve_points(n_points, false);
+    c.interp_scratch.reserve_rows(g.nrows);
     c.h_stage[2].ensure(np);
     c.h_stage[0].ensure(n_points * grid->dim);
     c.h_stage[3].ensure(n_points);
@@ -456,6 +457,7 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
     use_device(c);
     const ibc::DevGrid g = ibc::make_devgrid(*grid);
     c.interp_scratch.reserve_points(n, false);
+    c.interp_scratch.reserve_rows(g.nrows);
     ibc::interp_pipeline(c, g, d_field, d_points, n, c.interp_scratch, d_out);
     g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
   });

@@ -34,6 +34,9 @@ struct DevGrid {
 };
 
 __device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
+  if (i >= 0 && i < e) return i;  // common case, no integer division
+  if (i < 0 && i >= -e) return i + e;
+  if (i >= e && i < 2 * e) return i - e;
   int r = i % e;
   if (r < 0) r += e;
   return r;
@@ -44,7 +47,9 @@ __device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
 __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double* xw) {
   double w = x;
   if (g.periodic[a]) {
-    double r = fmod(__dsub_rn(x, g.origin[a]), g.len[a]);
+    const double d = __dsub_rn(x, g.origin[a]);
+    // fmod(d, len) == d exactly when |d| < len: skip the iterative fmod.
+    double r = fabs(d) < g.len[a] ? d : fmod(d, g.len[a]);
     if (r < 0.0) r = __dadd_rn(r, g.len[a]);
     w = __dadd_rn(g.origin[a], r);
   }

@@ -56,6 +56,7 @@ struct PointScratch {
   const uint32_t* sorted_perm = nullptr;
   size_t last_n = 0;
   bool run_keys_valid = false;
+  bool keys_are_rows = false;  // last sort was by row id only (interpolation)
   void reserve_points(size_t n, bool spread);
   void reserve_rows(size_t nrows);
   void release_all();

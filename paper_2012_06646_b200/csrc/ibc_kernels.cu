@@ -8,6 +8,8 @@
 //   K4 prep_records_kernel + spread_tiles_kernel  write-once spread
 //                                                                 (spread.hpp:165-216)
 //   K5 interp_kernel      interpolation gather                   (interpolate.hpp:22-58)
+// 3-D grids take the z-sweep kernels of ibc_zsweep.cuh for K4/K5; the
+// kernels here are the general path (1-D/2-D grids, very long x rows).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -15,6 +17,7 @@
 
 #include "ibc_internal.h"
 #include "ibc_sort.cuh"
+#include "ibc_zsweep.cuh"
 
 namespace ibc {
 
@@ -22,7 +25,7 @@ namespace {
 
 constexpr int kBlock = 256;
 constexpr int kSpreadThreads = 256;
-constexpr int kMaxPasses = 4;
+constexpr int kMaxPasses = sort::kMaxPasses;
 constexpr int kCounters = kMaxPasses + 1;  // tile counters + run count q
 
 __device__ __forceinline__ uint32_t lanemask_le() {
@@ -31,11 +34,14 @@ __device__ __forceinline__ uint32_t lanemask_le() {
 }
 
 // ---------------------------------------------------------------- K1
+// Cell key of every point (or, with row_only, its extended row id -- all the
+// interpolation needs) and the digit histograms of every radix pass.
 __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const double* __restrict__ X,
                                                            uint32_t n, uint32_t* __restrict__ keys,
-                                                           uint32_t* __restrict__ hist, int passes) {
-  __shared__ uint32_t sh[kMaxPasses * sort::kRadix];
-  for (int t = threadIdx.x; t < kMaxPasses * sort::kRadix; t += blockDim.x) sh[t] = 0u;
+                                                           uint32_t* __restrict__ hist,
+                                                           sort::DigitPlan plan, int row_only) {
+  __shared__ uint32_t sh[kMaxPasses * sort::kMaxRadix];
+  for (int t = threadIdx.x; t < kMaxPasses * sort::kMaxRadix; t += blockDim.x) sh[t] = 0u;
   __syncthreads();
   const int D = g.dim;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
@@ -44,12 +50,14 @@ __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const doub
       double xw;
       c[a] = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
     }
-    const uint32_t key = cell_key(g, c);
+    uint32_t key = cell_key(g, c);
+    if (row_only) key /= g.rowdiv;
     keys[i] = key;
-    for (int p = 0; p < passes; ++p) atomicAdd(&sh[p * sort::kRadix + ((key >> (8 * p)) & 255u)], 1u);
+    for (int p = 0; p < plan.passes; ++p)
+      atomicAdd(&sh[p * sort::kMaxRadix + ((key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u))], 1u);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < passes * sort::kRadix; t += blockDim.x)
+  for (int t = threadIdx.x; t < plan.passes * sort::kMaxRadix; t += blockDim.x)
     if (sh[t]) atomicAdd(&hist[t], sh[t]);
 }
 
@@ -76,8 +84,13 @@ __global__ void __launch_bounds__(kBlock) rowstart_kernel(const uint32_t* __rest
     if (i == n - 1)
       for (uint32_t r = row + 1; r <= nrows; ++r) rowstart[r] = n;
   }
+  __shared__ uint32_t s_q;
+  if (threadIdx.x == 0) s_q = 0;
+  __syncthreads();
   const uint32_t hb = __ballot_sync(0xffffffffu, head);
-  if ((threadIdx.x & 31) == 0 && hb) atomicAdd(q_out, (uint32_t)__popc(hb));
+  if ((threadIdx.x & 31) == 0 && hb) atomicAdd(&s_q, (uint32_t)__popc(hb));
+  __syncthreads();
+  if (threadIdx.x == 0 && s_q) atomicAdd(q_out, s_q);  // one global atomic per block
 }
 
 // ---------------------------------------------------------------- K4a
@@ -326,43 +339,63 @@ __global__ void __launch_bounds__(kBlock) head_write_kernel(const uint32_t* __re
   if (head) run_keys[base + __popc(hb & ((1u << lane) - 1u))] = sk[i];
 }
 
-int key_bits(const DevGrid& g) {
-  uint64_t ext = 1;
-  for (int a = 0; a < g.dim; ++a) ext *= (uint64_t)g.n[a] + 2;
-  const uint64_t max_key = ext - 1;
+int bits_for(uint64_t max_key) {
   int bits = 1;
   while (bits < 32 && (max_key >> bits) != 0) ++bits;
   return bits;
 }
 
+// Bits of the largest cell key (row_only: of the largest extended row id).
+int key_bits(const DevGrid& g, bool row_only) {
+  uint64_t ext = 1;
+  for (int a = row_only ? 1 : 0; a < g.dim; ++a) ext *= (uint64_t)g.n[a] + 2;
+  return bits_for(ext - 1);
+}
+
 inline unsigned grid_for(size_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
-// Keys + stable sort.  Leaves s.sorted_keys / s.sorted_perm.
-void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t n, PointScratch& s) {
+size_t sort_smem() { return sizeof(sort::PassSmem); }
+
+// Keys + stable sort.  Leaves s.sorted_keys / s.sorted_perm.  row_only sorts
+// by extended row id alone (enough for the interpolation's row grouping).
+void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t n, PointScratch& s,
+                 bool row_only) {
   cudaStream_t st = ctx.stream;
-  const int passes = (key_bits(g) + sort::kRadixBits - 1) / sort::kRadixBits;
+  const sort::DigitPlan plan = sort::plan_digits(key_bits(g, row_only));
   const size_t tiles = (n + sort::kTile - 1) / sort::kTile;
-  IBC_CUDA(cudaMemsetAsync(s.hist.p, 0, (size_t)kMaxPasses * sort::kRadix * 4, st));
+  IBC_CUDA(cudaMemsetAsync(s.hist.p, 0, (size_t)kMaxPasses * sort::kMaxRadix * 4, st));
   IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
-  IBC_CUDA(cudaMemsetAsync(s.lookback.p, 0, (size_t)passes * tiles * sort::kRadix * 4, st));
+  size_t lb_words = 0;
+  for (int p = 0; p < plan.passes; ++p) lb_words += tiles << plan.bits[p];
+  IBC_CUDA(cudaMemsetAsync(s.lookback.p, 0, lb_words * 4, st));
+
+  static bool attr_set[64] = {};
+  if (!attr_set[ctx.device & 63]) {
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)sort_smem()));
+    attr_set[ctx.device & 63] = true;
+  }
 
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
-  const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock), 148u * 8u));
-  keys_hist_kernel<<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, passes);
+  const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock), 148u * 6u));
+  keys_hist_kernel<<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan,
+                                          row_only ? 1 : 0);
   ++ctx.launches;
   ctx.prof_end(kProfKeys, ev);
 
   ctx.prof_begin(kProfSort, &ev);
-  sort::digit_scan<<<passes, sort::kThreads, 0, st>>>(s.hist.p, s.base.p);
+  sort::digit_scan<<<plan.passes, sort::kThreads, 0, st>>>(s.hist.p, s.base.p, plan);
   ++ctx.launches;
   int src = 0;
-  for (int p = 0; p < passes; ++p) {
-    sort::onesweep_pass<<<(unsigned)tiles, sort::kThreads, 0, st>>>(
+  size_t lb_off = 0;
+  for (int p = 0; p < plan.passes; ++p) {
+    sort::onesweep_pass<<<(unsigned)tiles, sort::kThreads, sort_smem(), st>>>(
         s.keys[src].p, p == 0 ? nullptr : s.vals[src].p, s.keys[src ^ 1].p, s.vals[src ^ 1].p,
-        (uint32_t)n, 8 * p, s.base.p + (size_t)p * sort::kRadix,
-        s.lookback.p + (size_t)p * tiles * sort::kRadix, s.counters.p + p);
+        (uint32_t)n, plan.shift[p], plan.bits[p], s.base.p + (size_t)p * sort::kMaxRadix,
+        s.lookback.p + lb_off, s.counters.p + p);
     ++ctx.launches;
+    lb_off += tiles << plan.bits[p];
     src ^= 1;
   }
   ctx.prof_end(kProfSort, ev);
@@ -371,6 +404,7 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
   s.sorted_perm = s.vals[src].p;
   s.last_n = n;
   s.run_keys_valid = false;
+  s.keys_are_rows = row_only;
 }
 
 void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
@@ -380,12 +414,40 @@ void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
   if (n == 0) {
     IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)g.nrows + 1) * 4, st));
   } else {
-    rowstart_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, g.rowdiv,
-                                                            g.nrows, s.rowstart.p,
-                                                            s.counters.p + kMaxPasses);
+    rowstart_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
+        s.sorted_keys, (uint32_t)n, s.keys_are_rows ? 1u : g.rowdiv, g.nrows, s.rowstart.p,
+        s.counters.p + kMaxPasses);
     ++ctx.launches;
   }
   ctx.prof_end(kProfRows, ev);
+}
+
+// z-sweep tiling for 3-D grids with rows short enough for shared memory.
+bool zsweep_tiling(const DevGrid& g, bool interp, zs::Tiling& T) {
+  if (g.dim != 3) return false;
+  const int nx = g.n[0];
+  T.nxp = nx + zs::kPadL + zs::kPadR;
+  if (T.nxp & 1) T.nxp += 1;
+  const size_t row_bytes = (size_t)T.nxp * 8;
+  const size_t budget = interp ? 100 * 1024 : 72 * 1024;
+  // spread: 4 planes x ty rows; interp: 4 planes x (ty + 5) rows
+  int ty = 16;
+  while (ty > 1 && 4 * (size_t)(ty + (interp ? 5 : 0)) * row_bytes > budget) --ty;
+  if (4 * (size_t)(ty + (interp ? 5 : 0)) * row_bytes > budget) return false;
+  ty = std::min(ty, g.n[1]);
+  if (ty < 1 || ty + 5 > zs::kMaxRows) return false;
+  T.ty = ty;
+  T.nty = (g.n[1] + ty - 1) / ty;
+  // Enough CTAs for ~3 per SM, but z chunks of at least 4 planes.
+  int zc = (int)std::max<long>(4, ((long)g.n[2] * T.nty) / (148L * 3));
+  zc = std::min(zc, g.n[2]);
+  T.zc = zc;
+  T.nzc = (g.n[2] + zc - 1) / zc;
+  return true;
+}
+
+size_t zsweep_smem(const zs::Tiling& T, bool interp) {
+  return (size_t)4 * (T.ty + (interp ? 5 : 0)) * T.nxp * sizeof(double);
 }
 
 SpreadTiling choose_tiling(const DevGrid& g) {
@@ -455,9 +517,9 @@ void PointScratch::reserve_points(size_t n, bool spread) {
     keys[b].ensure(n);
     vals[b].ensure(n);
   }
-  hist.ensure((size_t)kMaxPasses * sort::kRadix);
-  base.ensure((size_t)kMaxPasses * sort::kRadix);
-  lookback.ensure((size_t)kMaxPasses * std::max<size_t>(tiles, 1) * sort::kRadix);
+  hist.ensure((size_t)kMaxPasses * sort::kMaxRadix);
+  base.ensure((size_t)kMaxPasses * sort::kMaxRadix);
+  lookback.ensure((size_t)kMaxPasses * std::max<size_t>(tiles, 1) * sort::kMaxRadix);
   counters.ensure(kCounters);
   if (spread) {
     rec_cx.ensure(n);
@@ -481,37 +543,52 @@ void PointScratch::release_all() {
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
-  if (n > 0) sort_points(ctx, g, d_points, n, s);
-  else {
+  if (n > 0) {
+    sort_points(ctx, g, d_points, n, s, false);
+  } else {
     IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
     s.last_n = 0;
     s.sorted_keys = s.keys[0].p;
     s.sorted_perm = s.vals[0].p;
     s.run_keys_valid = false;
+    s.keys_are_rows = false;
   }
   row_table(ctx, g, n, s);
   cudaEvent_t ev = nullptr;
-  if (n > 0) {
-    ctx.prof_begin(kProfPrep, &ev);
-    prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_points, d_values, s.sorted_perm,
-                                                                (uint32_t)n, s.rec_cx.p, s.rec.p);
-    ++ctx.launches;
-    ctx.prof_end(kProfPrep, ev);
-  }
-  const SpreadTiling T = choose_tiling(g);
-  const size_t smem = (size_t)T.tx * T.ty * T.tz * sizeof(double);
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
     IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
+    IBC_CUDA(cudaFuncSetAttribute(zs::spread_zsweep_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr_set[ctx.device & 63] = true;
   }
-  ctx.prof_begin(kProfSpread, &ev);
-  const unsigned blocks = (unsigned)((size_t)T.ntx * T.nty * T.ntz);
-  spread_tiles_kernel<<<blocks, kSpreadThreads, smem, st>>>(g, T, s.rowstart.p, s.rec_cx.p, s.rec.p,
-                                                            (uint32_t)n, d_out);
-  ++ctx.launches;
-  ctx.prof_end(kProfSpread, ev);
+  zs::Tiling Z;
+  if (zsweep_tiling(g, false, Z)) {
+    ctx.prof_begin(kProfSpread, &ev);
+    zs::spread_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem(Z, false), st>>>(
+        g, Z, s.rowstart.p, s.sorted_keys, s.sorted_perm, d_points, d_values, d_out);
+    ++ctx.launches;
+    ctx.prof_end(kProfSpread, ev);
+  } else {
+    if (n > 0) {
+      ctx.prof_begin(kProfPrep, &ev);
+      prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
+          g, d_points, d_values, s.sorted_perm, (uint32_t)n, s.rec_cx.p, s.rec.p);
+      ++ctx.launches;
+      ctx.prof_end(kProfPrep, ev);
+    }
+    const SpreadTiling T = choose_tiling(g);
+    const size_t smem = (size_t)T.tx * T.ty * T.tz * sizeof(double);
+    ctx.prof_begin(kProfSpread, &ev);
+    const unsigned blocks = (unsigned)((size_t)T.ntx * T.nty * T.ntz);
+    spread_tiles_kernel<<<blocks, kSpreadThreads, smem, st>>>(g, T, s.rowstart.p, s.rec_cx.p,
+                                                              s.rec.p, (uint32_t)n, d_out);
+    ++ctx.launches;
+    ctx.prof_end(kProfSpread, ev);
+  }
   IBC_CUDA(cudaGetLastError());
   ++ctx.spread_calls;
 }
@@ -520,13 +597,31 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
                      size_t n, PointScratch& s, double* d_out) {
   if (n == 0) return;
   cudaStream_t st = ctx.stream;
-  sort_points(ctx, g, d_points, n, s);
+  zs::Tiling Z;
+  const bool zsweep = zsweep_tiling(g, true, Z);
+  sort_points(ctx, g, d_points, n, s, zsweep);
   cudaEvent_t ev = nullptr;
-  ctx.prof_begin(kProfInterp, &ev);
-  interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
-                                                        (uint32_t)n, d_out);
-  ++ctx.launches;
-  ctx.prof_end(kProfInterp, ev);
+  if (zsweep) {
+    row_table(ctx, g, n, s);
+    static bool attr_set[64] = {};
+    if (!attr_set[ctx.device & 63]) {
+      IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+      attr_set[ctx.device & 63] = true;
+    }
+    const int use_bulk = ((g.n[0] & 1) == 0 && (reinterpret_cast<uintptr_t>(d_field) & 15) == 0) ? 1 : 0;
+    ctx.prof_begin(kProfInterp, &ev);
+    zs::interp_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem(Z, true), st>>>(
+        g, Z, s.rowstart.p, s.sorted_perm, d_points, d_field, d_out, use_bulk);
+    ++ctx.launches;
+    ctx.prof_end(kProfInterp, ev);
+  } else {
+    ctx.prof_begin(kProfInterp, &ev);
+    interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
+                                                          (uint32_t)n, d_out);
+    ++ctx.launches;
+    ctx.prof_end(kProfInterp, ev);
+  }
   IBC_CUDA(cudaGetLastError());
   ++ctx.interp_calls;
 }

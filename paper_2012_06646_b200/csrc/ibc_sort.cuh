@@ -5,18 +5,19 @@
 // bit-identical to the reference's ws.keys / ws.perm (spread.hpp:100).
 //
 // Structure (Adinets & Merrill, "Onesweep", 2022), B200-sized:
-//  * The per-pass digit histograms of ALL passes come from one read of the
-//    keys, fused into the key-computation kernel (ibc_kernels.cu).
+//  * Keys are < prod(n_a + 2), so only key_bits(grid) bits are sorted, split
+//    into P = ceil(bits / 10) balanced digits of <= 10 bits (25 bits at 256^3
+//    -> 9/8/8: three passes instead of the reference's four 8-bit passes).
+//  * The digit histograms of ALL passes come from one read of the keys,
+//    fused into the key-computation kernel (ibc_kernels.cu).
 //  * One kernel per digit pass.  Each CTA claims a 4096-key tile through an
-//    atomic tile counter (tiles are processed in claim order, so the look-back
-//    always waits on CTAs that are already resident), ranks its keys with
-//    warp ballots (8 __ballot_sync per item build the match mask of equal
-//    digits; rank = popc(mask & lanemask_lt)), publishes its per-digit counts
-//    and resolves its global offsets by decoupled look-back over preceding
-//    tiles, then writes keys/values in digit-sorted runs through shared
-//    memory so the global scatter is coalesced.
-//  * Only ceil(key_bits / 8) passes run: keys are < prod(n_a + 2), e.g.
-//    25 bits for 256^3.
+//    atomic tile counter (so look-back only ever waits on CTAs that are
+//    already resident), ranks its keys with warp ballots (one __ballot_sync
+//    per digit bit builds the equal-digit match mask; rank =
+//    popc(mask & lanemask_lt)), publishes per-digit tile counts and resolves
+//    global offsets by decoupled look-back that polls 8 predecessor tiles
+//    per round trip, then writes keys/values in digit-sorted runs through
+//    shared memory so the global scatter is coalesced.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,17 +25,50 @@
 namespace ibc {
 namespace sort {
 
-constexpr int kRadixBits = 8;
-constexpr int kRadix = 1 << kRadixBits;
-constexpr int kThreads = 256;  // == kRadix: one thread per digit in the scans
+constexpr int kMaxDigitBits = 10;
+constexpr int kMaxRadix = 1 << kMaxDigitBits;
+constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;  // 4096 keys per tile
 constexpr int kWarpSpan = 32 * kItems;    // 512 consecutive keys per warp
+constexpr int kDigitsPerThread = kMaxRadix / kThreads;
+constexpr int kLookback = 8;              // predecessor tiles polled per round trip
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;
-constexpr uint32_t kMaxKeys = kValueMask;  // counts are packed in 30 bits
+constexpr int kMaxPasses = 4;
+
+// Shared memory of one pass (dynamic: > 48 KB).
+struct PassSmem {
+  uint32_t whist[kWarps][kMaxRadix];  // per-warp digit counts, then warp offsets
+  uint32_t keys[kTile];
+  uint32_t vals[kTile];
+  uint32_t tile_start[kMaxRadix];
+  uint32_t gofs[kMaxRadix];
+  uint32_t warp_tmp[kWarps];
+  uint32_t tile_id;
+};
+
+struct DigitPlan {
+  int passes;
+  int shift[kMaxPasses];
+  int bits[kMaxPasses];
+};
+
+inline DigitPlan plan_digits(int key_bits) {
+  DigitPlan p{};
+  p.passes = (key_bits + kMaxDigitBits - 1) / kMaxDigitBits;
+  if (p.passes < 1) p.passes = 1;
+  int shift = 0;
+  for (int i = 0; i < p.passes; ++i) {
+    const int rem = key_bits - shift, left = p.passes - i;
+    p.bits[i] = (rem + left - 1) / left;
+    p.shift[i] = shift;
+    shift += p.bits[i];
+  }
+  return p;
+}
 
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
@@ -45,8 +79,9 @@ __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Exclusive scan of one value per thread over a 256-thread block.
-__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp) {
+// Exclusive scan of one value per thread over a 256-thread block; *total gets the sum.
+__device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s_warp,
+                                                         uint32_t* total = nullptr) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   uint32_t x = v;
 #pragma unroll
@@ -56,32 +91,62 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   }
   if (lane == 31) s_warp[warp] = x;
   __syncthreads();
-  uint32_t base = 0;
+  uint32_t base = 0, all = 0;
 #pragma unroll
-  for (int w = 0; w < kWarps; ++w) base += (w < warp) ? s_warp[w] : 0u;
+  for (int w = 0; w < kWarps; ++w) {
+    const uint32_t s = s_warp[w];
+    base += (w < warp) ? s : 0u;
+    all += s;
+  }
   __syncthreads();
+  if (total) *total = all;
   return base + x - v;
+}
+
+// Decoupled look-back for one digit: sum of the counts of all preceding
+// tiles.  Polls kLookback predecessors per round trip.
+__device__ __forceinline__ uint32_t lookback_digit(const uint32_t* lookback, uint32_t tile,
+                                                   uint32_t radix, uint32_t d) {
+  uint32_t excl = 0;
+  int p = (int)tile - 1;
+  while (p >= 0) {
+    uint32_t v[kLookback];
+#pragma unroll
+    for (int j = 0; j < kLookback; ++j)
+      v[j] = (p - j >= 0) ? ld_acquire(lookback + (size_t)(p - j) * radix + d) : kFlagInc;
+    int consumed = 0;
+    bool done = false;
+#pragma unroll
+    for (int j = 0; j < kLookback; ++j) {
+      if (done || consumed != j) continue;
+      if (p - j < 0) { done = true; continue; }
+      const uint32_t f = v[j] & ~kValueMask;
+      if (f == 0u) continue;  // not yet published: re-poll from here
+      excl += v[j] & kValueMask;
+      ++consumed;
+      if (f == kFlagInc) done = true;
+    }
+    if (done) break;
+    p -= consumed;
+  }
+  return excl;
 }
 
 // One stable digit pass.  vals_in == nullptr means the identity permutation.
 __global__ void __launch_bounds__(kThreads) onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
-    const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ lookback,
+    int bits, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ lookback,
     uint32_t* __restrict__ tile_counter) {
-  __shared__ uint32_t s_whist[kWarps][kRadix];
-  __shared__ uint32_t s_keys[kTile];
-  __shared__ uint32_t s_vals[kTile];
-  __shared__ uint32_t s_tile_start[kRadix];
-  __shared__ uint32_t s_gofs[kRadix];
-  __shared__ uint32_t s_warp[kWarps];
-  __shared__ uint32_t s_tile_id;
-
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PassSmem& S = *reinterpret_cast<PassSmem*>(smem_raw);
+  const uint32_t radix = 1u << bits, mask = radix - 1u;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile_id = atomicAdd(tile_counter, 1u);
-  for (int i = tid; i < kWarps * kRadix; i += kThreads) (&s_whist[0][0])[i] = 0u;
+  if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
+  for (uint32_t i = tid; i < kWarps * radix; i += kThreads)
+    S.whist[i / radix][i % radix] = 0u;
   __syncthreads();
-  const uint32_t tile = s_tile_id;
+  const uint32_t tile = S.tile_id;
   const uint32_t tile_base = tile * (uint32_t)kTile;
   const uint32_t warp_base = tile_base + (uint32_t)warp * kWarpSpan;
 
@@ -98,61 +163,69 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
     }
   }
 
-  // Warp-level stable ranking: items are visited in (j, lane) order, which is
-  // index order, and each equal-digit group is counted through the warp's
-  // private histogram.
+  // Warp-level stable ranking in (j, lane) == index order.
   const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
   for (int j = 0; j < kItems; ++j) {
     const uint32_t idx = warp_base + (uint32_t)(j * 32 + lane);
     const bool valid = idx < n;
-    const uint32_t d = (key[j] >> shift) & (kRadix - 1);
+    const uint32_t d = (key[j] >> shift) & mask;
     uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-    for (int b = 0; b < kRadixBits; ++b) {
+    for (int b = 0; b < bits; ++b) {
       const bool bit = (d >> b) & 1u;
       const uint32_t bb = __ballot_sync(0xffffffffu, bit);
       peers &= bit ? bb : ~bb;
     }
     const uint32_t before = __popc(peers & lt_mask);
     uint32_t base = 0;
-    if (valid) base = s_whist[warp][d];
+    if (valid) base = S.whist[warp][d];
     __syncwarp();
-    if (valid && before == 0) s_whist[warp][d] = base + __popc(peers);
+    if (valid && before == 0) S.whist[warp][d] = base + __popc(peers);
     __syncwarp();
     rank[j] = base + before;
   }
   __syncthreads();
 
-  // Thread t owns digit t: warp-exclusive offsets, tile count, look-back.
-  {
-    const uint32_t d = (uint32_t)tid;
-    uint32_t count = 0;
+  // Digits are owned round-robin by threads: d = tid + 256 * i.
+  uint32_t count[kDigitsPerThread];
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) {
-      const uint32_t c = s_whist[w][d];
-      s_whist[w][d] = count;
-      count += c;
-    }
-    uint32_t* mine = lookback + (size_t)tile * kRadix + d;
-    uint32_t excl = 0;
-    if (tile == 0) {
-      st_release(mine, kFlagInc | count);
-    } else {
-      st_release(mine, kFlagAgg | count);
-      int p = (int)tile - 1;
-      while (true) {
-        const uint32_t v = ld_acquire(lookback + (size_t)p * kRadix + d);
-        if ((v & ~kValueMask) == 0u) continue;  // predecessor not published yet
-        excl += v & kValueMask;
-        if (v & kFlagInc) break;
-        --p;
+  for (int i = 0; i < kDigitsPerThread; ++i) {
+    const uint32_t d = tid + kThreads * i;
+    uint32_t c = 0;
+    if (d < radix) {
+#pragma unroll
+      for (int w = 0; w < kWarps; ++w) {
+        const uint32_t x = S.whist[w][d];
+        S.whist[w][d] = c;
+        c += x;
       }
-      st_release(mine, kFlagInc | (excl + count));
+      st_release(lookback + (size_t)tile * radix + d, (tile == 0 ? kFlagInc : kFlagAgg) | c);
     }
-    const uint32_t start = block_exclusive_scan(count, s_warp);
-    s_tile_start[d] = start;
-    s_gofs[d] = digit_base[d] + excl - start;
+    count[i] = c;
+  }
+  uint32_t excl[kDigitsPerThread];
+#pragma unroll
+  for (int i = 0; i < kDigitsPerThread; ++i) {
+    const uint32_t d = tid + kThreads * i;
+    excl[i] = 0;
+    if (d < radix && tile > 0) {
+      excl[i] = lookback_digit(lookback, tile, radix, d);
+      st_release(lookback + (size_t)tile * radix + d, kFlagInc | (excl[i] + count[i]));
+    }
+  }
+  // Tile-local exclusive scan over digits (digit-major across the threads).
+  uint32_t carry = 0;
+#pragma unroll
+  for (int i = 0; i < kDigitsPerThread; ++i) {
+    const uint32_t d = tid + kThreads * i;
+    if ((uint32_t)(kThreads * i) >= radix) break;  // block-uniform
+    uint32_t total;
+    const uint32_t start = carry + block_exclusive_scan(count[i], S.warp_tmp, &total);
+    carry += total;
+    if (d < radix) {
+      S.tile_start[d] = start;
+      S.gofs[d] = digit_base[d] + excl[i] - start;
+    }
   }
   __syncthreads();
 
@@ -160,30 +233,41 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
   for (int j = 0; j < kItems; ++j) {
     const uint32_t idx = warp_base + (uint32_t)(j * 32 + lane);
     if (idx < n) {
-      const uint32_t d = (key[j] >> shift) & (kRadix - 1);
-      const uint32_t pos = s_tile_start[d] + s_whist[warp][d] + rank[j];
-      s_keys[pos] = key[j];
-      s_vals[pos] = val[j];
+      const uint32_t d = (key[j] >> shift) & mask;
+      const uint32_t pos = S.tile_start[d] + S.whist[warp][d] + rank[j];
+      S.keys[pos] = key[j];
+      S.vals[pos] = val[j];
     }
   }
   __syncthreads();
 
   const uint32_t tile_n = min((uint32_t)kTile, n - tile_base);
   for (uint32_t i = tid; i < tile_n; i += kThreads) {
-    const uint32_t k = s_keys[i];
-    const uint32_t d = (k >> shift) & (kRadix - 1);
-    const uint32_t o = s_gofs[d] + i;
+    const uint32_t k = S.keys[i];
+    const uint32_t o = S.gofs[(k >> shift) & mask] + i;
     keys_out[o] = k;
-    vals_out[o] = s_vals[i];
+    vals_out[o] = S.vals[i];
   }
 }
 
 // Exclusive scan of each pass's global digit histogram (one block per pass).
 __global__ void __launch_bounds__(kThreads) digit_scan(const uint32_t* __restrict__ hist,
-                                                       uint32_t* __restrict__ base) {
+                                                       uint32_t* __restrict__ base,
+                                                       DigitPlan plan) {
   __shared__ uint32_t s_warp[kWarps];
-  const uint32_t v = hist[blockIdx.x * kRadix + threadIdx.x];
-  base[blockIdx.x * kRadix + threadIdx.x] = block_exclusive_scan(v, s_warp);
+  const int p = blockIdx.x;
+  const uint32_t radix = 1u << plan.bits[p];
+  const uint32_t* h = hist + (size_t)p * kMaxRadix;
+  uint32_t* b = base + (size_t)p * kMaxRadix;
+  uint32_t carry = 0;
+  for (uint32_t i0 = 0; i0 < radix; i0 += kThreads) {
+    const uint32_t i = i0 + threadIdx.x;
+    const uint32_t v = i < radix ? h[i] : 0u;
+    uint32_t total;
+    const uint32_t ex = block_exclusive_scan(v, s_warp, &total);
+    if (i < radix) b[i] = carry + ex;
+    carry += total;
+  }
 }
 
 }  // namespace sort

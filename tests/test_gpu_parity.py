@@ -357,3 +357,36 @@ def test_clustered_long_runs():
     _, keys, perm, _ = O.spread_fused(og(g), pts, vals)
     assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm)
     assert O.max_rel_deviation(got.values, want) <= TOL
+
+
+@pytest.mark.parametrize("per", [(True, True, True), (False, True, False), (True, False, True),
+                                 (False, False, False)])
+def test_zsweep_medium_grids_mixed_periodicity(per):
+    # 3-D grids take the z-sweep kernels; ghost cells on closed axes included
+    rng = np.random.default_rng(17 + sum(per))
+    g = ib.StaggeredGrid([24, 20, 37], 0.5, [0.3, 0.0, 0.7], list(per), [0.25, -1.0, 2.0])
+    n = 4000
+    pts, vals = rand_points(g, n, rng), rng.uniform(-1, 1, n)
+    want, keys, perm, run_keys = O.spread_fused(og(g), pts, vals)
+    ws = ib.SpreadWorkspace(n, g)
+    got = ib.spread_fused(pts, vals, g, K, ws, 4)
+    assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm)
+    assert np.array_equal(ws.run_keys, run_keys)
+    assert O.max_rel_deviation(got.values, want) <= TOL
+    e = rng.uniform(-1, 1, g.point_count())
+    assert O.max_rel_deviation(ib.interpolate(ib.GridField(g, e), pts, K), O.interpolate(og(g), e, pts)) <= TOL
+
+
+def test_dense_one_point_per_cell():
+    # weak-scaling density (1 point per cell): long rows, several batch groups per warp
+    rng = np.random.default_rng(23)
+    N = 40
+    g = ib.StaggeredGrid([N] * 3, 0.1, [0.5, 0.5, 0.0], [True] * 3)
+    pts = rng.uniform(0, N * 0.1, (N ** 3, 3))
+    vals = rng.uniform(-1, 1, N ** 3)
+    want = O.spread_serial(og(g), pts, vals)
+    ws = ib.SpreadWorkspace(N ** 3, g)
+    got = ib.spread_fused(pts, vals, g, K, ws, 8)
+    assert O.max_rel_deviation(got.values, want) <= TOL
+    e = rng.uniform(-1, 1, g.point_count())
+    assert O.max_rel_deviation(ib.interpolate(ib.GridField(g, e), pts, K), O.interpolate(og(g), e, pts)) <= TOL
