@@ -36,6 +36,7 @@ __device__ __forceinline__ uint32_t lanemask_le() {
 // ---------------------------------------------------------------- K1
 // Cell key of every point (or, with row_only, its extended row id -- all the
 // interpolation needs) and the digit histograms of every radix pass.
+template <int D>
 __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const double* __restrict__ X,
                                                            uint32_t n, uint32_t* __restrict__ keys,
                                                            uint32_t* __restrict__ hist,
@@ -43,18 +44,22 @@ __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const doub
   __shared__ uint32_t sh[kMaxPasses * sort::kMaxRadix];
   for (int t = threadIdx.x; t < kMaxPasses * sort::kMaxRadix; t += blockDim.x) sh[t] = 0u;
   __syncthreads();
-  const int D = g.dim;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    int c[3] = {0, 0, 0};
+    uint64_t k = 0;
+#pragma unroll
     for (int a = 0; a < D; ++a) {
       double xw;
-      c[a] = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
+      int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
+      if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
+      k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
     }
-    uint32_t key = cell_key(g, c);
+    uint32_t key = (uint32_t)k;
     if (row_only) key /= g.rowdiv;
     keys[i] = key;
-    for (int p = 0; p < plan.passes; ++p)
-      atomicAdd(&sh[p * sort::kMaxRadix + ((key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u))], 1u);
+#pragma unroll
+    for (int p = 0; p < kMaxPasses; ++p)
+      if (p < plan.passes)
+        atomicAdd(&sh[p * sort::kMaxRadix + ((key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u))], 1u);
   }
   __syncthreads();
   for (int t = threadIdx.x; t < plan.passes * sort::kMaxRadix; t += blockDim.x)
@@ -373,14 +378,21 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
   if (!attr_set[ctx.device & 63]) {
     IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)sort_smem()));
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  100));
     attr_set[ctx.device & 63] = true;
   }
 
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
   const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock), 148u * 6u));
-  keys_hist_kernel<<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan,
-                                          row_only ? 1 : 0);
+  const int ro = row_only ? 1 : 0;
+  if (g.dim == 3)
+    keys_hist_kernel<3><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);
+  else if (g.dim == 2)
+    keys_hist_kernel<2><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);
+  else
+    keys_hist_kernel<1><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);
   ++ctx.launches;
   ctx.prof_end(kProfKeys, ev);
 
@@ -422,32 +434,37 @@ void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
   ctx.prof_end(kProfRows, ev);
 }
 
+size_t zsweep_smem_bytes(const zs::Tiling& T, bool interp) {
+  return interp ? (size_t)4 * (T.ty + 5) * T.nxp * sizeof(double)
+                : ((size_t)4 * T.ty * T.nxp + zs::kSThreads) * sizeof(double);
+}
+
 // z-sweep tiling for 3-D grids with rows short enough for shared memory.
+// spread: window of 4 planes x ty rows (small, ~6 CTAs / SM);
+// interp: window of 4 planes x (ty + 5) rows.
 bool zsweep_tiling(const DevGrid& g, bool interp, zs::Tiling& T) {
   if (g.dim != 3) return false;
   const int nx = g.n[0];
   T.nxp = nx + zs::kPadL + zs::kPadR;
   if (T.nxp & 1) T.nxp += 1;
   const size_t row_bytes = (size_t)T.nxp * 8;
-  const size_t budget = interp ? 100 * 1024 : 72 * 1024;
-  // spread: 4 planes x ty rows; interp: 4 planes x (ty + 5) rows
+  const size_t budget = interp ? 100 * 1024 : 36 * 1024;
+  const int extra = interp ? 5 : 0;
   int ty = 16;
-  while (ty > 1 && 4 * (size_t)(ty + (interp ? 5 : 0)) * row_bytes > budget) --ty;
-  if (4 * (size_t)(ty + (interp ? 5 : 0)) * row_bytes > budget) return false;
+  while (ty > 1 && 4 * (size_t)(ty + extra) * row_bytes > budget) --ty;
+  if (4 * (size_t)(ty + extra) * row_bytes > 160 * 1024) return false;
   ty = std::min(ty, g.n[1]);
   if (ty < 1 || ty + 5 > zs::kMaxRows) return false;
   T.ty = ty;
   T.nty = (g.n[1] + ty - 1) / ty;
-  // Enough CTAs for ~3 per SM, but z chunks of at least 4 planes.
-  int zc = (int)std::max<long>(4, ((long)g.n[2] * T.nty) / (148L * 3));
+  const size_t smem = zsweep_smem_bytes(T, interp);
+  const long per_sm = std::max<long>(1, std::min<long>(interp ? 8 : 16, (220L * 1024) / (long)smem));
+  // z chunks of >= 4 planes, enough CTAs to fill every SM about 1.5 times.
+  int zc = (int)std::max<long>(4, ((long)g.n[2] * T.nty * 2) / (148L * per_sm * 3));
   zc = std::min(zc, g.n[2]);
   T.zc = zc;
   T.nzc = (g.n[2] + zc - 1) / zc;
   return true;
-}
-
-size_t zsweep_smem(const zs::Tiling& T, bool interp) {
-  return (size_t)4 * (T.ty + (interp ? 5 : 0)) * T.nxp * sizeof(double);
 }
 
 SpreadTiling choose_tiling(const DevGrid& g) {
@@ -561,6 +578,10 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                                   160 * 1024));
     IBC_CUDA(cudaFuncSetAttribute(zs::spread_zsweep_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    IBC_CUDA(cudaFuncSetAttribute(zs::spread_zsweep_kernel,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr_set[ctx.device & 63] = true;
@@ -568,7 +589,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   zs::Tiling Z;
   if (zsweep_tiling(g, false, Z)) {
     ctx.prof_begin(kProfSpread, &ev);
-    zs::spread_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem(Z, false), st>>>(
+    zs::spread_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kSThreads, zsweep_smem_bytes(Z, false), st>>>(
         g, Z, s.rowstart.p, s.sorted_keys, s.sorted_perm, d_points, d_values, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
@@ -611,7 +632,7 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
     }
     const int use_bulk = ((g.n[0] & 1) == 0 && (reinterpret_cast<uintptr_t>(d_field) & 15) == 0) ? 1 : 0;
     ctx.prof_begin(kProfInterp, &ev);
-    zs::interp_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem(Z, true), st>>>(
+    zs::interp_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem_bytes(Z, true), st>>>(
         g, Z, s.rowstart.p, s.sorted_perm, d_points, d_field, d_out, use_bulk);
     ++ctx.launches;
     ctx.prof_end(kProfInterp, ev);

@@ -70,13 +70,16 @@ inline DigitPlan plan_digits(int key_bits) {
   return p;
 }
 
+// The look-back words carry only their own payload (no other data is
+// published through them), so relaxed gpu-scope accesses suffice: they are
+// served by L2 without the L1 invalidation (CCTL.IVALL) an acquire costs.
 __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 __device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Exclusive scan of one value per thread over a 256-thread block; *total gets the sum.
@@ -143,8 +146,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
   const uint32_t radix = 1u << bits, mask = radix - 1u;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
-  for (uint32_t i = tid; i < kWarps * radix; i += kThreads)
-    S.whist[i / radix][i % radix] = 0u;
+  for (uint32_t i = tid; i < kWarps * radix; i += kThreads) S.whist[i >> bits][i & mask] = 0u;
   __syncthreads();
   const uint32_t tile = S.tile_id;
   const uint32_t tile_base = tile * (uint32_t)kTile;

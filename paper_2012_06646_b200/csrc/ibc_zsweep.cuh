@@ -84,20 +84,38 @@ __device__ __forceinline__ uint32_t row_id(const DevGrid& g, int cyw, int czw) {
 
 // One staged spread point held by a lane.
 struct SrcPoint {
-  int cx, cyu, rank;
+  int cx, cyu, rank, run_after;  // run_after: following lanes in the same cell (heads only)
   bool valid;
   double gx[4], wy[4], wz[4];
 };
 
+constexpr int kSThreads = 128;  // spread CTA: 4 warps, small window -> 6 CTAs / SM
+constexpr int kSWarps = kSThreads / 32;
+
+// Fold the periodic x pad of one window row and store it (x in [0, nx)).
+__device__ __forceinline__ double folded(const double* row, int x, int nx, bool periodic) {
+  double v = row[x];
+  if (periodic) {
+    if (nx >= 4) {
+      if (x < 2) v += row[x + nx];
+      if (x >= nx - 3) v += row[x - nx];
+    } else {
+      for (int p = x - nx; p >= -3; p -= nx) v += row[p];
+      for (int p = x + nx; p <= nx + 1; p += nx) v += row[p];
+    }
+  }
+  return v;
+}
+
 // ------------------------------------------------------------------ spread
-__global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
+__global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
     DevGrid g, Tiling T, const uint32_t* __restrict__ rowstart,
     const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ perm,
     const double* __restrict__ X, const double* __restrict__ G, double* __restrict__ out) {
-  extern __shared__ __align__(16) double win[];  // [4][ty][nxp]
+  extern __shared__ __align__(16) double win[];  // [4][ty][nxp], then one dummy slot per thread
   __shared__ uint32_t s_rb[kMaxRows];
   __shared__ uint32_t s_pref[kMaxRows + 1];
-  __shared__ int s_wlo[kWarps + 1];
+  __shared__ int s_wlo[kSWarps + 1];
   __shared__ int s_groups;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -108,8 +126,11 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
   const int rows = y1 - y0;
   const int srows = rows + 3;  // unwrapped source rows y0-1 .. y1+1
   const int plane = T.ty * T.nxp;
+  double* dummy = win + 4 * plane + tid;  // sink for lanes with nothing to add
   const uint32_t le = lanemask_le();
-  for (int i = tid; i < 4 * plane; i += kThreads) win[i] = 0.0;
+  const bool px = g.periodic[0] != 0;
+  const bool vec = (nx & 1) == 0;  // double2 write-back (row bodies are 16-byte aligned)
+  for (int i = tid; i < 4 * plane + kSThreads; i += kSThreads) win[i] = 0.0;
 
   for (int s = z0 - 1; s <= z1 + 2; ++s) {
     // (a) Target plane s-3 is complete (its last source plane was s-1):
@@ -118,20 +139,27 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
     const bool flush = t >= z0 && t < z1;
     if (flush) {
       const double* wp = win + (t & 3) * plane;
-      for (int r = 0; r < rows; ++r) {
-        const double* row = wp + r * T.nxp + kPadL;
-        double* orow = out + ((size_t)t * ny + (size_t)(y0 + r)) * nx;
-        for (int x = tid; x < nx; x += kThreads) {
-          double v = row[x];
-          if (g.periodic[0]) {
-            for (int p = x - nx; p >= -3; p -= nx) v += row[p];
-            for (int p = x + nx; p <= nx + 1; p += nx) v += row[p];
+      if (vec) {
+        const int half = nx >> 1;
+        for (int i = tid; i < rows * half; i += kSThreads) {
+          const int r = i / half, x = 2 * (i - r * half);
+          const double* row = wp + r * T.nxp + kPadL;
+          double2 v = *reinterpret_cast<const double2*>(row + x);
+          if (px) {
+            v.x = folded(row, x, nx, true);
+            v.y = folded(row, x + 1, nx, true);
           }
-          orow[x] = v;
+          *reinterpret_cast<double2*>(out + ((size_t)t * ny + (size_t)(y0 + r)) * nx + x) = v;
+        }
+      } else {
+        for (int r = 0; r < rows; ++r) {
+          const double* row = wp + r * T.nxp + kPadL;
+          double* orow = out + ((size_t)t * ny + (size_t)(y0 + r)) * nx;
+          for (int x = tid; x < nx; x += kSThreads) orow[x] = folded(row, x, nx, px);
         }
       }
     }
-    // Source-row table of plane s.
+    // Source-row table of plane s (warp 0).
     const bool src_plane = g.periodic[2] ? true : (s >= -1 && s <= nz);
     const bool sweep = s <= z1 + 1 && src_plane;
     if (warp == 0) {
@@ -156,27 +184,25 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
         if (lane >= o) incl += y;
       }
       const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      const uint32_t excl = incl - len;
       if (lane < kMaxRows) {
         s_rb[lane] = rb;
-        s_pref[lane] = incl - len;
+        s_pref[lane] = excl;
       }
       if (lane == 0) s_pref[kMaxRows] = total;
       // Row-aligned chunks: warp w owns rows [wlo[w], wlo[w+1]); a row is
       // never split across warps.
-      const uint32_t excl = incl - len;
       int lo = srows;
-      for (int w = 0; w <= kWarps; ++w) {
-        const uint32_t target = (uint32_t)(((uint64_t)total * w) / kWarps);
+      for (int w = 0; w <= kSWarps; ++w) {
+        const uint32_t target = (uint32_t)(((uint64_t)total * w) / kSWarps);
         const uint32_t m = __ballot_sync(0xffffffffu, lane < srows && excl >= target);
-        const int j = (w == kWarps || m == 0u) ? srows : __ffs(m) - 1;
+        const int j = (w == kSWarps || m == 0u) ? srows : __ffs(m) - 1;
         if (lane == w) lo = j;
       }
-      if (lane <= kWarps) s_wlo[lane] = lo;
-    }
-    __syncthreads();
-    if (warp == 0) {
+      if (lane <= kSWarps) s_wlo[lane] = lo;
+      __syncwarp();
       int gcount = 0;
-      if (lane < kWarps) {
+      if (lane < kSWarps) {
         const int a = s_wlo[lane], b = s_wlo[lane + 1];
         const uint32_t pts = (b > a) ? (s_pref[b] - s_pref[a]) : 0u;
         gcount = (int)((pts + 32 * kBatches - 1) / (32 * kBatches));
@@ -185,19 +211,17 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
       for (int o = 16; o > 0; o >>= 1) gcount = max(gcount, __shfl_down_sync(0xffffffffu, gcount, o));
       if (lane == 0) s_groups = gcount;
     }
+    __syncthreads();
     // (b) The flushed slot becomes plane s+1's slot: clear it.
     if (flush) {
-      double* wp = win + (t & 3) * plane;
-      for (int i = tid; i < plane; i += kThreads) wp[i] = 0.0;
+      double2* wp = reinterpret_cast<double2*>(win + (t & 3) * plane);
+      for (int i = tid; i < (plane >> 1); i += kSThreads) wp[i] = make_double2(0.0, 0.0);
     }
-    __syncthreads();
     const int groups = s_groups;
     const int wlo = s_wlo[warp], whi = s_wlo[warp + 1];
     const uint32_t pbeg = s_pref[wlo], pend = s_pref[whi];
-    if (groups == 0) {
-      __syncthreads();  // the tables are rebuilt next step
-      continue;
-    }
+    __syncthreads();
+    if (groups == 0) continue;  // the next table build happens after a barrier
 
     for (int gi = 0; gi < groups; ++gi) {
       // (c) Stage up to kBatches x 32 points of this warp's rows into registers.
@@ -209,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
         SrcPoint& q = P[b];
         q.valid = p < pend;
         q.cx = 0;
-        q.cyu = 0;
+        q.cyu = y0;
         uint32_t key = 0xffffffffu;
         if (q.valid) {
           int j = wlo;
@@ -224,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
             double xw;
             const int c = cell_of(g, a, __ldg(X + (size_t)i * 3 + a), &xw);
             cosine_weights(displacement(g, a, xw, c), g.inv_h, w[a]);
-            if (a == 0) q.cx = g.periodic[0] ? wrap_cell(c, nx) : c;
+            if (a == 0) q.cx = px ? wrap_cell(c, nx) : c;
           }
           const double gv = __ldg(G + i);
 #pragma unroll
@@ -237,43 +261,45 @@ __global__ void __launch_bounds__(kThreads) spread_zsweep_kernel(
 #pragma unroll
           for (int k = 0; k < 4; ++k) q.gx[k] = q.wy[k] = q.wz[k] = 0.0;
         }
-        // Rank among equal-cell lanes (adjacent: keys are sorted).
+        // Points sharing a cell are adjacent lanes (keys are sorted): the
+        // head lane adds its followers' contributions before touching memory.
         const uint32_t pkey = __shfl_up_sync(0xffffffffu, key, 1);
         const bool head = q.valid && (lane == 0 || pkey != key);
         const uint32_t hm = __ballot_sync(0xffffffffu, head);
-        q.rank = q.valid ? lane - (31 - __clz(hm & le)) : 0;
-        maxrank[b] = __reduce_max_sync(0xffffffffu, (unsigned)q.rank);
+        const uint32_t vm = __ballot_sync(0xffffffffu, q.valid);
+        q.rank = q.valid ? lane - (31 - __clz(hm & le)) : 1;
+        const uint32_t later = hm & ~le;
+        const int next = later ? __ffs(later) - 1 : __popc(vm);
+        q.run_after = (head ? next - lane - 1 : 0);
+        maxrank[b] = __reduce_max_sync(0xffffffffu, (unsigned)q.run_after);
       }
-      // (d) Four sigma_y phases.
+      // (d) Four sigma_y phases; within a phase distinct source rows hit
+      //     distinct target rows.
 #pragma unroll
       for (int sy = -2; sy <= 1; ++sy) {
 #pragma unroll
         for (int b = 0; b < kBatches; ++b) {
           const SrcPoint& q = P[b];
           const int ty = q.cyu + sy;
-          const bool yok = q.valid && ty >= y0 && ty < y1;
-          if (__ballot_sync(0xffffffffu, yok) == 0u) continue;
-          double* rowp = win + (ty - y0) * T.nxp + q.cx + (kPadL - 2);
+          const bool yok = q.valid && q.rank == 0 && ty >= y0 && ty < y1;
+          if (__ballot_sync(0xffffffffu, q.valid && ty >= y0 && ty < y1) == 0u) continue;
+          const int rowoff = yok ? (ty - y0) * T.nxp + q.cx + (kPadL - 2) : 0;
 #pragma unroll
           for (int sz = -2; sz <= 1; ++sz) {
             const int tz = s + sz;
             if (tz < z0 || tz >= z1) continue;  // warp-uniform
-            double* p = rowp + (tz & 3) * plane;
+            double* base = win + (tz & 3) * plane + rowoff;
             const double a = q.wy[sy + 2] * q.wz[sz + 2];
-            if (maxrank[b] == 0) {
 #pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                if (yok) p[k] += q.gx[k] * a;
-                __syncwarp();
+            for (int k = 0; k < 4; ++k) {
+              double v = q.gx[k] * a;
+              for (int j = 1; j <= maxrank[b]; ++j) {
+                const double w = __shfl_down_sync(0xffffffffu, v, j);
+                if (j <= q.run_after) v += w;
               }
-            } else {
-              for (int rr = 0; rr <= maxrank[b]; ++rr) {
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                  if (yok && q.rank == rr) p[k] += q.gx[k] * a;
-                  __syncwarp();
-                }
-              }
+              double* dst = yok ? base + k : dummy;
+              *dst += v;
+              __syncwarp();
             }
           }
         }
@@ -310,7 +336,7 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t parity[4] = {0, 0, 0, 0};
+  uint32_t parity = 0;  // bit i: phase parity of s_bar[i]
 
   // Fill window slot for field plane t (unwrapped).
   auto load_plane = [&](int t) {
@@ -359,8 +385,8 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
   auto wait_plane = [&](int t) {
     const bool zin = g.periodic[2] || (t >= 0 && t < nz);
     if (use_bulk && zin) {
-      mbar_wait(&s_bar[t & 3], parity[t & 3]);
-      parity[t & 3] ^= 1u;
+      mbar_wait(&s_bar[t & 3], (parity >> (t & 3)) & 1u);
+      parity ^= 1u << (t & 3);
     }
   };
 
