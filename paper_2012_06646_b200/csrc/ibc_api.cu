@@ -463,6 +463,11 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
   });
 }
 
+// Debug hook (not part of ibcuda.h): clock64 timeline of one z-sweep CTA.
+int ibc_debug_zsweep_trace(int block, long long* out) {
+  return (int)ibc::debug_zsweep_trace(block, out);
+}
+
 uint64_t ibc_delta_evaluations(void) { return g_delta_evaluations.load(std::memory_order_relaxed); }
 void ibc_reset_delta_evaluations(void) { g_delta_evaluations.store(0, std::memory_order_relaxed); }
 

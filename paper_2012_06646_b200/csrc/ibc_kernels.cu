@@ -647,6 +647,16 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
   ++ctx.interp_calls;
 }
 
+int debug_zsweep_trace(int block, long long* out) {
+  if (out) {
+    cudaDeviceSynchronize();
+    return (int)cudaMemcpyFromSymbol(out, zs::g_trace, sizeof(long long) * 2 * 64 * 8);
+  }
+  long long zero[2 * 64 * 8] = {};
+  cudaMemcpyToSymbol(zs::g_trace, zero, sizeof(zero));
+  return (int)cudaMemcpyToSymbol(zs::g_trace_block, &block, sizeof(int));
+}
+
 size_t read_run_count(Context& ctx, PointScratch& s) {
   uint32_t q = 0;
   IBC_CUDA(cudaMemcpyAsync(&q, s.counters.p + kMaxPasses, 4, cudaMemcpyDeviceToHost, ctx.stream));

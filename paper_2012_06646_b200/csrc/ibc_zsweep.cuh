@@ -43,6 +43,16 @@ struct Tiling {
   int ty, zc, nty, nzc, nxp;  // nxp = n0 + kPadL + kPadR (even)
 };
 
+// Debug timeline (clock64 per step and phase, CTA `trace_block`, thread 0).
+__device__ long long g_trace[2][64][8];
+__device__ int g_trace_block = -1;
+#define ZS_TRACE(which, step, slot)                                               \
+  do {                                                                            \
+    if ((int)blockIdx.x == g_trace_block && threadIdx.x == 0 && (step) >= 0 &&   \
+        (step) < 64)                                                              \
+      g_trace[which][step][slot] = clock64();                                     \
+  } while (0)
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -133,6 +143,8 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
   for (int i = tid; i < 4 * plane + kSThreads; i += kSThreads) win[i] = 0.0;
 
   for (int s = z0 - 1; s <= z1 + 2; ++s) {
+    const int step = s - (z0 - 1);
+    ZS_TRACE(0, step, 0);
     // (a) Target plane s-3 is complete (its last source plane was s-1):
     //     fold the periodic x pad back and write it to HBM once.
     const int t = s - 3;
@@ -159,6 +171,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
         }
       }
     }
+    ZS_TRACE(0, step, 1);
     // Source-row table of plane s (warp 0).
     const bool src_plane = g.periodic[2] ? true : (s >= -1 && s <= nz);
     const bool sweep = s <= z1 + 1 && src_plane;
@@ -212,6 +225,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
       if (lane == 0) s_groups = gcount;
     }
     __syncthreads();
+    ZS_TRACE(0, step, 2);
     // (b) The flushed slot becomes plane s+1's slot: clear it.
     if (flush) {
       double2* wp = reinterpret_cast<double2*>(win + (t & 3) * plane);
@@ -221,6 +235,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
     const int wlo = s_wlo[warp], whi = s_wlo[warp + 1];
     const uint32_t pbeg = s_pref[wlo], pend = s_pref[whi];
     __syncthreads();
+    ZS_TRACE(0, step, 3);
     if (groups == 0) continue;  // the next table build happens after a barrier
 
     for (int gi = 0; gi < groups; ++gi) {
@@ -273,6 +288,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
         q.run_after = (head ? next - lane - 1 : 0);
         maxrank[b] = __reduce_max_sync(0xffffffffu, (unsigned)q.run_after);
       }
+      ZS_TRACE(0, step, 4);
       // (d) Four sigma_y phases; within a phase distinct source rows hit
       //     distinct target rows.
 #pragma unroll
@@ -304,6 +320,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
           }
         }
         __syncthreads();
+        ZS_TRACE(0, step, 5 + (sy + 2 < 3 ? sy + 2 : 2));
       }
     }
   }
@@ -395,6 +412,8 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
   __syncthreads();
 
   for (int s = hz0; s < hz1; ++s) {
+    const int step = s - hz0;
+    ZS_TRACE(1, step, 0);
     // Points homed in plane s, rows [hy0, hy1): one contiguous sorted range.
     const int szw = g.periodic[2] ? wrap_cell(s, nz) : s;
     const uint32_t rb = __ldg(rowstart + row_id(g, hy0, szw));
@@ -427,11 +446,16 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
       }
       out[i] = acc * g.hd;
     }
+    ZS_TRACE(1, step, 1);
     if (s + 1 < hz1) {
       __syncthreads();  // everyone is done with plane s-2
+      ZS_TRACE(1, step, 2);
       load_plane(s + 2);
+      ZS_TRACE(1, step, 3);
       wait_plane(s + 2);
+      ZS_TRACE(1, step, 4);
       __syncthreads();
+      ZS_TRACE(1, step, 5);
     }
   }
 }
