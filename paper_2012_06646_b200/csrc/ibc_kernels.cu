@@ -36,6 +36,26 @@ __device__ __forceinline__ uint32_t lanemask_le() {
 // ---------------------------------------------------------------- K1
 // Cell key of every point (or, with row_only, its extended row id -- all the
 // interpolation needs) and the digit histograms of every radix pass.
+constexpr int kKeysUnroll = 4;
+
+template <int D>
+__device__ __forceinline__ uint32_t key_of(const DevGrid& g, const double* x, bool row_only) {
+  uint64_t k = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double xw;
+    int c = cell_of(g, a, x[a], &xw);
+    if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
+    k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
+  }
+  uint32_t key = (uint32_t)k;
+  if (row_only) key /= g.rowdiv;
+  return key;
+}
+
+// A few hundred resident CTAs, kKeysUnroll points per thread per round with
+// all coordinate loads issued first; per-CTA shared histograms flushed with
+// one global atomic per non-empty bin.
 template <int D>
 __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const double* __restrict__ X,
                                                            uint32_t n, uint32_t* __restrict__ keys,
@@ -44,22 +64,27 @@ __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const doub
   __shared__ uint32_t sh[kMaxPasses * sort::kMaxRadix];
   for (int t = threadIdx.x; t < kMaxPasses * sort::kMaxRadix; t += blockDim.x) sh[t] = 0u;
   __syncthreads();
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    uint64_t k = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * kKeysUnroll) {
+    double x[kKeysUnroll][D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double xw;
-      int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
-      if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
-      k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
+    for (int u = 0; u < kKeysUnroll; ++u) {
+      const uint32_t i = i0 + u * stride;
+#pragma unroll
+      for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
     }
-    uint32_t key = (uint32_t)k;
-    if (row_only) key /= g.rowdiv;
-    keys[i] = key;
 #pragma unroll
-    for (int p = 0; p < kMaxPasses; ++p)
-      if (p < plan.passes)
-        atomicAdd(&sh[p * sort::kMaxRadix + ((key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u))], 1u);
+    for (int u = 0; u < kKeysUnroll; ++u) {
+      const uint32_t i = i0 + u * stride;
+      if (i >= n) break;
+      const uint32_t key = key_of<D>(g, x[u], row_only != 0);
+      keys[i] = key;
+#pragma unroll
+      for (int p = 0; p < kMaxPasses; ++p)
+        if (p < plan.passes)
+          atomicAdd(&sh[p * sort::kMaxRadix + ((key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u))],
+                    1u);
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < plan.passes * sort::kMaxRadix; t += blockDim.x)
@@ -385,7 +410,7 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
 
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
-  const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock), 148u * 6u));
+  const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock * kKeysUnroll), 148u * 2u));
   const int ro = row_only ? 1 : 0;
   if (g.dim == 3)
     keys_hist_kernel<3><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);

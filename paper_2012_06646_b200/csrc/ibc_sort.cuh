@@ -15,7 +15,7 @@
 //    already resident), ranks its keys with warp ballots (one __ballot_sync
 //    per digit bit builds the equal-digit match mask; rank =
 //    popc(mask & lanemask_lt)), publishes per-digit tile counts and resolves
-//    global offsets by decoupled look-back that polls 8 predecessor tiles
+//    global offsets by decoupled look-back that polls 32 predecessor tiles
 //    per round trip, then writes keys/values in digit-sorted runs through
 //    shared memory so the global scatter is coalesced.
 #pragma once
@@ -33,7 +33,7 @@ constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;  // 4096 keys per tile
 constexpr int kWarpSpan = 32 * kItems;    // 512 consecutive keys per warp
 constexpr int kDigitsPerThread = kMaxRadix / kThreads;
-constexpr int kLookback = 8;              // predecessor tiles polled per round trip
+constexpr int kLookback = 32;             // predecessor tiles polled per round trip
 constexpr uint32_t kFlagAgg = 1u << 30;
 constexpr uint32_t kFlagInc = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1;

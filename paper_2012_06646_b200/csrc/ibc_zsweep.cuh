@@ -355,48 +355,62 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
   __syncthreads();
   uint32_t parity = 0;  // bit i: phase parity of s_bar[i]
 
-  // Fill window slot for field plane t (unwrapped).
+  // Fill window slot for field plane t (unwrapped): row bodies by TMA bulk
+  // copy (or plain loads), zero rows outside closed axes.
   auto load_plane = [&](int t) {
     double* wp = fwin + (t & 3) * plane;
     const bool zin = g.periodic[2] || (t >= 0 && t < nz);
     const int tw = g.periodic[2] ? wrap_cell(t, nz) : t;
-    // Row bodies: TMA bulk copies when aligned, plain loads otherwise.
-    if (use_bulk && zin) {
-      if (tid == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        uint32_t bytes = 0;
-        for (int r = 0; r < frows; ++r) {
-          const int yu = hy0 - 2 + r;
-          if (g.periodic[1] || (yu >= 0 && yu < ny)) bytes += (uint32_t)nx * 8u;
-        }
-        mbar_expect_tx(&s_bar[t & 3], bytes);
-        for (int r = 0; r < frows; ++r) {
-          const int yu = hy0 - 2 + r;
-          if (!(g.periodic[1] || (yu >= 0 && yu < ny))) continue;
-          const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
-          bulk_g2s(wp + r * T.nxp + kPadL, field + ((size_t)tw * ny + yw) * nx, (uint32_t)nx * 8u,
-                   &s_bar[t & 3]);
-        }
+    if (use_bulk && zin && tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      uint32_t bytes = 0;
+      for (int r = 0; r < frows; ++r) {
+        const int yu = hy0 - 2 + r;
+        if (g.periodic[1] || (yu >= 0 && yu < ny)) bytes += (uint32_t)nx * 8u;
+      }
+      mbar_expect_tx(&s_bar[t & 3], bytes);
+      for (int r = 0; r < frows; ++r) {
+        const int yu = hy0 - 2 + r;
+        if (!(g.periodic[1] || (yu >= 0 && yu < ny))) continue;
+        const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
+        bulk_g2s(wp + r * T.nxp + kPadL, field + ((size_t)tw * ny + yw) * nx, (uint32_t)nx * 8u,
+                 &s_bar[t & 3]);
       }
     }
-    for (int r = 0; r < frows; ++r) {
+    // Everything the bulk copies do not write: all of each row without TMA,
+    // else only the x pads (zero here; periodic pads are copied from the
+    // row body once it has landed, see fill_pads).
+    const int total = frows * T.nxp;
+    for (int e = tid; e < total; e += kThreads) {
+      const int r = e / T.nxp, xi = e - r * T.nxp;
       const int yu = hy0 - 2 + r;
       const bool yin = g.periodic[1] || (yu >= 0 && yu < ny);
-      const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
-      double* row = wp + r * T.nxp;
-      const double* src = field + ((size_t)tw * ny + yw) * nx;
-      const bool body_bulk = use_bulk && zin && yin;
-      for (int xi = tid; xi < T.nxp; xi += kThreads) {
-        const int x = xi - kPadL;
-        const bool body = x >= 0 && x < nx;
-        if (body && body_bulk) continue;
-        double v = 0.0;
-        if (zin && yin) {
-          if (body) v = __ldg(src + x);
-          else if (g.periodic[0]) v = __ldg(src + wrap_cell(x, nx));
-        }
-        row[xi] = v;
+      const int x = xi - kPadL;
+      const bool body = x >= 0 && x < nx;
+      if (use_bulk && zin && yin && (body || g.periodic[0])) continue;  // TMA / fill_pads
+      double v = 0.0;
+      if (!use_bulk && zin && yin) {
+        const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
+        const double* src = field + ((size_t)tw * ny + yw) * nx;
+        if (body) v = __ldg(src + x);
+        else if (g.periodic[0]) v = __ldg(src + wrap_cell(x, nx));
       }
+      wp[e] = v;
+    }
+  };
+  // Periodic x pads of bulk-copied rows, from the landed row bodies.
+  auto fill_pads = [&](int t) {
+    const bool zin = g.periodic[2] || (t >= 0 && t < nz);
+    if (!(use_bulk && zin && g.periodic[0])) return;
+    double* wp = fwin + (t & 3) * plane;
+    const int npad = kPadL + (T.nxp - kPadL - nx);
+    for (int e = tid; e < frows * npad; e += kThreads) {
+      const int r = e / npad, j = e - r * npad;
+      const int yu = hy0 - 2 + r;
+      if (!(g.periodic[1] || (yu >= 0 && yu < ny))) continue;
+      const int xi = j < kPadL ? j : nx + j;  // padded index
+      double* row = wp + r * T.nxp;
+      row[xi] = row[kPadL + wrap_cell(xi - kPadL, nx)];
     }
   };
   auto wait_plane = [&](int t) {
@@ -409,6 +423,7 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
 
   for (int t = hz0 - 2; t <= hz0 + 1; ++t) load_plane(t);
   for (int t = hz0 - 2; t <= hz0 + 1; ++t) wait_plane(t);
+  for (int t = hz0 - 2; t <= hz0 + 1; ++t) fill_pads(t);
   __syncthreads();
 
   for (int s = hz0; s < hz1; ++s) {
@@ -453,6 +468,7 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
       load_plane(s + 2);
       ZS_TRACE(1, step, 3);
       wait_plane(s + 2);
+      fill_pads(s + 2);
       ZS_TRACE(1, step, 4);
       __syncthreads();
       ZS_TRACE(1, step, 5);
