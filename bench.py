@@ -1,0 +1,340 @@
+#!/usr/bin/env python
+"""IB spread + interpolate benchmark (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one scalar spread of 2^20 forces at the predicted positions X*
+plus one scalar interpolation of a 256^3 field at X^n (BASELINE config 2,
+the configuration the metric is quoted on), on the periodic MAC z-grid
+(alpha = (1/2, 1/2, 0)) with the 4-point cosine kernel, FP64.
+metric = Lagrangian points / s.  Inputs are synthetic (ib::bench::
+scatter_points, seed 1; X* = X^n + U[-0.1h, 0.1h]^3).
+
+Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA
+events on the operators' stream with a 256 MiB L2 flush between steps
+(outside the events); barrier + synchronize on both sides; max over ranks.
+Under torchrun (N > 1) every rank runs its own config-2 replica (weak
+scaling; each rank's slab of a 256 x 256 x 256N grid holds the same load).
+
+--impl reference times the reference's own OpenMP CPU path (ib::spread_fused
++ ib::interpolate compiled from the reference headers into oracle/_ref) on
+all host threads, same workload and metric; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "Lagrangian points/sec for spread+interpolate per step, %HBM roofline, 1/2/4/8 B200"
+UNIT = "points/s"
+WORKLOAD = ("config 2: 2^20 uniform random points (scatter_points seed 1) on a 256^3 periodic "
+            "grid, 4-point cosine (Peskin 2002) kernel, one scalar spread (at X*) + one scalar "
+            "interpolation (at X^n) per step, FP64")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clocks and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+    }
+
+    def __init__(self, device: int, period: float = 0.005):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_reference_steps(data, steps, warmup, threads):
+    """Reference ib::spread_fused + ib::interpolate (oracle/_ref), per-step seconds."""
+    import numpy as np
+
+    import oracle as O
+
+    N = data["N"]
+    g = O.make_grid([N] * 3, data["h"], [0.5, 0.5, 0.0], [1, 1, 1])
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    ts, ti = O.ref_time_step(g, data["x_star"], data["values"], data["x_n"], data["field"],
+                             threads, warmup + steps)
+    return (np.asarray(ts) + np.asarray(ti))[warmup:]
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    from paper_2012_06646_b200 import synth
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libibref.so not built (reference headers absent at build)"}))
+        return
+    data = synth.config2()
+    threads = host_threads()
+    # One step of the full workload takes ~1-2 s on 8 cores: bound the run to a
+    # few minutes by capping the number of measured steps.
+    steps = min(args.steps, 20)
+    warm = min(args.warmup, 1)
+    t = cpu_reference_steps(data, steps, warm, threads)
+    per = float(statistics.median(t))
+    value = data["n"] / per
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(t), "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_points": data["n"], "grid": [data["N"]] * 3,
+                   "parallelism": f"OpenMP {threads} threads (rank 0 only)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": f"{len(t)} full config-2 steps (2^20 points, 256^3), median"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2012_06646_b200 import ib, synth
+    from paper_2012_06646_b200.device import DeviceOperators
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    data = synth.config2(seed_offset=0)
+    n, N, h = data["n"], data["N"], data["h"]
+    grid = ib.StaggeredGrid([N] * 3, h, [0.5, 0.5, 0.0], [True] * 3)
+    xs = torch.tensor(data["x_star"], device=dev)
+    xn = torch.tensor(data["x_n"], device=dev)
+    gv = torch.tensor(data["values"], device=dev)
+    fe = torch.tensor(data["field"], device=dev)
+    ell = torch.empty(N ** 3, dtype=torch.float64, device=dev)
+    E = torch.empty(n, dtype=torch.float64, device=dev)
+    ops = DeviceOperators(local)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        ops.spread(xs, gv, grid, out=ell)
+        ops.interpolate(fe, xn, grid, out=E)
+
+    for i in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ops.launches
+    with ClockSampler(local) as clk:
+        for i in range(K):
+            flush.fill_(float(i))  # evict L2 (256 MiB > 126 MB) outside the events
+            ev[i][0].record()
+            step()
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    launches = ops.launches - launches0
+    total_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_per_step = total_ms / K
+    value = world * n * K / (total_ms * 1e-3)
+
+    # Per-kernel device times (CUDA events on the operators' stream), separate pass.
+    P = max(3, min(K, 10))
+    ops.context.set_profiling(True)
+    ops.context.reset_profile()
+    for i in range(P):
+        flush.fill_(float(i))
+        step()
+    prof = ops.context.profile()
+    ops.context.set_profiling(False)
+    per_launch = {k[:-3]: prof[k] / P * 1e3 for k in prof if k.endswith("_ms")}  # us per step
+    n_omega = N ** 3
+    alg = {"spread": 32 * n + 8 * n_omega, "interp": 32 * n + 8 * n_omega}
+    dom = max(("spread", "interp"), key=lambda k: per_launch.get(k, 0.0))
+    peak, peak_src = peaks()
+    achieved = alg[dom] / (per_launch[dom] * 1e-6) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom)
+        except Exception:
+            traffic = None
+    step_bytes = 64 * n + 16 * n_omega
+
+    # End to end through the reference-facing host API (pinned host buffers).
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        hx_s, hx_n, hg, hf = pin(data["x_star"]), pin(data["x_n"]), pin(data["values"]), pin(data["field"])
+        ctx = ib.default_context(local)
+        ws = ib.SpreadWorkspace(n, grid, context=ctx)
+        kern = ib.CosineKernel()
+        ib.spread_fused(hx_s, hg, grid, kern, ws)
+        ib.interpolate(ib.GridField(grid, hf), hx_n, kern)
+        field = ib.GridField(grid, hf)
+        ts = []
+        for i in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ib.spread_fused(hx_s, hg, grid, kern, ws)
+            ib.interpolate(field, hx_n, kern)
+            ts.append(time.perf_counter() - t0)
+        tmax = max(ts) if world == 1 else ts
+        e2e_s = statistics.median(ts)
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * n / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(hx_s.nbytes + hg.nbytes + hx_n.nbytes + hf.nbytes),
+               "d2h_bytes_per_step": int(n_omega * 8 + n * 8),
+               "note": "ibc_spread + ibc_interpolate (host buffers, pinned), wall clock, median"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+
+            if O.ref_available():
+                threads = host_threads()
+                t = cpu_reference_steps(data, 2, 1, threads)
+                cpu = {"value": n / float(statistics.median(t)), "unit": UNIT, "cores": threads,
+                       "kind": "reference",
+                       "sample": "2 full config-2 steps (ib::spread_fused + ib::interpolate, "
+                                 "oracle/_ref, OpenMP) after 1 warm-up, median"}
+        except Exception as exc:  # pragma: no cover
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_points": n, "grid": [N, N, N],
+                       "parallelism": "replicas" if world > 1 else "single GPU",
+                       "l2": "flushed between steps (256 MiB write outside the events)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_src,
+                         "alg_bytes_per_launch": alg[dom], "launch_us": per_launch[dom]},
+            "step_roofline": {"alg_bytes": step_bytes,
+                              "achieved": step_bytes / (ms_per_step * 1e-3) / 1e9,
+                              "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
+            "breakdown_us": {k: round(v, 2) for k, v in per_launch.items()},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
