@@ -46,7 +46,7 @@ enum ProfClass { kProfKeys = 0, kProfSort, kProfRows, kProfPrep, kProfSpread, kP
 struct PointScratch {
   size_t cap = 0;
   DevBuf<uint32_t> keys[2], vals[2];
-  DevBuf<uint32_t> hist, base, lookback, counters;
+  DevBuf<uint32_t> hist, base, counters;  // per-tile digit histograms, digit totals
   DevBuf<uint32_t> rowstart;
   DevBuf<int> rec_cx;
   DevBuf<double> rec;         // 12 x cap weight records (spread)

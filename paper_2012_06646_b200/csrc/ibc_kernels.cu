@@ -53,42 +53,40 @@ __device__ __forceinline__ uint32_t key_of(const DevGrid& g, const double* x, bo
   return key;
 }
 
-// A few hundred resident CTAs, kKeysUnroll points per thread per round with
-// all coordinate loads issued first; per-CTA shared histograms flushed with
-// one global atomic per non-empty bin.
+// One CTA per 4096-key sort tile (the input order): cell keys of its points
+// and the tile's digit histogram for the first radix pass (hist0[d][tile]).
 template <int D>
 __global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const double* __restrict__ X,
                                                            uint32_t n, uint32_t* __restrict__ keys,
-                                                           uint32_t* __restrict__ hist,
-                                                           sort::DigitPlan plan, int row_only) {
-  __shared__ uint32_t sh[kMaxPasses * sort::kMaxRadix];
-  for (int t = threadIdx.x; t < kMaxPasses * sort::kMaxRadix; t += blockDim.x) sh[t] = 0u;
+                                                           uint32_t* __restrict__ hist0, int ntiles,
+                                                           int shift0, int bits0, int row_only) {
+  __shared__ uint32_t sh[sort::kMaxRadix];
+  const uint32_t radix = 1u << bits0, mask = radix - 1u;
+  for (uint32_t t = threadIdx.x; t < radix; t += blockDim.x) sh[t] = 0u;
   __syncthreads();
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * kKeysUnroll) {
+  const uint32_t base = blockIdx.x * (uint32_t)sort::kTile;
+  constexpr int kPer = sort::kTile / kBlock;  // 16 points per thread
+  for (int j0 = 0; j0 < kPer; j0 += kKeysUnroll) {
     double x[kKeysUnroll][D];
 #pragma unroll
     for (int u = 0; u < kKeysUnroll; ++u) {
-      const uint32_t i = i0 + u * stride;
+      const uint32_t i = base + (uint32_t)(j0 + u) * kBlock + threadIdx.x;
 #pragma unroll
       for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kKeysUnroll; ++u) {
-      const uint32_t i = i0 + u * stride;
-      if (i >= n) break;
-      const uint32_t key = key_of<D>(g, x[u], row_only != 0);
-      keys[i] = key;
-#pragma unroll
-      for (int p = 0; p < kMaxPasses; ++p)
-        if (p < plan.passes)
-          atomicAdd(&sh[p * sort::kMaxRadix + ((key >> plan.shift[p]) & ((1u << plan.bits[p]) - 1u))],
-                    1u);
+      const uint32_t i = base + (uint32_t)(j0 + u) * kBlock + threadIdx.x;
+      if (i < n) {
+        const uint32_t key = key_of<D>(g, x[u], row_only != 0);
+        keys[i] = key;
+        atomicAdd(&sh[(key >> shift0) & mask], 1u);
+      }
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < plan.passes * sort::kMaxRadix; t += blockDim.x)
-    if (sh[t]) atomicAdd(&hist[t], sh[t]);
+  for (uint32_t t = threadIdx.x; t < radix; t += blockDim.x)
+    hist0[(size_t)t * ntiles + blockIdx.x] = sh[t];
 }
 
 // ---------------------------------------------------------------- K3
@@ -386,53 +384,65 @@ inline unsigned grid_for(size_t n, int block) { return (unsigned)((n + block - 1
 
 size_t sort_smem() { return sizeof(sort::PassSmem); }
 
-// Keys + stable sort.  Leaves s.sorted_keys / s.sorted_perm.  row_only sorts
-// by extended row id alone (enough for the interpolation's row grouping).
+// Keys + stable sort.  Leaves s.sorted_keys / s.sorted_perm (and, with a
+// payload, s.rec: 32-byte sorted records).  row_only sorts by extended row id
+// alone (enough for the interpolation's row grouping).
 void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t n, PointScratch& s,
-                 bool row_only) {
+                 bool row_only, int payload = sort::kPayloadNone,
+                 const double* d_values = nullptr) {
   cudaStream_t st = ctx.stream;
   const sort::DigitPlan plan = sort::plan_digits(key_bits(g, row_only));
-  const size_t tiles = (n + sort::kTile - 1) / sort::kTile;
-  IBC_CUDA(cudaMemsetAsync(s.hist.p, 0, (size_t)kMaxPasses * sort::kMaxRadix * 4, st));
+  const int ntiles = (int)((n + sort::kTile - 1) / sort::kTile);
+  size_t hoff[kMaxPasses + 1] = {0};
+  for (int p = 0; p < plan.passes; ++p) hoff[p + 1] = hoff[p] + ((size_t)ntiles << plan.bits[p]);
+  if (plan.passes > 1)
+    IBC_CUDA(cudaMemsetAsync(s.hist.p + hoff[1], 0, (hoff[plan.passes] - hoff[1]) * 4, st));
   IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
-  size_t lb_words = 0;
-  for (int p = 0; p < plan.passes; ++p) lb_words += tiles << plan.bits[p];
-  IBC_CUDA(cudaMemsetAsync(s.lookback.p, 0, lb_words * 4, st));
 
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
-    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)sort_smem()));
-    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                  100));
+    const int sm = (int)sort_smem();
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr_set[ctx.device & 63] = true;
   }
 
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
-  const unsigned kb = std::max(1u, std::min(grid_for(n, kBlock * kKeysUnroll), 148u * 2u));
   const int ro = row_only ? 1 : 0;
   if (g.dim == 3)
-    keys_hist_kernel<3><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);
+    keys_hist_kernel<3><<<ntiles, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
+                                                   ntiles, plan.shift[0], plan.bits[0], ro);
   else if (g.dim == 2)
-    keys_hist_kernel<2><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);
+    keys_hist_kernel<2><<<ntiles, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
+                                                   ntiles, plan.shift[0], plan.bits[0], ro);
   else
-    keys_hist_kernel<1><<<kb, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p, plan, ro);
+    keys_hist_kernel<1><<<ntiles, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
+                                                   ntiles, plan.shift[0], plan.bits[0], ro);
   ++ctx.launches;
   ctx.prof_end(kProfKeys, ev);
 
   ctx.prof_begin(kProfSort, &ev);
-  sort::digit_scan<<<plan.passes, sort::kThreads, 0, st>>>(s.hist.p, s.base.p, plan);
-  ++ctx.launches;
   int src = 0;
-  size_t lb_off = 0;
   for (int p = 0; p < plan.passes; ++p) {
-    sort::onesweep_pass<<<(unsigned)tiles, sort::kThreads, sort_smem(), st>>>(
-        s.keys[src].p, p == 0 ? nullptr : s.vals[src].p, s.keys[src ^ 1].p, s.vals[src ^ 1].p,
-        (uint32_t)n, plan.shift[p], plan.bits[p], s.base.p + (size_t)p * sort::kMaxRadix,
-        s.lookback.p + lb_off, s.counters.p + p);
-    ++ctx.launches;
-    lb_off += tiles << plan.bits[p];
+    uint32_t* hp = s.hist.p + hoff[p];
+    uint32_t* tot = s.base.p + (size_t)p * sort::kMaxRadix;
+    sort::tile_scan<<<1u << plan.bits[p], sort::kThreads, 0, st>>>(hp, tot, ntiles);
+    const bool last = p + 1 == plan.passes;
+    uint32_t* nh = last ? nullptr : s.hist.p + hoff[p + 1];
+    const int nshift = last ? 0 : plan.shift[p + 1], nbits = last ? 1 : plan.bits[p + 1];
+    const int pl = last ? payload : sort::kPayloadNone;
+    auto args = [&](auto kern) {
+      kern<<<ntiles, sort::kThreads, sort_smem(), st>>>(
+          s.keys[src].p, p == 0 ? nullptr : s.vals[src].p, s.keys[src ^ 1].p, s.vals[src ^ 1].p,
+          (uint32_t)n, plan.shift[p], plan.bits[p], hp, tot, ntiles, nh, nshift, nbits, d_points,
+          d_values, s.rec.p);
+    };
+    if (pl == sort::kPayloadSpread) args(sort::onesweep_pass<sort::kPayloadSpread>);
+    else if (pl == sort::kPayloadInterp) args(sort::onesweep_pass<sort::kPayloadInterp>);
+    else args(sort::onesweep_pass<sort::kPayloadNone>);
+    ctx.launches += 2;
     src ^= 1;
   }
   ctx.prof_end(kProfSort, ev);
@@ -559,14 +569,11 @@ void PointScratch::reserve_points(size_t n, bool spread) {
     keys[b].ensure(n);
     vals[b].ensure(n);
   }
-  hist.ensure((size_t)kMaxPasses * sort::kMaxRadix);
+  hist.ensure((size_t)kMaxPasses * sort::kMaxRadix * std::max<size_t>(tiles, 1));
   base.ensure((size_t)kMaxPasses * sort::kMaxRadix);
-  lookback.ensure((size_t)kMaxPasses * std::max<size_t>(tiles, 1) * sort::kMaxRadix);
   counters.ensure(kCounters);
-  if (spread) {
-    rec_cx.ensure(n);
-    rec.ensure(12 * std::max<size_t>(n, 1));
-  }
+  rec.ensure(12 * std::max<size_t>(n, 1));  // 12 doubles (V1 weights) or 4 (sorted records)
+  if (spread) rec_cx.ensure(n);
   cap = std::max(cap, n);
 }
 
@@ -577,7 +584,7 @@ void PointScratch::release_all() {
     keys[b].release();
     vals[b].release();
   }
-  hist.release(); base.release(); lookback.release(); counters.release(); rowstart.release();
+  hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release();
   cap = 0;
 }

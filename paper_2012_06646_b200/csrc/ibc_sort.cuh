@@ -1,23 +1,27 @@
-// ibc_sort.cuh -- stable onesweep LSD radix sort of (cell key, point index).
+// ibc_sort.cuh -- stable LSD radix sort of (cell key, point index) on sm_100a.
 //
 // Replaces ib::key_value_sort<uint32_t> (sort.hpp:17-71).  Same contract:
 // stable, so equal keys keep input order and the permutation is unique --
 // bit-identical to the reference's ws.keys / ws.perm (spread.hpp:100).
 //
-// Structure (Adinets & Merrill, "Onesweep", 2022), B200-sized:
+// B200 structure:
 //  * Keys are < prod(n_a + 2), so only key_bits(grid) bits are sorted, split
-//    into P = ceil(bits / 10) balanced digits of <= 10 bits (25 bits at 256^3
-//    -> 9/8/8: three passes instead of the reference's four 8-bit passes).
-//  * The digit histograms of ALL passes come from one read of the keys,
-//    fused into the key-computation kernel (ibc_kernels.cu).
-//  * One kernel per digit pass.  Each CTA claims a 4096-key tile through an
-//    atomic tile counter (so look-back only ever waits on CTAs that are
-//    already resident), ranks its keys with warp ballots (one __ballot_sync
-//    per digit bit builds the equal-digit match mask; rank =
-//    popc(mask & lanemask_lt)), publishes per-digit tile counts and resolves
-//    global offsets by decoupled look-back that polls 32 predecessor tiles
-//    per round trip, then writes keys/values in digit-sorted runs through
-//    shared memory so the global scatter is coalesced.
+//    into P = ceil(bits / 10) balanced digits of <= 10 bits (25 bits at
+//    256^3 -> 9/8/8: three passes instead of the reference's four).
+//  * Each pass is ONE scatter kernel over 4096-key tiles.  A tile ranks its
+//    keys with warp ballots (one __ballot_sync per digit bit builds the
+//    equal-digit match mask; rank = popc(mask & lanemask_lt)), and reads its
+//    global digit offsets from a table prepared before the pass -- there is
+//    no decoupled look-back, so no tile ever waits on another:
+//      - the per-tile digit histogram of pass 0 comes from the key kernel
+//        (which works tile by tile over the input order),
+//      - the per-tile histogram of pass p+1 is accumulated by pass p's
+//        scatter (each key knows its output slot, hence its next tile),
+//      - a small column scan turns histograms into offsets between passes.
+//  * Keys/values leave the tile through shared memory in digit-sorted runs,
+//    so the global scatter is coalesced.  The last pass can also gather a
+//    32-byte payload per point (coordinates + value or index) into sorted
+//    order, so the operators stream contiguous records with TMA bulk copies.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -32,14 +36,11 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;
 constexpr int kTile = kThreads * kItems;  // 4096 keys per tile
 constexpr int kWarpSpan = 32 * kItems;    // 512 consecutive keys per warp
-constexpr int kDigitsPerThread = kMaxRadix / kThreads;
-constexpr int kLookback = 32;             // predecessor tiles polled per round trip
-constexpr uint32_t kFlagAgg = 1u << 30;
-constexpr uint32_t kFlagInc = 2u << 30;
-constexpr uint32_t kValueMask = (1u << 30) - 1;
 constexpr int kMaxPasses = 4;
 
-// Shared memory of one pass (dynamic: > 48 KB).
+// Payload gathered by the last pass, one 32-byte record per sorted position.
+enum Payload { kPayloadNone = 0, kPayloadSpread = 1, kPayloadInterp = 2 };
+
 struct PassSmem {
   uint32_t whist[kWarps][kMaxRadix];  // per-warp digit counts, then warp offsets
   uint32_t keys[kTile];
@@ -47,7 +48,6 @@ struct PassSmem {
   uint32_t tile_start[kMaxRadix];
   uint32_t gofs[kMaxRadix];
   uint32_t warp_tmp[kWarps];
-  uint32_t tile_id;
 };
 
 struct DigitPlan {
@@ -68,18 +68,6 @@ inline DigitPlan plan_digits(int key_bits) {
     shift += p.bits[i];
   }
   return p;
-}
-
-// The look-back words carry only their own payload (no other data is
-// published through them), so relaxed gpu-scope accesses suffice: they are
-// served by L2 without the L1 invalidation (CCTL.IVALL) an acquire costs.
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Exclusive scan of one value per thread over a 256-thread block; *total gets the sum.
@@ -106,49 +94,55 @@ __device__ __forceinline__ uint32_t block_exclusive_scan(uint32_t v, uint32_t* s
   return base + x - v;
 }
 
-// Decoupled look-back for one digit: sum of the counts of all preceding
-// tiles.  Polls kLookback predecessors per round trip.
-__device__ __forceinline__ uint32_t lookback_digit(const uint32_t* lookback, uint32_t tile,
-                                                   uint32_t radix, uint32_t d) {
-  uint32_t excl = 0;
-  int p = (int)tile - 1;
-  while (p >= 0) {
-    uint32_t v[kLookback];
-#pragma unroll
-    for (int j = 0; j < kLookback; ++j)
-      v[j] = (p - j >= 0) ? ld_acquire(lookback + (size_t)(p - j) * radix + d) : kFlagInc;
-    int consumed = 0;
-    bool done = false;
-#pragma unroll
-    for (int j = 0; j < kLookback; ++j) {
-      if (done || consumed != j) continue;
-      if (p - j < 0) { done = true; continue; }
-      const uint32_t f = v[j] & ~kValueMask;
-      if (f == 0u) continue;  // not yet published: re-poll from here
-      excl += v[j] & kValueMask;
-      ++consumed;
-      if (f == kFlagInc) done = true;
-    }
-    if (done) break;
-    p -= consumed;
+// Column scan between passes: hist[d][t] (digit-major, ntiles per digit) ->
+// exclusive prefix over tiles, in place; total[d] = column sum.  One block
+// per digit.
+__global__ void __launch_bounds__(kThreads) tile_scan(uint32_t* __restrict__ hist,
+                                                      uint32_t* __restrict__ total, int ntiles) {
+  __shared__ uint32_t s_warp[kWarps];
+  uint32_t* col = hist + (size_t)blockIdx.x * ntiles;
+  uint32_t carry = 0;
+  for (int t0 = 0; t0 < ntiles; t0 += kThreads) {
+    const int t = t0 + threadIdx.x;
+    const uint32_t v = t < ntiles ? col[t] : 0u;
+    uint32_t sum;
+    const uint32_t ex = block_exclusive_scan(v, s_warp, &sum);
+    if (t < ntiles) col[t] = carry + ex;
+    carry += sum;
   }
-  return excl;
+  if (threadIdx.x == 0) total[blockIdx.x] = carry;
 }
 
-// One stable digit pass.  vals_in == nullptr means the identity permutation.
+// One stable digit pass over tile blockIdx.x.  vals_in == nullptr means the
+// identity permutation.  tile_off[d][t]: exclusive prefix of digit d over
+// preceding tiles; total[d]: count of digit d.  next_hist (may be null):
+// per-tile histogram of the next pass, accumulated over output slots.
+template <int PAYLOAD>
 __global__ void __launch_bounds__(kThreads) onesweep_pass(
     const uint32_t* __restrict__ keys_in, const uint32_t* __restrict__ vals_in,
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
-    int bits, const uint32_t* __restrict__ digit_base, uint32_t* __restrict__ lookback,
-    uint32_t* __restrict__ tile_counter) {
+    int bits, const uint32_t* __restrict__ tile_off, const uint32_t* __restrict__ total,
+    int ntiles, uint32_t* __restrict__ next_hist, int next_shift, int next_bits,
+    const double* __restrict__ pts, const double* __restrict__ gvals, double* __restrict__ rec) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem& S = *reinterpret_cast<PassSmem*>(smem_raw);
   const uint32_t radix = 1u << bits, mask = radix - 1u;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) S.tile_id = atomicAdd(tile_counter, 1u);
+  const uint32_t tile = blockIdx.x;
   for (uint32_t i = tid; i < kWarps * radix; i += kThreads) S.whist[i >> bits][i & mask] = 0u;
+  // Global digit bases: exclusive scan of the digit totals.
+  {
+    uint32_t carry = 0;
+    for (uint32_t d0 = 0; d0 < radix; d0 += kThreads) {
+      const uint32_t d = d0 + tid;
+      const uint32_t v = d < radix ? total[d] : 0u;
+      uint32_t sum;
+      const uint32_t ex = block_exclusive_scan(v, S.warp_tmp, &sum);
+      if (d < radix) S.gofs[d] = carry + ex + tile_off[(size_t)d * ntiles + tile];
+      carry += sum;
+    }
+  }
   __syncthreads();
-  const uint32_t tile = S.tile_id;
   const uint32_t tile_base = tile * (uint32_t)kTile;
   const uint32_t warp_base = tile_base + (uint32_t)warp * kWarpSpan;
 
@@ -188,45 +182,27 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
   }
   __syncthreads();
 
-  // Digits are owned round-robin by threads: d = tid + 256 * i.
-  uint32_t count[kDigitsPerThread];
+  // Per digit: warp-exclusive offsets and the tile count; tile-local starts.
+  {
+    uint32_t carry = 0;
+    for (uint32_t d0 = 0; d0 < radix; d0 += kThreads) {
+      const uint32_t d = d0 + tid;
+      uint32_t c = 0;
+      if (d < radix) {
 #pragma unroll
-  for (int i = 0; i < kDigitsPerThread; ++i) {
-    const uint32_t d = tid + kThreads * i;
-    uint32_t c = 0;
-    if (d < radix) {
-#pragma unroll
-      for (int w = 0; w < kWarps; ++w) {
-        const uint32_t x = S.whist[w][d];
-        S.whist[w][d] = c;
-        c += x;
+        for (int w = 0; w < kWarps; ++w) {
+          const uint32_t x = S.whist[w][d];
+          S.whist[w][d] = c;
+          c += x;
+        }
       }
-      st_release(lookback + (size_t)tile * radix + d, (tile == 0 ? kFlagInc : kFlagAgg) | c);
-    }
-    count[i] = c;
-  }
-  uint32_t excl[kDigitsPerThread];
-#pragma unroll
-  for (int i = 0; i < kDigitsPerThread; ++i) {
-    const uint32_t d = tid + kThreads * i;
-    excl[i] = 0;
-    if (d < radix && tile > 0) {
-      excl[i] = lookback_digit(lookback, tile, radix, d);
-      st_release(lookback + (size_t)tile * radix + d, kFlagInc | (excl[i] + count[i]));
-    }
-  }
-  // Tile-local exclusive scan over digits (digit-major across the threads).
-  uint32_t carry = 0;
-#pragma unroll
-  for (int i = 0; i < kDigitsPerThread; ++i) {
-    const uint32_t d = tid + kThreads * i;
-    if ((uint32_t)(kThreads * i) >= radix) break;  // block-uniform
-    uint32_t total;
-    const uint32_t start = carry + block_exclusive_scan(count[i], S.warp_tmp, &total);
-    carry += total;
-    if (d < radix) {
-      S.tile_start[d] = start;
-      S.gofs[d] = digit_base[d] + excl[i] - start;
+      uint32_t sum;
+      const uint32_t start = carry + block_exclusive_scan(c, S.warp_tmp, &sum);
+      carry += sum;
+      if (d < radix) {
+        S.tile_start[d] = start;
+        S.gofs[d] -= start;
+      }
     }
   }
   __syncthreads();
@@ -244,31 +220,25 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
   __syncthreads();
 
   const uint32_t tile_n = min((uint32_t)kTile, n - tile_base);
+  const uint32_t nmask = (1u << next_bits) - 1u;
   for (uint32_t i = tid; i < tile_n; i += kThreads) {
     const uint32_t k = S.keys[i];
+    const uint32_t v = S.vals[i];
     const uint32_t o = S.gofs[(k >> shift) & mask] + i;
     keys_out[o] = k;
-    vals_out[o] = S.vals[i];
-  }
-}
-
-// Exclusive scan of each pass's global digit histogram (one block per pass).
-__global__ void __launch_bounds__(kThreads) digit_scan(const uint32_t* __restrict__ hist,
-                                                       uint32_t* __restrict__ base,
-                                                       DigitPlan plan) {
-  __shared__ uint32_t s_warp[kWarps];
-  const int p = blockIdx.x;
-  const uint32_t radix = 1u << plan.bits[p];
-  const uint32_t* h = hist + (size_t)p * kMaxRadix;
-  uint32_t* b = base + (size_t)p * kMaxRadix;
-  uint32_t carry = 0;
-  for (uint32_t i0 = 0; i0 < radix; i0 += kThreads) {
-    const uint32_t i = i0 + threadIdx.x;
-    const uint32_t v = i < radix ? h[i] : 0u;
-    uint32_t total;
-    const uint32_t ex = block_exclusive_scan(v, s_warp, &total);
-    if (i < radix) b[i] = carry + ex;
-    carry += total;
+    vals_out[o] = v;
+    if (next_hist)
+      atomicAdd(&next_hist[(size_t)((k >> next_shift) & nmask) * ntiles + o / (uint32_t)kTile], 1u);
+    if (PAYLOAD != kPayloadNone) {
+      const double* x = pts + (size_t)v * 3;
+      double4 r;
+      r.x = __ldg(x);
+      r.y = __ldg(x + 1);
+      r.z = __ldg(x + 2);
+      if (PAYLOAD == kPayloadSpread) r.w = __ldg(gvals + v);
+      else r.w = __longlong_as_double((long long)v);
+      reinterpret_cast<double4*>(rec)[o] = r;
+    }
   }
 }
 
