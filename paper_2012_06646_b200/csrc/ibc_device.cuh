@@ -44,6 +44,11 @@ __device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
 
 // wrap_position (grid.hpp:197-207) + cell_index for even support
 // (grid.hpp:121-130) on one axis.  Returns the cell; *xw gets the wrapped x.
+// The cell must equal ceil((xw - o) / h - alpha) exactly as the reference
+// rounds it.  Fast path: q = (xw - o) * (1/h) is within ~2.3e-16 |q| of the
+// correctly rounded quotient, so unless t = q - alpha lies within 1e-13 (|q|+1)
+// of an integer, ceil(t) is the reference's cell; otherwise (a ~1e-13 fraction
+// of points) the IEEE division is evaluated.
 __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double* xw) {
   double w = x;
   if (g.periodic[a]) {
@@ -54,14 +59,20 @@ __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double
     w = __dadd_rn(g.origin[a], r);
   }
   *xw = w;
-  const double t = __dsub_rn(__ddiv_rn(__dsub_rn(w, g.origin[a]), g.h), g.alpha[a]);
-  return (int)ceil(t);
+  const double d = __dsub_rn(w, g.origin[a]);
+  const double q = __dmul_rn(d, g.inv_h);
+  const double t = __dsub_rn(q, g.alpha[a]);
+  const double c = ceil(t);
+  const double margin = 1e-13 * (fabs(q) + 1.0);
+  if (c - t > margin && t - (c - 1.0) > margin) return (int)c;
+  return (int)ceil(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]));
 }
 
 // displacement_ratio (support_window.hpp:48-55): (xw - h*(i+alpha) - o) / h.
+// Only feeds the weights (not bit-exact anyway): multiply by 1/h.
 __device__ __forceinline__ double displacement(const DevGrid& g, int a, double xw, int c) {
   const double hp = __dadd_rn(__dmul_rn(g.h, __dadd_rn((double)c, g.alpha[a])), g.origin[a]);
-  return __ddiv_rn(__dsub_rn(xw, hp), g.h);
+  return (xw - hp) * g.inv_h;
 }
 
 // cell_key (grid.hpp:158-170) of already-computed (unwrapped) cells.

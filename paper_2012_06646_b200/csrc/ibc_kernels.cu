@@ -55,28 +55,30 @@ __device__ __forceinline__ uint32_t key_of(const DevGrid& g, const double* x, bo
 
 // One CTA per 4096-key sort tile (the input order): cell keys of its points
 // and the tile's digit histogram for the first radix pass (hist0[d][tile]).
+constexpr int kKeysThreads = 1024;
+
 template <int D>
-__global__ void __launch_bounds__(kBlock) keys_hist_kernel(DevGrid g, const double* __restrict__ X,
-                                                           uint32_t n, uint32_t* __restrict__ keys,
-                                                           uint32_t* __restrict__ hist0, int ntiles,
-                                                           int shift0, int bits0, int row_only) {
+__global__ void __launch_bounds__(kKeysThreads) keys_hist_kernel(
+    DevGrid g, const double* __restrict__ X, uint32_t n, uint32_t* __restrict__ keys,
+    uint32_t* __restrict__ hist0, int ntiles, int shift0, int bits0, int row_only) {
   __shared__ uint32_t sh[sort::kMaxRadix];
   const uint32_t radix = 1u << bits0, mask = radix - 1u;
   for (uint32_t t = threadIdx.x; t < radix; t += blockDim.x) sh[t] = 0u;
   __syncthreads();
   const uint32_t base = blockIdx.x * (uint32_t)sort::kTile;
-  constexpr int kPer = sort::kTile / kBlock;  // 16 points per thread
+  constexpr int kPer = sort::kTile / kKeysThreads;  // 4 points per thread
+  static_assert(kPer % kKeysUnroll == 0, "tile split");
   for (int j0 = 0; j0 < kPer; j0 += kKeysUnroll) {
     double x[kKeysUnroll][D];
 #pragma unroll
     for (int u = 0; u < kKeysUnroll; ++u) {
-      const uint32_t i = base + (uint32_t)(j0 + u) * kBlock + threadIdx.x;
+      const uint32_t i = base + (uint32_t)(j0 + u) * kKeysThreads + threadIdx.x;
 #pragma unroll
       for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < kKeysUnroll; ++u) {
-      const uint32_t i = base + (uint32_t)(j0 + u) * kBlock + threadIdx.x;
+      const uint32_t i = base + (uint32_t)(j0 + u) * kKeysThreads + threadIdx.x;
       if (i < n) {
         const uint32_t key = key_of<D>(g, x[u], row_only != 0);
         keys[i] = key;
@@ -112,13 +114,8 @@ __global__ void __launch_bounds__(kBlock) rowstart_kernel(const uint32_t* __rest
     if (i == n - 1)
       for (uint32_t r = row + 1; r <= nrows; ++r) rowstart[r] = n;
   }
-  __shared__ uint32_t s_q;
-  if (threadIdx.x == 0) s_q = 0;
-  __syncthreads();
-  const uint32_t hb = __ballot_sync(0xffffffffu, head);
-  if ((threadIdx.x & 31) == 0 && hb) atomicAdd(&s_q, (uint32_t)__popc(hb));
-  __syncthreads();
-  if (threadIdx.x == 0 && s_q) atomicAdd(q_out, s_q);  // one global atomic per block
+  (void)head;
+  (void)q_out;  // the run count q is computed lazily (compute_run_keys)
 }
 
 // ---------------------------------------------------------------- K4a
@@ -335,7 +332,8 @@ __global__ void __launch_bounds__(kBlock) head_count_kernel(const uint32_t* __re
   if (threadIdx.x == 0) counts[blockIdx.x] = s;
 }
 
-__global__ void __launch_bounds__(sort::kThreads) block_scan_kernel(uint32_t* counts, uint32_t nb) {
+__global__ void __launch_bounds__(sort::kThreads) block_scan_kernel(uint32_t* counts, uint32_t nb,
+                                                                   uint32_t* q_out) {
   __shared__ uint32_t s_warp[sort::kWarps];
   __shared__ uint32_t s_carry;
   if (threadIdx.x == 0) s_carry = 0;
@@ -350,6 +348,7 @@ __global__ void __launch_bounds__(sort::kThreads) block_scan_kernel(uint32_t* co
     if (threadIdx.x == sort::kThreads - 1) s_carry = carry + ex + v;
     __syncthreads();
   }
+  if (threadIdx.x == 0) *q_out = s_carry;
 }
 
 __global__ void __launch_bounds__(kBlock) head_write_kernel(const uint32_t* __restrict__ sk, uint32_t n,
@@ -412,13 +411,13 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
   ctx.prof_begin(kProfKeys, &ev);
   const int ro = row_only ? 1 : 0;
   if (g.dim == 3)
-    keys_hist_kernel<3><<<ntiles, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
+    keys_hist_kernel<3><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
                                                    ntiles, plan.shift[0], plan.bits[0], ro);
   else if (g.dim == 2)
-    keys_hist_kernel<2><<<ntiles, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
+    keys_hist_kernel<2><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
                                                    ntiles, plan.shift[0], plan.bits[0], ro);
   else
-    keys_hist_kernel<1><<<ntiles, kBlock, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
+    keys_hist_kernel<1><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
                                                    ntiles, plan.shift[0], plan.bits[0], ro);
   ++ctx.launches;
   ctx.prof_end(kProfKeys, ev);
@@ -471,7 +470,7 @@ void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
 
 size_t zsweep_smem_bytes(const zs::Tiling& T, bool interp) {
   return interp ? (size_t)4 * (T.ty + 5) * T.nxp * sizeof(double)
-                : ((size_t)4 * T.ty * T.nxp + zs::kSThreads) * sizeof(double);
+                : sizeof(zs::SpreadSmem) + ((size_t)4 * T.ty * T.nxp + zs::kSThreads) * sizeof(double);
 }
 
 // z-sweep tiling for 3-D grids with rows short enough for shared memory.
@@ -483,7 +482,7 @@ bool zsweep_tiling(const DevGrid& g, bool interp, zs::Tiling& T) {
   T.nxp = nx + zs::kPadL + zs::kPadR;
   if (T.nxp & 1) T.nxp += 1;
   const size_t row_bytes = (size_t)T.nxp * 8;
-  const size_t budget = interp ? 100 * 1024 : 36 * 1024;
+  const size_t budget = interp ? 100 * 1024 : 34 * 1024;
   const int extra = interp ? 5 : 0;
   int ty = 16;
   while (ty > 1 && 4 * (size_t)(ty + extra) * row_bytes > budget) --ty;
@@ -497,6 +496,7 @@ bool zsweep_tiling(const DevGrid& g, bool interp, zs::Tiling& T) {
   // z chunks of >= 4 planes, enough CTAs to fill every SM about 1.5 times.
   int zc = (int)std::max<long>(4, ((long)g.n[2] * T.nty * 2) / (148L * per_sm * 3));
   zc = std::min(zc, g.n[2]);
+  if (!interp) zc = std::min(zc, zs::kMaxSteps - 4);
   T.zc = zc;
   T.nzc = (g.n[2] + zc - 1) / zc;
   return true;
@@ -592,8 +592,11 @@ void PointScratch::release_all() {
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
+  zs::Tiling Z;
+  const bool zsweep = zsweep_tiling(g, false, Z);
   if (n > 0) {
-    sort_points(ctx, g, d_points, n, s, false);
+    sort_points(ctx, g, d_points, n, s, false,
+                zsweep ? sort::kPayloadSpread : sort::kPayloadNone, d_values);
   } else {
     IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
     s.last_n = 0;
@@ -618,11 +621,10 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
     attr_set[ctx.device & 63] = true;
   }
-  zs::Tiling Z;
-  if (zsweep_tiling(g, false, Z)) {
+  if (zsweep) {
     ctx.prof_begin(kProfSpread, &ev);
     zs::spread_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kSThreads, zsweep_smem_bytes(Z, false), st>>>(
-        g, Z, s.rowstart.p, s.sorted_keys, s.sorted_perm, d_points, d_values, d_out);
+        g, Z, s.rowstart.p, s.rec.p, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   } else {
@@ -689,29 +691,30 @@ int debug_zsweep_trace(int block, long long* out) {
   return (int)cudaMemcpyToSymbol(zs::g_trace_block, &block, sizeof(int));
 }
 
-size_t read_run_count(Context& ctx, PointScratch& s) {
+// ws.run_keys and ws.run_count (= q) on the device, computed on demand from
+// the sorted keys (reduce.hpp:36-69); cached until the next sort.
+size_t compute_run_keys(Context& ctx, PointScratch& s) {
+  const size_t n = s.last_n;
+  if (n == 0) return 0;
+  cudaStream_t st = ctx.stream;
+  if (!s.run_keys_valid) {
+    const unsigned nb = grid_for(n, kBlock);
+    s.block_counts.ensure(nb);
+    s.run_keys.ensure(n);
+    head_count_kernel<<<nb, kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, s.block_counts.p);
+    block_scan_kernel<<<1, sort::kThreads, 0, st>>>(s.block_counts.p, nb, s.counters.p + kMaxPasses);
+    head_write_kernel<<<nb, kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, s.block_counts.p,
+                                             s.run_keys.p);
+    ctx.launches += 3;
+    IBC_CUDA(cudaGetLastError());
+    s.run_keys_valid = true;
+  }
   uint32_t q = 0;
-  IBC_CUDA(cudaMemcpyAsync(&q, s.counters.p + kMaxPasses, 4, cudaMemcpyDeviceToHost, ctx.stream));
-  IBC_CUDA(cudaStreamSynchronize(ctx.stream));
+  IBC_CUDA(cudaMemcpyAsync(&q, s.counters.p + kMaxPasses, 4, cudaMemcpyDeviceToHost, st));
+  IBC_CUDA(cudaStreamSynchronize(st));
   return q;
 }
 
-size_t compute_run_keys(Context& ctx, PointScratch& s) {
-  const size_t n = s.last_n;
-  const size_t q = read_run_count(ctx, s);
-  if (s.run_keys_valid || n == 0) return q;
-  cudaStream_t st = ctx.stream;
-  const unsigned nb = grid_for(n, kBlock);
-  s.block_counts.ensure(nb);
-  s.run_keys.ensure(std::max<size_t>(q, 1));
-  head_count_kernel<<<nb, kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, s.block_counts.p);
-  block_scan_kernel<<<1, sort::kThreads, 0, st>>>(s.block_counts.p, nb);
-  head_write_kernel<<<nb, kBlock, 0, st>>>(s.sorted_keys, (uint32_t)n, s.block_counts.p, s.run_keys.p);
-  ctx.launches += 3;
-  IBC_CUDA(cudaGetLastError());
-  IBC_CUDA(cudaStreamSynchronize(st));
-  s.run_keys_valid = true;
-  return q;
-}
+size_t read_run_count(Context& ctx, PointScratch& s) { return compute_run_keys(ctx, s); }
 
 }  // namespace ibc

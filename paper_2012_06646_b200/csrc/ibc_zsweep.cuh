@@ -118,15 +118,30 @@ __device__ __forceinline__ double folded(const double* row, int x, int nx, bool 
 }
 
 // ------------------------------------------------------------------ spread
+constexpr int kStages = 3;        // TMA ring depth (work items in flight)
+constexpr int kCap = 256;         // sorted points per work item (32 B records)
+constexpr int kMaxSteps = 72;     // z-steps per CTA (zc + 4)
+
+struct SpreadSmem {
+  double4 ring[kStages][kCap];               // sorted records {x, y, z, G}
+  uint64_t bar[kStages];
+  uint32_t rs[kMaxSteps][kMaxRows];          // per step, per source row: sorted range start
+  uint32_t pref[kMaxSteps][kMaxRows + 1];    // per step: prefix of row lengths
+  uint32_t item0[kMaxSteps + 1];             // first work item of each step
+};
+
+__device__ __forceinline__ int find_row(const uint32_t* pref, int nrows, uint32_t p) {
+  int j = 0;
+  while (j + 1 < nrows && pref[j + 1] <= p) ++j;
+  return j;
+}
+
 __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
-    DevGrid g, Tiling T, const uint32_t* __restrict__ rowstart,
-    const uint32_t* __restrict__ skeys, const uint32_t* __restrict__ perm,
-    const double* __restrict__ X, const double* __restrict__ G, double* __restrict__ out) {
-  extern __shared__ __align__(16) double win[];  // [4][ty][nxp], then one dummy slot per thread
-  __shared__ uint32_t s_rb[kMaxRows];
-  __shared__ uint32_t s_pref[kMaxRows + 1];
-  __shared__ int s_wlo[kSWarps + 1];
-  __shared__ int s_groups;
+    DevGrid g, Tiling T, const uint32_t* __restrict__ rowstart, const double* __restrict__ rec,
+    double* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  SpreadSmem& S = *reinterpret_cast<SpreadSmem*>(smem_raw);
+  double* win = reinterpret_cast<double*>(smem_raw + sizeof(SpreadSmem));  // [4][ty][nxp] + dummies
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
@@ -134,194 +149,247 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
   const int y0 = by * T.ty, y1 = min(y0 + T.ty, ny);
   const int z0 = bz * T.zc, z1 = min(z0 + T.zc, nz);
   const int rows = y1 - y0;
-  const int srows = rows + 3;  // unwrapped source rows y0-1 .. y1+1
+  const int srows = rows + 3;            // unwrapped source rows y0-1 .. y1+1
+  const int nsteps = (z1 + 1) - (z0 - 1) + 1;  // source planes z0-1 .. z1+1
   const int plane = T.ty * T.nxp;
   double* dummy = win + 4 * plane + tid;  // sink for lanes with nothing to add
   const uint32_t le = lanemask_le();
   const bool px = g.periodic[0] != 0;
-  const bool vec = (nx & 1) == 0;  // double2 write-back (row bodies are 16-byte aligned)
-  for (int i = tid; i < 4 * plane + kSThreads; i += kSThreads) win[i] = 0.0;
+  const bool vec = (nx & 1) == 0;
 
-  for (int s = z0 - 1; s <= z1 + 2; ++s) {
-    const int step = s - (z0 - 1);
-    ZS_TRACE(0, step, 0);
-    // (a) Target plane s-3 is complete (its last source plane was s-1):
-    //     fold the periodic x pad back and write it to HBM once.
+  for (int i = tid; i < 4 * plane + kSThreads; i += kSThreads) win[i] = 0.0;
+  // Prologue: sorted ranges of every (step, source row) of this CTA.
+  for (int e = tid; e < nsteps * srows; e += kSThreads) {
+    const int st = e / srows, j = e - st * srows;
+    const int s = z0 - 1 + st, cyu = y0 - 1 + j;
+    uint32_t rb = 0, len = 0;
+    const bool zok = g.periodic[2] || (s >= -1 && s <= nz);
+    const bool yok = g.periodic[1] || (cyu >= -1 && cyu <= ny);
+    if (zok && yok) {
+      const int cyw = g.periodic[1] ? wrap_cell(cyu, ny) : cyu;
+      const int szw = g.periodic[2] ? wrap_cell(s, nz) : s;
+      const uint32_t rid = row_id(g, cyw, szw);
+      rb = __ldg(rowstart + rid);
+      len = __ldg(rowstart + rid + 1) - rb;
+    }
+    S.rs[st][j] = rb;
+    S.pref[st][j + 1] = len;  // lengths for now
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kStages; ++i) mbar_init(&S.bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid < nsteps) {
+    uint32_t acc = 0;
+    S.pref[tid][0] = 0;
+    for (int j = 0; j < srows; ++j) {
+      acc += S.pref[tid][j + 1];
+      S.pref[tid][j + 1] = acc;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t it = 0;
+    for (int st = 0; st < nsteps; ++st) {
+      S.item0[st] = it;
+      it += (S.pref[st][srows] + kCap - 1) / kCap;
+    }
+    S.item0[nsteps] = it;
+  }
+  __syncthreads();
+  const uint32_t nitems = S.item0[nsteps];
+
+  // Producer (thread 0): TMA bulk copies of work item k into ring slot k % kStages.
+  auto issue = [&](uint32_t k) {
+    if (k >= nitems) return;
+    int st = 0;
+    while (st + 1 < nsteps && S.item0[st + 1] <= k) ++st;
+    const uint32_t a = (k - S.item0[st]) * kCap;
+    const uint32_t b = min(a + (uint32_t)kCap, S.pref[st][srows]);
+    const int slot = (int)(k % kStages);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(&S.bar[slot], (b - a) * 32u);
+    uint32_t run_src = 0, run_dst = 0, run_len = 0;
+    for (int j = 0; j < srows; ++j) {
+      const uint32_t pa = max(S.pref[st][j], a), pb = min(S.pref[st][j + 1], b);
+      if (pa >= pb) continue;
+      const uint32_t src = S.rs[st][j] + (pa - S.pref[st][j]);
+      if (run_len && run_src + run_len == src) {
+        run_len += pb - pa;
+      } else {
+        if (run_len)
+          bulk_g2s(&S.ring[slot][run_dst], rec + (size_t)run_src * 4, run_len * 32u, &S.bar[slot]);
+        run_src = src;
+        run_dst = pa - a;
+        run_len = pb - pa;
+      }
+    }
+    if (run_len) bulk_g2s(&S.ring[slot][run_dst], rec + (size_t)run_src * 4, run_len * 32u, &S.bar[slot]);
+  };
+  if (tid == 0)
+    for (uint32_t k = 0; k < (uint32_t)kStages; ++k) issue(k);
+
+  uint32_t item = 0;
+  for (int st = 0; st <= nsteps; ++st) {
+    const int s = z0 - 1 + st;
+    // (a) Target plane s-3 is complete (its last source plane was s-1): fold
+    //     the periodic x pad back, write it to HBM once, clear the slot for
+    //     plane s+1.  Each element is read and cleared by one thread.
     const int t = s - 3;
-    const bool flush = t >= z0 && t < z1;
-    if (flush) {
-      const double* wp = win + (t & 3) * plane;
-      if (vec) {
+    if (t >= z0 && t < z1) {
+      double* wp = win + (t & 3) * plane;
+      if (vec && nx >= 4) {
         const int half = nx >> 1;
-        for (int i = tid; i < rows * half; i += kSThreads) {
-          const int r = i / half, x = 2 * (i - r * half);
-          const double* row = wp + r * T.nxp + kPadL;
-          double2 v = *reinterpret_cast<const double2*>(row + x);
-          if (px) {
-            v.x = folded(row, x, nx, true);
-            v.y = folded(row, x + 1, nx, true);
+        for (int r = 0; r < rows; ++r) {
+          double* row = wp + r * T.nxp + kPadL;
+          double* orow = out + ((size_t)t * ny + (size_t)(y0 + r)) * nx;
+          for (int i = tid; i < half; i += kSThreads) {
+            const int x = 2 * i;
+            double2 v = *reinterpret_cast<double2*>(row + x);
+            *reinterpret_cast<double2*>(row + x) = make_double2(0.0, 0.0);
+            if (px) {
+              if (x < 2) {
+                v.x += row[x + nx];
+                v.y += row[x + 1 + nx];
+                row[x + nx] = 0.0;
+                row[x + 1 + nx] = 0.0;
+              }
+              if (x + 1 >= nx - 3) {
+                if (x >= nx - 3) { v.x += row[x - nx]; row[x - nx] = 0.0; }
+                v.y += row[x + 1 - nx];
+                row[x + 1 - nx] = 0.0;
+              }
+            }
+            *reinterpret_cast<double2*>(orow + x) = v;
           }
-          *reinterpret_cast<double2*>(out + ((size_t)t * ny + (size_t)(y0 + r)) * nx + x) = v;
+          if (!px && tid < kPadL + kPadR) {  // closed x: pads only collect dropped targets
+            const int pi = tid < kPadL ? tid - kPadL : nx + (tid - kPadL);
+            row[pi] = 0.0;
+          }
         }
       } else {
+        __syncthreads();
         for (int r = 0; r < rows; ++r) {
           const double* row = wp + r * T.nxp + kPadL;
           double* orow = out + ((size_t)t * ny + (size_t)(y0 + r)) * nx;
           for (int x = tid; x < nx; x += kSThreads) orow[x] = folded(row, x, nx, px);
         }
+        __syncthreads();
+        for (int i = tid; i < plane; i += kSThreads) wp[i] = 0.0;
       }
     }
-    ZS_TRACE(0, step, 1);
-    // Source-row table of plane s (warp 0).
-    const bool src_plane = g.periodic[2] ? true : (s >= -1 && s <= nz);
-    const bool sweep = s <= z1 + 1 && src_plane;
-    if (warp == 0) {
-      uint32_t len = 0, rb = 0;
-      if (sweep && lane < srows) {
-        const int cyu = y0 - 1 + lane;
-        int cyw = cyu;
-        bool ok = true;
-        if (g.periodic[1]) cyw = wrap_cell(cyu, ny);
-        else ok = cyu >= -1 && cyu <= ny;
-        if (ok) {
-          const int szw = g.periodic[2] ? wrap_cell(s, nz) : s;
-          const uint32_t rid = row_id(g, cyw, szw);
-          rb = __ldg(rowstart + rid);
-          len = __ldg(rowstart + rid + 1) - rb;
-        }
-      }
-      uint32_t incl = len;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-      const uint32_t excl = incl - len;
-      if (lane < kMaxRows) {
-        s_rb[lane] = rb;
-        s_pref[lane] = excl;
-      }
-      if (lane == 0) s_pref[kMaxRows] = total;
-      // Row-aligned chunks: warp w owns rows [wlo[w], wlo[w+1]); a row is
-      // never split across warps.
-      int lo = srows;
-      for (int w = 0; w <= kSWarps; ++w) {
-        const uint32_t target = (uint32_t)(((uint64_t)total * w) / kSWarps);
-        const uint32_t m = __ballot_sync(0xffffffffu, lane < srows && excl >= target);
-        const int j = (w == kSWarps || m == 0u) ? srows : __ffs(m) - 1;
-        if (lane == w) lo = j;
-      }
-      if (lane <= kSWarps) s_wlo[lane] = lo;
-      __syncwarp();
-      int gcount = 0;
-      if (lane < kSWarps) {
-        const int a = s_wlo[lane], b = s_wlo[lane + 1];
-        const uint32_t pts = (b > a) ? (s_pref[b] - s_pref[a]) : 0u;
-        gcount = (int)((pts + 32 * kBatches - 1) / (32 * kBatches));
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) gcount = max(gcount, __shfl_down_sync(0xffffffffu, gcount, o));
-      if (lane == 0) s_groups = gcount;
-    }
+    if (st == nsteps) break;
     __syncthreads();
-    ZS_TRACE(0, step, 2);
-    // (b) The flushed slot becomes plane s+1's slot: clear it.
-    if (flush) {
-      double2* wp = reinterpret_cast<double2*>(win + (t & 3) * plane);
-      for (int i = tid; i < (plane >> 1); i += kSThreads) wp[i] = make_double2(0.0, 0.0);
-    }
-    const int groups = s_groups;
-    const int wlo = s_wlo[warp], whi = s_wlo[warp + 1];
-    const uint32_t pbeg = s_pref[wlo], pend = s_pref[whi];
-    __syncthreads();
-    ZS_TRACE(0, step, 3);
-    if (groups == 0) continue;  // the next table build happens after a barrier
+    ZS_TRACE(0, st, 0);
 
-    for (int gi = 0; gi < groups; ++gi) {
-      // (c) Stage up to kBatches x 32 points of this warp's rows into registers.
-      SrcPoint P[kBatches];
-      int maxrank[kBatches];
-#pragma unroll
-      for (int b = 0; b < kBatches; ++b) {
-        const uint32_t p = pbeg + (uint32_t)(gi * kBatches + b) * 32u + (uint32_t)lane;
-        SrcPoint& q = P[b];
-        q.valid = p < pend;
-        q.cx = 0;
-        q.cyu = y0;
+    const uint32_t* pref = S.pref[st];
+    const uint32_t total = pref[srows];
+    for (uint32_t c = 0; c * kCap < total; ++c, ++item) {
+      const int slot = (int)(item % kStages);
+      mbar_wait(&S.bar[slot], (item / kStages) & 1u);
+      const uint32_t a = c * kCap, cnt = min((uint32_t)kCap, total - a);
+      // Row-aligned split of [a, a + cnt) among the warps (same on every thread).
+      int lo = 0, hi = 0, groups = 0;
+      {
+        int wl[kSWarps + 1];
+        const int jf = find_row(pref, srows, a);
+        const int jl = find_row(pref, srows, a + cnt - 1);
+        int j = jf;
+        for (int w = 0; w <= kSWarps; ++w) {
+          const uint32_t target = a + (uint32_t)(((uint64_t)cnt * w) / kSWarps);
+          while (j <= jl && max(pref[j], a) < target) ++j;
+          wl[w] = (w == kSWarps) ? (int)cnt
+                                 : (int)min(cnt, max(pref[min(j, jl + 1)], a) - a);
+          if (w == 0) wl[0] = 0;
+        }
+        for (int w = 0; w < kSWarps; ++w) groups = max(groups, (wl[w + 1] - wl[w] + 31) / 32);
+        lo = wl[warp];
+        hi = wl[warp + 1];
+      }
+      for (int gi = 0; gi < groups; ++gi) {
+        // (b) One point per lane from the ring: cell, weights, in-cell rank.
+        const int pl = lo + gi * 32 + lane;
+        const bool valid = pl < hi;
+        int cx = 0, cyu = y0;
         uint32_t key = 0xffffffffu;
-        if (q.valid) {
-          int j = wlo;
-          while (j + 1 < whi && s_pref[j + 1] <= p) ++j;
-          const uint32_t r = s_rb[j] + (p - s_pref[j]);
-          key = __ldg(skeys + r);
-          const uint32_t i = __ldg(perm + r);
-          q.cyu = y0 - 1 + j;
+        double gx[4], wy[4], wz[4];
+        if (valid) {
+          const double4 r = S.ring[slot][pl];
+          const int j = find_row(pref, srows, a + (uint32_t)pl);
+          cyu = y0 - 1 + j;
+          const double xx[3] = {r.x, r.y, r.z};
           double w[3][4];
+          int c3[3];
 #pragma unroll
-          for (int a = 0; a < 3; ++a) {
+          for (int ax = 0; ax < 3; ++ax) {
             double xw;
-            const int c = cell_of(g, a, __ldg(X + (size_t)i * 3 + a), &xw);
-            cosine_weights(displacement(g, a, xw, c), g.inv_h, w[a]);
-            if (a == 0) q.cx = px ? wrap_cell(c, nx) : c;
+            c3[ax] = cell_of(g, ax, xx[ax], &xw);
+            cosine_weights(displacement(g, ax, xw, c3[ax]), g.inv_h, w[ax]);
           }
-          const double gv = __ldg(G + i);
+          cx = px ? wrap_cell(c3[0], nx) : c3[0];
+          key = cell_key(g, c3);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            q.gx[k] = w[0][k] * gv;
-            q.wy[k] = w[1][k];
-            q.wz[k] = w[2][k];
+            gx[k] = w[0][k] * r.w;
+            wy[k] = w[1][k];
+            wz[k] = w[2][k];
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) q.gx[k] = q.wy[k] = q.wz[k] = 0.0;
+          for (int k = 0; k < 4; ++k) gx[k] = wy[k] = wz[k] = 0.0;
         }
-        // Points sharing a cell are adjacent lanes (keys are sorted): the
-        // head lane adds its followers' contributions before touching memory.
         const uint32_t pkey = __shfl_up_sync(0xffffffffu, key, 1);
-        const bool head = q.valid && (lane == 0 || pkey != key);
+        const bool head = valid && (lane == 0 || pkey != key);
         const uint32_t hm = __ballot_sync(0xffffffffu, head);
-        const uint32_t vm = __ballot_sync(0xffffffffu, q.valid);
-        q.rank = q.valid ? lane - (31 - __clz(hm & le)) : 1;
+        const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+        const int rank = valid ? lane - (31 - __clz(hm & le)) : 1;
         const uint32_t later = hm & ~le;
         const int next = later ? __ffs(later) - 1 : __popc(vm);
-        q.run_after = (head ? next - lane - 1 : 0);
-        maxrank[b] = __reduce_max_sync(0xffffffffu, (unsigned)q.run_after);
-      }
-      ZS_TRACE(0, step, 4);
-      // (d) Four sigma_y phases; within a phase distinct source rows hit
-      //     distinct target rows.
+        const int run_after = head ? next - lane - 1 : 0;
+        const int maxrank = __reduce_max_sync(0xffffffffu, (unsigned)run_after);
+        // (c) Four sigma_y phases: distinct source rows hit distinct target rows.
+#pragma unroll 1
+        for (int sy = -2; sy <= 1; ++sy) {
+          const int ty = cyu + sy;
+          const bool inrow = valid && ty >= y0 && ty < y1;
+          if (__ballot_sync(0xffffffffu, inrow) != 0u) {
+            const bool yok = inrow && rank == 0;
+            const int rowoff = yok ? (ty - y0) * T.nxp + cx + (kPadL - 2) : 0;
+            const double wyv = sy == -2 ? wy[0] : sy == -1 ? wy[1] : sy == 0 ? wy[2] : wy[3];
 #pragma unroll
-      for (int sy = -2; sy <= 1; ++sy) {
+            for (int sz = -2; sz <= 1; ++sz) {
+              const int tz = s + sz;
+              if (tz < z0 || tz >= z1) continue;  // warp-uniform
+              double* base = win + (tz & 3) * plane + rowoff;
+              const double a2 = wyv * wz[sz + 2];
+              if (maxrank == 0) {
 #pragma unroll
-        for (int b = 0; b < kBatches; ++b) {
-          const SrcPoint& q = P[b];
-          const int ty = q.cyu + sy;
-          const bool yok = q.valid && q.rank == 0 && ty >= y0 && ty < y1;
-          if (__ballot_sync(0xffffffffu, q.valid && ty >= y0 && ty < y1) == 0u) continue;
-          const int rowoff = yok ? (ty - y0) * T.nxp + q.cx + (kPadL - 2) : 0;
+                for (int k = 0; k < 4; ++k) {
+                  double* dst = yok ? base + k : dummy;
+                  *dst += gx[k] * a2;
+                  __syncwarp();
+                }
+              } else {
 #pragma unroll
-          for (int sz = -2; sz <= 1; ++sz) {
-            const int tz = s + sz;
-            if (tz < z0 || tz >= z1) continue;  // warp-uniform
-            double* base = win + (tz & 3) * plane + rowoff;
-            const double a = q.wy[sy + 2] * q.wz[sz + 2];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              double v = q.gx[k] * a;
-              for (int j = 1; j <= maxrank[b]; ++j) {
-                const double w = __shfl_down_sync(0xffffffffu, v, j);
-                if (j <= q.run_after) v += w;
+                for (int k = 0; k < 4; ++k) {
+                  double v = gx[k] * a2;
+                  for (int jj = 1; jj <= maxrank; ++jj) {
+                    const double w2 = __shfl_down_sync(0xffffffffu, v, jj);
+                    if (jj <= run_after) v += w2;
+                  }
+                  double* dst = yok ? base + k : dummy;
+                  *dst += v;
+                  __syncwarp();
+                }
               }
-              double* dst = yok ? base + k : dummy;
-              *dst += v;
-              __syncwarp();
             }
           }
+          __syncthreads();
         }
-        __syncthreads();
-        ZS_TRACE(0, step, 5 + (sy + 2 < 3 ? sy + 2 : 2));
       }
+      // The slot is free: prefetch work item item + kStages into it.
+      if (tid == 0) issue(item + kStages);
     }
   }
 }
