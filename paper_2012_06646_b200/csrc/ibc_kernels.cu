@@ -259,6 +259,147 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
   }
 }
 
+// ---------------------------------------------------------------- K4c
+// Barrier-free write-once spread over whole x rows (3-D and 2-D grids).
+// Warp w of a CTA owns ONE target row (ty, tz), kept in a private, padded
+// shared-memory row (x index + 4; periodic x wraps through the pad, folded
+// back at the end).  It pulls, in fixed (sigma_z, sigma_y) order, the sorted
+// points of the 16 source rows that reach it -- rows are contiguous ranges
+// of the key sort -- with each point's delta weights precomputed once
+// (prep_records_kernel).  Lanes in one batch come from one source row, so
+// distinct cells hit distinct targets; equal cells are adjacent lanes and
+// are serialized by rank.  No atomics, no CTA barriers, fixed summation
+// order: bitwise reproducible.  Every grid value is written once.
+struct RowTiling {
+  int ty, tz, nty, ntz, nxp, warps;
+};
+constexpr int kRowPad = 4;
+
+__global__ void __launch_bounds__(256) spread_rows_kernel(
+    DevGrid g, RowTiling T, const uint32_t* __restrict__ rowstart,
+    const int* __restrict__ rec_cx, const double* __restrict__ rec, uint32_t n,
+    double* __restrict__ out) {
+  extern __shared__ __align__(16) double srow[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const int by = blockIdx.x % T.nty, bz = blockIdx.x / T.nty;
+  const int ty = by * T.ty + warp % T.ty, tz = bz * T.tz + warp / T.ty;
+  double* row = srow + (size_t)warp * T.nxp;
+  double* dummy = srow + (size_t)T.warps * T.nxp + warp * 32 + lane;
+  if (ty >= ny || tz >= nz) return;  // warp-uniform; no CTA barriers below
+  for (int i = lane; i < T.nxp; i += 32) row[i] = 0.0;
+  *dummy = 0.0;
+  __syncwarp();
+  const uint32_t le = lanemask_le();
+  const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
+  const int sylo = g.dim >= 2 ? -2 : 0, syhi = g.dim >= 2 ? 1 : 0;
+  const bool px = g.periodic[0] != 0;
+  for (int sz = szlo; sz <= szhi; ++sz) {
+    int cz = 0;
+    if (g.dim >= 3) {
+      cz = tz - sz;
+      if (g.periodic[2]) cz = wrap_cell(cz, nz);
+      else if (cz < -1 || cz > nz) continue;
+    }
+    const double* wzc = rec + (size_t)(8 + sz + 2) * n;
+    for (int sy = sylo; sy <= syhi; ++sy) {
+      int cy = 0;
+      if (g.dim >= 2) {
+        cy = ty - sy;
+        if (g.periodic[1]) cy = wrap_cell(cy, ny);
+        else if (cy < -1 || cy > ny) continue;
+      }
+      const uint32_t rid = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
+                           (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(ny + 2) : 0u);
+      const uint32_t rb = __ldg(rowstart + rid), re = __ldg(rowstart + rid + 1);
+      const double* wyc = rec + (size_t)(4 + sy + 2) * n;
+      for (uint32_t base = rb; base < re; base += 32) {
+        const uint32_t r = base + lane;
+        const bool valid = r < re;
+        int cx = -0x40000000;
+        double a = 0.0, gk[4] = {0.0, 0.0, 0.0, 0.0};
+        if (valid) {
+          cx = __ldg(rec_cx + r);
+          a = __ldg(wyc + r) * __ldg(wzc + r);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) gk[k] = __ldg(rec + (size_t)k * n + r);
+        }
+        const int pcx = __shfl_up_sync(0xffffffffu, cx, 1);
+        const bool head = valid && (lane == 0 || pcx != cx);
+        const bool dup = __ballot_sync(0xffffffffu, valid && !head) != 0u;
+        double* p = row + (kRowPad - 2) + cx;
+        if (!dup) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            double* dst = valid ? p + k : dummy;
+            *dst += gk[k] * a;
+            __syncwarp();
+          }
+        } else {
+          const uint32_t hm = __ballot_sync(0xffffffffu, head);
+          const int rank = valid ? lane - (31 - __clz(hm & le)) : 0;
+          const int maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
+          for (int rr = 0; rr <= maxrank; ++rr) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              double* dst = (valid && rank == rr) ? p + k : dummy;
+              *dst += gk[k] * a;
+              __syncwarp();
+            }
+          }
+        }
+      }
+    }
+  }
+  // Fold the periodic x pad back and write the row (each element once).
+  const double* body = row + kRowPad;
+  double* orow = out + ((size_t)tz * ny + ty) * nx;
+  if ((nx & 1) == 0 && nx >= 4) {
+    for (int x = 2 * lane; x < nx; x += 64) {
+      double2 v = *reinterpret_cast<const double2*>(body + x);
+      if (px) {
+        if (x < 2) { v.x += body[x + nx]; v.y += body[x + 1 + nx]; }
+        if (x >= nx - 3) v.x += body[x - nx];
+        if (x + 1 >= nx - 3) v.y += body[x + 1 - nx];
+      }
+      *reinterpret_cast<double2*>(orow + x) = v;
+    }
+  } else {
+    for (int x = lane; x < nx; x += 32) {
+      double v = body[x];
+      if (px) {
+        for (int q = x - nx; q >= -3; q -= nx) v += body[q];
+        for (int q = x + nx; q <= nx + 1; q += nx) v += body[q];
+      }
+      orow[x] = v;
+    }
+  }
+}
+
+bool rows_tiling(const DevGrid& g, RowTiling& T) {
+  if (g.dim < 2) return false;
+  const int nx = g.n[0];
+  T.nxp = nx + kRowPad + 2;
+  if (T.nxp & 1) T.nxp += 1;
+  const size_t per_warp = ((size_t)T.nxp + 32) * sizeof(double);
+  int warps = 8;
+  while (warps > 1 && warps * per_warp > 200 * 1024) --warps;
+  if (warps * per_warp > 200 * 1024) return false;
+  if (g.dim >= 3) {
+    T.ty = warps >= 8 ? 4 : (warps >= 4 ? 2 : 1);
+    T.tz = std::max(1, std::min(warps / T.ty, 2));
+  } else {
+    T.ty = warps;
+    T.tz = 1;
+  }
+  T.ty = std::min(T.ty, g.n[1]);
+  T.tz = std::min(T.tz, g.n[2]);
+  T.warps = T.ty * T.tz;
+  T.nty = (g.n[1] + T.ty - 1) / T.ty;
+  T.ntz = (g.n[2] + T.tz - 1) / T.tz;
+  return true;
+}
+
 // ---------------------------------------------------------------- K5
 // One thread per point, visited in sorted (cell) order so neighbouring
 // threads gather neighbouring grid values; result stored at the point's
@@ -592,11 +733,8 @@ void PointScratch::release_all() {
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
-  zs::Tiling Z;
-  const bool zsweep = zsweep_tiling(g, false, Z);
   if (n > 0) {
-    sort_points(ctx, g, d_points, n, s, false,
-                zsweep ? sort::kPayloadSpread : sort::kPayloadNone, d_values);
+    sort_points(ctx, g, d_points, n, s, false);
   } else {
     IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
     s.last_n = 0;
@@ -611,30 +749,32 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   if (!attr_set[ctx.device & 63]) {
     IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(zs::spread_zsweep_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(zs::spread_zsweep_kernel,
-                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
+    IBC_CUDA(cudaFuncSetAttribute(spread_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  210 * 1024));
+    IBC_CUDA(cudaFuncSetAttribute(spread_rows_kernel,
                                   cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
+                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     attr_set[ctx.device & 63] = true;
   }
-  if (zsweep) {
+  if (n > 0) {
+    ctx.prof_begin(kProfPrep, &ev);
+    prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
+        g, d_points, d_values, s.sorted_perm, (uint32_t)n, s.rec_cx.p, s.rec.p);
+    ++ctx.launches;
+    ctx.prof_end(kProfPrep, ev);
+  }
+  RowTiling R;
+  if (rows_tiling(g, R)) {
     ctx.prof_begin(kProfSpread, &ev);
-    zs::spread_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kSThreads, zsweep_smem_bytes(Z, false), st>>>(
-        g, Z, s.rowstart.p, s.rec.p, d_out);
+    const size_t smem = (size_t)R.warps * ((size_t)R.nxp + 32) * sizeof(double);
+    spread_rows_kernel<<<(unsigned)(R.nty * R.ntz), 32 * R.warps, smem, st>>>(
+        g, R, s.rowstart.p, s.rec_cx.p, s.rec.p, (uint32_t)n, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   } else {
-    if (n > 0) {
-      ctx.prof_begin(kProfPrep, &ev);
-      prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
-          g, d_points, d_values, s.sorted_perm, (uint32_t)n, s.rec_cx.p, s.rec.p);
-      ++ctx.launches;
-      ctx.prof_end(kProfPrep, ev);
-    }
     const SpreadTiling T = choose_tiling(g);
     const size_t smem = (size_t)T.tx * T.ty * T.tz * sizeof(double);
     ctx.prof_begin(kProfSpread, &ev);

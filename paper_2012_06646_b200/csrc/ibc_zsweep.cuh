@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
     for (uint32_t c = 0; c * kCap < total; ++c, ++item) {
       const int slot = (int)(item % kStages);
       mbar_wait(&S.bar[slot], (item / kStages) & 1u);
+      ZS_TRACE(0, st, 1);
       const uint32_t a = c * kCap, cnt = min((uint32_t)kCap, total - a);
       // Row-aligned split of [a, a + cnt) among the warps (same on every thread).
       int lo = 0, hi = 0, groups = 0;
@@ -348,6 +349,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
         const int next = later ? __ffs(later) - 1 : __popc(vm);
         const int run_after = head ? next - lane - 1 : 0;
         const int maxrank = __reduce_max_sync(0xffffffffu, (unsigned)run_after);
+        ZS_TRACE(0, st, 2);
         // (c) Four sigma_y phases: distinct source rows hit distinct target rows.
 #pragma unroll 1
         for (int sy = -2; sy <= 1; ++sy) {
@@ -386,6 +388,7 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
             }
           }
           __syncthreads();
+          ZS_TRACE(0, st, 5 + sy);
         }
       }
       // The slot is free: prefetch work item item + kStages into it.
