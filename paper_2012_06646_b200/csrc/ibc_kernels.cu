@@ -275,6 +275,8 @@ struct RowTiling {
 };
 constexpr int kRowPad = 4;
 
+constexpr int kRowsPerWarp = 4;
+
 __global__ void __launch_bounds__(256) spread_rows_kernel(
     DevGrid g, RowTiling T, const uint32_t* __restrict__ rowstart,
     const int* __restrict__ rec_cx, const double* __restrict__ rec, uint32_t n,
@@ -283,17 +285,28 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int by = blockIdx.x % T.nty, bz = blockIdx.x / T.nty;
-  const int ty = by * T.ty + warp % T.ty, tz = bz * T.tz + warp / T.ty;
-  double* row = srow + (size_t)warp * T.nxp;
-  double* dummy = srow + (size_t)T.warps * T.nxp + warp * 32 + lane;
-  if (ty >= ny || tz >= nz) return;  // warp-uniform; no CTA barriers below
-  for (int i = lane; i < T.nxp; i += 32) row[i] = 0.0;
+  // Warp w owns target rows ty0 .. ty0+3 of plane tz (3-D: warps stack in z;
+  // 2-D: in y).
+  int ty0, tz;
+  if (g.dim >= 3) {
+    ty0 = by * kRowsPerWarp;
+    tz = bz * T.warps + warp;
+  } else {
+    ty0 = (by * T.warps + warp) * kRowsPerWarp;
+    tz = 0;
+  }
+  double* rows = srow + (size_t)warp * kRowsPerWarp * T.nxp;
+  double* dummy = srow + (size_t)T.warps * kRowsPerWarp * T.nxp + warp * 32 + lane;
+  if (ty0 >= ny || tz >= nz) return;  // warp-uniform; no CTA barriers below
+  const int nrow = min(kRowsPerWarp, ny - ty0);
+  for (int i = lane; i < kRowsPerWarp * T.nxp; i += 32) rows[i] = 0.0;
   *dummy = 0.0;
   __syncwarp();
   const uint32_t le = lanemask_le();
   const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
-  const int sylo = g.dim >= 2 ? -2 : 0, syhi = g.dim >= 2 ? 1 : 0;
   const bool px = g.periodic[0] != 0;
+  // Source rows cy in [ty0-1, ty0+nrow+1] (unwrapped); for dim 1 only cy = 0.
+  const int cylo = g.dim >= 2 ? ty0 - 1 : 0, cyhi = g.dim >= 2 ? ty0 + nrow + 1 : 0;
   for (int sz = szlo; sz <= szhi; ++sz) {
     int cz = 0;
     if (g.dim >= 3) {
@@ -302,48 +315,50 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
       else if (cz < -1 || cz > nz) continue;
     }
     const double* wzc = rec + (size_t)(8 + sz + 2) * n;
-    for (int sy = sylo; sy <= syhi; ++sy) {
-      int cy = 0;
+    for (int cyu = cylo; cyu <= cyhi; ++cyu) {
+      int cy = cyu;
       if (g.dim >= 2) {
-        cy = ty - sy;
-        if (g.periodic[1]) cy = wrap_cell(cy, ny);
-        else if (cy < -1 || cy > ny) continue;
+        if (g.periodic[1]) cy = wrap_cell(cyu, ny);
+        else if (cyu < -1 || cyu > ny) continue;
       }
       const uint32_t rid = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
                            (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(ny + 2) : 0u);
       const uint32_t rb = __ldg(rowstart + rid), re = __ldg(rowstart + rid + 1);
-      const double* wyc = rec + (size_t)(4 + sy + 2) * n;
       for (uint32_t base = rb; base < re; base += 32) {
         const uint32_t r = base + lane;
         const bool valid = r < re;
         int cx = -0x40000000;
-        double a = 0.0, gk[4] = {0.0, 0.0, 0.0, 0.0};
+        double gz[4] = {0.0, 0.0, 0.0, 0.0}, wy[4] = {0.0, 0.0, 0.0, 0.0};
         if (valid) {
           cx = __ldg(rec_cx + r);
-          a = __ldg(wyc + r) * __ldg(wzc + r);
+          const double wz = __ldg(wzc + r);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) gk[k] = __ldg(rec + (size_t)k * n + r);
+          for (int k = 0; k < 4; ++k) {
+            gz[k] = __ldg(rec + (size_t)k * n + r) * wz;
+            wy[k] = __ldg(rec + (size_t)(4 + k) * n + r);
+          }
         }
         const int pcx = __shfl_up_sync(0xffffffffu, cx, 1);
         const bool head = valid && (lane == 0 || pcx != cx);
         const bool dup = __ballot_sync(0xffffffffu, valid && !head) != 0u;
-        double* p = row + (kRowPad - 2) + cx;
-        if (!dup) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            double* dst = valid ? p + k : dummy;
-            *dst += gk[k] * a;
-            __syncwarp();
-          }
-        } else {
+        int rank = 0, maxrank = 0;
+        if (dup) {
           const uint32_t hm = __ballot_sync(0xffffffffu, head);
-          const int rank = valid ? lane - (31 - __clz(hm & le)) : 0;
-          const int maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
-          for (int rr = 0; rr <= maxrank; ++rr) {
+          rank = valid ? lane - (31 - __clz(hm & le)) : 0;
+          maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
+        }
+        for (int rr = 0; rr <= maxrank; ++rr) {
+          const bool on = valid && rank == rr;
+#pragma unroll
+          for (int i = 0; i < kRowsPerWarp; ++i) {
+            const int sy = g.dim >= 2 ? ty0 + i - cyu : 0;  // warp-uniform
+            if (i >= nrow || sy < -2 || sy > 1) continue;
+            const double wyv = sy == -2 ? wy[0] : sy == -1 ? wy[1] : sy == 0 ? wy[2] : wy[3];
+            double* p = rows + i * T.nxp + (kRowPad - 2) + cx;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              double* dst = (valid && rank == rr) ? p + k : dummy;
-              *dst += gk[k] * a;
+              double* dst = on ? p + k : dummy;
+              *dst += gz[k] * wyv;
               __syncwarp();
             }
           }
@@ -351,27 +366,29 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
       }
     }
   }
-  // Fold the periodic x pad back and write the row (each element once).
-  const double* body = row + kRowPad;
-  double* orow = out + ((size_t)tz * ny + ty) * nx;
-  if ((nx & 1) == 0 && nx >= 4) {
-    for (int x = 2 * lane; x < nx; x += 64) {
-      double2 v = *reinterpret_cast<const double2*>(body + x);
-      if (px) {
-        if (x < 2) { v.x += body[x + nx]; v.y += body[x + 1 + nx]; }
-        if (x >= nx - 3) v.x += body[x - nx];
-        if (x + 1 >= nx - 3) v.y += body[x + 1 - nx];
+  // Fold the periodic x pad back and write the rows (each element once).
+  for (int i = 0; i < nrow; ++i) {
+    const double* body = rows + i * T.nxp + kRowPad;
+    double* orow = out + ((size_t)tz * ny + (ty0 + i)) * nx;
+    if ((nx & 1) == 0 && nx >= 4) {
+      for (int x = 2 * lane; x < nx; x += 64) {
+        double2 v = *reinterpret_cast<const double2*>(body + x);
+        if (px) {
+          if (x < 2) { v.x += body[x + nx]; v.y += body[x + 1 + nx]; }
+          if (x >= nx - 3) v.x += body[x - nx];
+          if (x + 1 >= nx - 3) v.y += body[x + 1 - nx];
+        }
+        *reinterpret_cast<double2*>(orow + x) = v;
       }
-      *reinterpret_cast<double2*>(orow + x) = v;
-    }
-  } else {
-    for (int x = lane; x < nx; x += 32) {
-      double v = body[x];
-      if (px) {
-        for (int q = x - nx; q >= -3; q -= nx) v += body[q];
-        for (int q = x + nx; q <= nx + 1; q += nx) v += body[q];
+    } else {
+      for (int x = lane; x < nx; x += 32) {
+        double v = body[x];
+        if (px) {
+          for (int q = x - nx; q >= -3; q -= nx) v += body[q];
+          for (int q = x + nx; q <= nx + 1; q += nx) v += body[q];
+        }
+        orow[x] = v;
       }
-      orow[x] = v;
     }
   }
 }
@@ -381,22 +398,24 @@ bool rows_tiling(const DevGrid& g, RowTiling& T) {
   const int nx = g.n[0];
   T.nxp = nx + kRowPad + 2;
   if (T.nxp & 1) T.nxp += 1;
-  const size_t per_warp = ((size_t)T.nxp + 32) * sizeof(double);
+  const size_t per_warp = ((size_t)kRowsPerWarp * T.nxp + 32) * sizeof(double);
   int warps = 8;
   while (warps > 1 && warps * per_warp > 200 * 1024) --warps;
   if (warps * per_warp > 200 * 1024) return false;
+  T.ty = kRowsPerWarp;
+  T.tz = 1;
   if (g.dim >= 3) {
-    T.ty = warps >= 8 ? 4 : (warps >= 4 ? 2 : 1);
-    T.tz = std::max(1, std::min(warps / T.ty, 2));
+    warps = std::min(warps, g.n[2]);
+    T.warps = warps;
+    T.nty = (g.n[1] + kRowsPerWarp - 1) / kRowsPerWarp;
+    T.ntz = (g.n[2] + warps - 1) / warps;
   } else {
-    T.ty = warps;
-    T.tz = 1;
+    const int blocks_y = (g.n[1] + kRowsPerWarp - 1) / kRowsPerWarp;
+    warps = std::min(warps, blocks_y);
+    T.warps = warps;
+    T.nty = (blocks_y + warps - 1) / warps;
+    T.ntz = 1;
   }
-  T.ty = std::min(T.ty, g.n[1]);
-  T.tz = std::min(T.tz, g.n[2]);
-  T.warps = T.ty * T.tz;
-  T.nty = (g.n[1] + T.ty - 1) / T.ty;
-  T.ntz = (g.n[2] + T.tz - 1) / T.tz;
   return true;
 }
 
@@ -769,7 +788,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   RowTiling R;
   if (rows_tiling(g, R)) {
     ctx.prof_begin(kProfSpread, &ev);
-    const size_t smem = (size_t)R.warps * ((size_t)R.nxp + 32) * sizeof(double);
+    const size_t smem = (size_t)R.warps * ((size_t)kRowsPerWarp * R.nxp + 32) * sizeof(double);
     spread_rows_kernel<<<(unsigned)(R.nty * R.ntz), 32 * R.warps, smem, st>>>(
         g, R, s.rowstart.p, s.rec_cx.p, s.rec.p, (uint32_t)n, d_out);
     ++ctx.launches;
