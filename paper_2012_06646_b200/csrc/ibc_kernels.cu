@@ -277,6 +277,12 @@ constexpr int kRowPad = 4;
 
 constexpr int kRowsPerWarp = 4;
 
+// Skewed row layout: padded x index xi lives at xi + (xi >> 4).  Points of a
+// sparse row sit ~16 cells apart; without the skew all lanes of a warp would
+// hit the same shared-memory bank pair.
+__device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
+inline int skewed_len(int nxp) { return nxp + (nxp >> 4) + 2; }
+
 __global__ void __launch_bounds__(256) spread_rows_kernel(
     DevGrid g, RowTiling T, const uint32_t* __restrict__ rowstart,
     const int* __restrict__ rec_cx, const double* __restrict__ rec, uint32_t n,
@@ -296,11 +302,9 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
     tz = 0;
   }
   double* rows = srow + (size_t)warp * kRowsPerWarp * T.nxp;
-  double* dummy = srow + (size_t)T.warps * kRowsPerWarp * T.nxp + warp * 32 + lane;
   if (ty0 >= ny || tz >= nz) return;  // warp-uniform; no CTA barriers below
   const int nrow = min(kRowsPerWarp, ny - ty0);
   for (int i = lane; i < kRowsPerWarp * T.nxp; i += 32) rows[i] = 0.0;
-  *dummy = 0.0;
   __syncwarp();
   const uint32_t le = lanemask_le();
   const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
@@ -354,11 +358,11 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
             const int sy = g.dim >= 2 ? ty0 + i - cyu : 0;  // warp-uniform
             if (i >= nrow || sy < -2 || sy > 1) continue;
             const double wyv = sy == -2 ? wy[0] : sy == -1 ? wy[1] : sy == 0 ? wy[2] : wy[3];
-            double* p = rows + i * T.nxp + (kRowPad - 2) + cx;
+            double* rowi = rows + i * T.nxp;
+            const int xi = (kRowPad - 2) + cx;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-              double* dst = on ? p + k : dummy;
-              *dst += gz[k] * wyv;
+              if (on) rowi[skew(xi + k)] += gz[k] * wyv;
               __syncwarp();
             }
           }
@@ -368,27 +372,15 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
   }
   // Fold the periodic x pad back and write the rows (each element once).
   for (int i = 0; i < nrow; ++i) {
-    const double* body = rows + i * T.nxp + kRowPad;
+    const double* rowi = rows + i * T.nxp;
     double* orow = out + ((size_t)tz * ny + (ty0 + i)) * nx;
-    if ((nx & 1) == 0 && nx >= 4) {
-      for (int x = 2 * lane; x < nx; x += 64) {
-        double2 v = *reinterpret_cast<const double2*>(body + x);
-        if (px) {
-          if (x < 2) { v.x += body[x + nx]; v.y += body[x + 1 + nx]; }
-          if (x >= nx - 3) v.x += body[x - nx];
-          if (x + 1 >= nx - 3) v.y += body[x + 1 - nx];
-        }
-        *reinterpret_cast<double2*>(orow + x) = v;
+    for (int x = lane; x < nx; x += 32) {
+      double v = rowi[skew(x + kRowPad)];
+      if (px) {
+        for (int q = x - nx; q >= -3; q -= nx) v += rowi[skew(q + kRowPad)];
+        for (int q = x + nx; q <= nx + 1; q += nx) v += rowi[skew(q + kRowPad)];
       }
-    } else {
-      for (int x = lane; x < nx; x += 32) {
-        double v = body[x];
-        if (px) {
-          for (int q = x - nx; q >= -3; q -= nx) v += body[q];
-          for (int q = x + nx; q <= nx + 1; q += nx) v += body[q];
-        }
-        orow[x] = v;
-      }
+      orow[x] = v;
     }
   }
 }
@@ -396,9 +388,9 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
 bool rows_tiling(const DevGrid& g, RowTiling& T) {
   if (g.dim < 2) return false;
   const int nx = g.n[0];
-  T.nxp = nx + kRowPad + 2;
+  T.nxp = skewed_len(nx + kRowPad + 2);
   if (T.nxp & 1) T.nxp += 1;
-  const size_t per_warp = ((size_t)kRowsPerWarp * T.nxp + 32) * sizeof(double);
+  const size_t per_warp = (size_t)kRowsPerWarp * T.nxp * sizeof(double);
   int warps = 8;
   while (warps > 1 && warps * per_warp > 200 * 1024) --warps;
   if (warps * per_warp > 200 * 1024) return false;
@@ -637,26 +629,26 @@ size_t zsweep_smem_bytes(const zs::Tiling& T, bool interp) {
 // spread: window of 4 planes x ty rows (small, ~6 CTAs / SM);
 // interp: window of 4 planes x (ty + 5) rows.
 bool zsweep_tiling(const DevGrid& g, bool interp, zs::Tiling& T) {
-  if (g.dim != 3) return false;
+  if (g.dim != 3 || !interp) return false;
   const int nx = g.n[0];
-  T.nxp = nx + zs::kPadL + zs::kPadR;
+  const int rowlen = nx + zs::kPadL + zs::kPadR;
+  T.nxp = rowlen + (rowlen >> 4) + 2;
   if (T.nxp & 1) T.nxp += 1;
   const size_t row_bytes = (size_t)T.nxp * 8;
-  const size_t budget = interp ? 100 * 1024 : 34 * 1024;
-  const int extra = interp ? 5 : 0;
-  int ty = 16;
-  while (ty > 1 && 4 * (size_t)(ty + extra) * row_bytes > budget) --ty;
-  if (4 * (size_t)(ty + extra) * row_bytes > 160 * 1024) return false;
+  int ty = 8;
+  while (ty > 1 && (4 * (size_t)(ty + 5) * row_bytes > 110 * 1024 ||
+                    (size_t)(ty + 5) * rowlen > (size_t)zs::kIThreads * zs::kMaxPlaneVals))
+    --ty;
+  if (4 * (size_t)(ty + 5) * row_bytes > 200 * 1024 ||
+      (size_t)(ty + 5) * rowlen > (size_t)zs::kIThreads * zs::kMaxPlaneVals)
+    return false;
   ty = std::min(ty, g.n[1]);
-  if (ty < 1 || ty + 5 > zs::kMaxRows) return false;
   T.ty = ty;
   T.nty = (g.n[1] + ty - 1) / ty;
-  const size_t smem = zsweep_smem_bytes(T, interp);
-  const long per_sm = std::max<long>(1, std::min<long>(interp ? 8 : 16, (220L * 1024) / (long)smem));
-  // z chunks of >= 4 planes, enough CTAs to fill every SM about 1.5 times.
+  const size_t smem = zsweep_smem_bytes(T, true);
+  const long per_sm = std::max<long>(1, std::min<long>(8, (220L * 1024) / (long)smem));
   int zc = (int)std::max<long>(4, ((long)g.n[2] * T.nty * 2) / (148L * per_sm * 3));
   zc = std::min(zc, g.n[2]);
-  if (!interp) zc = std::min(zc, zs::kMaxSteps - 4);
   T.zc = zc;
   T.nzc = (g.n[2] + zc - 1) / zc;
   return true;
@@ -788,7 +780,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   RowTiling R;
   if (rows_tiling(g, R)) {
     ctx.prof_begin(kProfSpread, &ev);
-    const size_t smem = (size_t)R.warps * ((size_t)kRowsPerWarp * R.nxp + 32) * sizeof(double);
+    const size_t smem = (size_t)R.warps * kRowsPerWarp * R.nxp * sizeof(double);
     spread_rows_kernel<<<(unsigned)(R.nty * R.ntz), 32 * R.warps, smem, st>>>(
         g, R, s.rowstart.p, s.rec_cx.p, s.rec.p, (uint32_t)n, d_out);
     ++ctx.launches;
@@ -813,7 +805,7 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
   cudaStream_t st = ctx.stream;
   zs::Tiling Z;
   const bool zsweep = zsweep_tiling(g, true, Z);
-  sort_points(ctx, g, d_points, n, s, zsweep);
+  sort_points(ctx, g, d_points, n, s, zsweep, zsweep ? sort::kPayloadInterp : sort::kPayloadNone);
   cudaEvent_t ev = nullptr;
   if (zsweep) {
     row_table(ctx, g, n, s);
@@ -823,10 +815,9 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
       attr_set[ctx.device & 63] = true;
     }
-    const int use_bulk = ((g.n[0] & 1) == 0 && (reinterpret_cast<uintptr_t>(d_field) & 15) == 0) ? 1 : 0;
     ctx.prof_begin(kProfInterp, &ev);
     zs::interp_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem_bytes(Z, true), st>>>(
-        g, Z, s.rowstart.p, s.sorted_perm, d_points, d_field, d_out, use_bulk);
+        g, Z, s.rowstart.p, s.rec.p, d_field, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfInterp, ev);
   } else {

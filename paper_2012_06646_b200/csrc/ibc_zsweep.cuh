@@ -398,13 +398,17 @@ __global__ void __launch_bounds__(kSThreads) spread_zsweep_kernel(
 }
 
 // ------------------------------------------------------------------ interpolation
-__global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
-    DevGrid g, Tiling T, const uint32_t* __restrict__ rowstart, const uint32_t* __restrict__ perm,
-    const double* __restrict__ X, const double* __restrict__ field, double* __restrict__ out,
-    int use_bulk) {
-  extern __shared__ __align__(16) double fwin[];  // [4][frows][nxp]
-  __shared__ __align__(8) uint64_t s_bar[4];
+// Skewed row layout (see spread_rows_kernel): padded x index xi -> xi + xi/16,
+// so the gathers of points ~16 cells apart fall on distinct banks.
+__device__ __forceinline__ int iskew(int xi) { return xi + (xi >> 4); }
 
+constexpr int kIThreads = 256;
+constexpr int kMaxPlaneVals = 16;  // field values per thread per plane prefetch
+
+__global__ void __launch_bounds__(kIThreads) interp_zsweep_kernel(
+    DevGrid g, Tiling T, const uint32_t* __restrict__ rowstart, const double* __restrict__ rec,
+    const double* __restrict__ field, double* __restrict__ out) {
+  extern __shared__ __align__(16) double fwin[];  // [4][frows][nxp] (skewed rows)
   const int tid = threadIdx.x;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int by = blockIdx.x % T.nty, bz = blockIdx.x / T.nty;
@@ -417,133 +421,99 @@ __global__ void __launch_bounds__(kThreads) interp_zsweep_kernel(
   const int hz0 = (!g.periodic[2] && z0 == 0) ? -1 : z0;
   const int hz1 = (!g.periodic[2] && z1 == nz) ? nz + 1 : z1;
   const int frows = (hy1 - hy0) + 3;  // field rows hy0-2 .. hy1
+  const int rowlen = nx + kPadL + kPadR;  // padded x extent
   const int plane = frows * T.nxp;
+  const int pvals = frows * rowlen;
 
-  if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&s_bar[i], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  uint32_t parity = 0;  // bit i: phase parity of s_bar[i]
-
-  // Fill window slot for field plane t (unwrapped): row bodies by TMA bulk
-  // copy (or plain loads), zero rows outside closed axes.
-  auto load_plane = [&](int t) {
-    double* wp = fwin + (t & 3) * plane;
+  // Field plane t (unwrapped) -> registers (coalesced loads), then -> window.
+  double pre[kMaxPlaneVals];
+  auto fetch_plane = [&](int t) {
     const bool zin = g.periodic[2] || (t >= 0 && t < nz);
     const int tw = g.periodic[2] ? wrap_cell(t, nz) : t;
-    if (use_bulk && zin && tid == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      uint32_t bytes = 0;
-      for (int r = 0; r < frows; ++r) {
-        const int yu = hy0 - 2 + r;
-        if (g.periodic[1] || (yu >= 0 && yu < ny)) bytes += (uint32_t)nx * 8u;
-      }
-      mbar_expect_tx(&s_bar[t & 3], bytes);
-      for (int r = 0; r < frows; ++r) {
-        const int yu = hy0 - 2 + r;
-        if (!(g.periodic[1] || (yu >= 0 && yu < ny))) continue;
-        const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
-        bulk_g2s(wp + r * T.nxp + kPadL, field + ((size_t)tw * ny + yw) * nx, (uint32_t)nx * 8u,
-                 &s_bar[t & 3]);
-      }
-    }
-    // Everything the bulk copies do not write: all of each row without TMA,
-    // else only the x pads (zero here; periodic pads are copied from the
-    // row body once it has landed, see fill_pads).
-    const int total = frows * T.nxp;
-    for (int e = tid; e < total; e += kThreads) {
-      const int r = e / T.nxp, xi = e - r * T.nxp;
-      const int yu = hy0 - 2 + r;
-      const bool yin = g.periodic[1] || (yu >= 0 && yu < ny);
-      const int x = xi - kPadL;
-      const bool body = x >= 0 && x < nx;
-      if (use_bulk && zin && yin && (body || g.periodic[0])) continue;  // TMA / fill_pads
+#pragma unroll
+    for (int k = 0; k < kMaxPlaneVals; ++k) {
+      const int e = tid + k * kIThreads;
       double v = 0.0;
-      if (!use_bulk && zin && yin) {
-        const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
-        const double* src = field + ((size_t)tw * ny + yw) * nx;
-        if (body) v = __ldg(src + x);
-        else if (g.periodic[0]) v = __ldg(src + wrap_cell(x, nx));
+      if (e < pvals && zin) {
+        const int r = e / rowlen, xi = e - r * rowlen;
+        const int yu = hy0 - 2 + r, x = xi - kPadL;
+        const bool yin = g.periodic[1] || (yu >= 0 && yu < ny);
+        const bool xin = g.periodic[0] || (x >= 0 && x < nx);
+        if (yin && xin) {
+          const int yw = g.periodic[1] ? wrap_cell(yu, ny) : yu;
+          const int xw = g.periodic[0] ? wrap_cell(x, nx) : x;
+          v = __ldg(field + ((size_t)tw * ny + yw) * nx + xw);
+        }
       }
-      wp[e] = v;
+      pre[k] = v;
     }
   };
-  // Periodic x pads of bulk-copied rows, from the landed row bodies.
-  auto fill_pads = [&](int t) {
-    const bool zin = g.periodic[2] || (t >= 0 && t < nz);
-    if (!(use_bulk && zin && g.periodic[0])) return;
+  auto store_plane = [&](int t) {
     double* wp = fwin + (t & 3) * plane;
-    const int npad = kPadL + (T.nxp - kPadL - nx);
-    for (int e = tid; e < frows * npad; e += kThreads) {
-      const int r = e / npad, j = e - r * npad;
-      const int yu = hy0 - 2 + r;
-      if (!(g.periodic[1] || (yu >= 0 && yu < ny))) continue;
-      const int xi = j < kPadL ? j : nx + j;  // padded index
-      double* row = wp + r * T.nxp;
-      row[xi] = row[kPadL + wrap_cell(xi - kPadL, nx)];
-    }
-  };
-  auto wait_plane = [&](int t) {
-    const bool zin = g.periodic[2] || (t >= 0 && t < nz);
-    if (use_bulk && zin) {
-      mbar_wait(&s_bar[t & 3], (parity >> (t & 3)) & 1u);
-      parity ^= 1u << (t & 3);
+#pragma unroll
+    for (int k = 0; k < kMaxPlaneVals; ++k) {
+      const int e = tid + k * kIThreads;
+      if (e < pvals) {
+        const int r = e / rowlen, xi = e - r * rowlen;
+        wp[r * T.nxp + iskew(xi)] = pre[k];
+      }
     }
   };
 
-  for (int t = hz0 - 2; t <= hz0 + 1; ++t) load_plane(t);
-  for (int t = hz0 - 2; t <= hz0 + 1; ++t) wait_plane(t);
-  for (int t = hz0 - 2; t <= hz0 + 1; ++t) fill_pads(t);
+  for (int t = hz0 - 2; t <= hz0 + 1; ++t) {
+    fetch_plane(t);
+    store_plane(t);
+  }
   __syncthreads();
 
   for (int s = hz0; s < hz1; ++s) {
     const int step = s - hz0;
     ZS_TRACE(1, step, 0);
+    if (s + 2 < hz1 + 1) fetch_plane(s + 2);  // in flight during this step's gathers
     // Points homed in plane s, rows [hy0, hy1): one contiguous sorted range.
     const int szw = g.periodic[2] ? wrap_cell(s, nz) : s;
     const uint32_t rb = __ldg(rowstart + row_id(g, hy0, szw));
     const uint32_t re = __ldg(rowstart + row_id(g, hy1 - 1, szw) + 1);
-    for (uint32_t r = rb + tid; r < re; r += kThreads) {
-      const uint32_t i = __ldg(perm + r);
+    for (uint32_t r = rb + tid; r < re; r += kIThreads) {
+      const double2 q0 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r);
+      const double2 q1 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r + 1);
+      const uint32_t i = (uint32_t)__double_as_longlong(q1.y);
+      const double xx[3] = {q0.x, q0.y, q1.x};
       double w[3][4];
       int c[3];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
         double xw;
-        c[a] = cell_of(g, a, __ldg(X + (size_t)i * 3 + a), &xw);
+        c[a] = cell_of(g, a, xx[a], &xw);
         cosine_weights(displacement(g, a, xw, c[a]), g.inv_h, w[a]);
       }
       const int cx = g.periodic[0] ? wrap_cell(c[0], nx) : c[0];
       const int cy = g.periodic[1] ? wrap_cell(c[1], ny) : c[1];
-      double acc = 0.0;
+      double part[4];
 #pragma unroll
       for (int kz = 0; kz < 4; ++kz) {
         const double* pz = fwin + ((s + kz - 2) & 3) * plane;
+        double acc = 0.0;
 #pragma unroll
         for (int ky = 0; ky < 4; ++ky) {
-          const double* prow = pz + (cy - hy0 + ky) * T.nxp + cx + (kPadL - 2);
+          const double* prow = pz + (cy - hy0 + ky) * T.nxp;
 #pragma unroll
           for (int kx = 0; kx < 4; ++kx) {
             const double wt = (w[0][kx] * w[1][ky]) * w[2][kz];
-            acc += wt * prow[kx];
+            acc += wt * prow[iskew(cx + kx + (kPadL - 2))];
           }
         }
+        part[kz] = acc;
       }
-      out[i] = acc * g.hd;
+      out[i] = ((part[0] + part[1]) + (part[2] + part[3])) * g.hd;
     }
     ZS_TRACE(1, step, 1);
     if (s + 1 < hz1) {
       __syncthreads();  // everyone is done with plane s-2
-      ZS_TRACE(1, step, 2);
-      load_plane(s + 2);
-      ZS_TRACE(1, step, 3);
-      wait_plane(s + 2);
-      fill_pads(s + 2);
-      ZS_TRACE(1, step, 4);
+      store_plane(s + 2);
       __syncthreads();
-      ZS_TRACE(1, step, 5);
     }
+    ZS_TRACE(1, step, 2);
   }
 }
 
