@@ -387,15 +387,47 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
 #pragma unroll
       for (int i = 0; i < kRowsPerWarp; ++i)
         any_on[i] = leader && (__ballot_sync(0xffffffffu, on[i]) & grp) != 0u;
+      // Group members after the leader, lowest lane first (leaders only).
+      int mem[3] = {lane, lane, lane};
+      {
+        uint32_t rest = leader ? (grp & (grp - 1u)) : 0u;
+#pragma unroll
+        for (int m = 0; m < 3; ++m) {
+          if (rest) {
+            mem[m] = __ffs(rest) - 1;
+            rest &= rest - 1u;
+          }
+        }
+      }
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
 #pragma unroll
         for (int i = 0; i < kRowsPerWarp; ++i) {
           double v = gz[k] * wyv[i];
-          for (int m = 1; m < maxmem; ++m) {
-            const int src = leader && m < nmem ? (int)__fns(grp, 0, m + 1) : lane;
-            const double w = __shfl_sync(0xffffffffu, v, src);
-            if (leader && m < nmem) v += w;
+          if (maxmem > 1) {
+            // Groups of up to 4 lanes through registers, larger ones by a
+            // serial walk over the group (rare: clustered points).
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+              const double w = __shfl_sync(0xffffffffu, v, mem[m]);
+              if (leader && m + 1 < nmem) v += w;
+            }
+            if (maxmem > 4) {
+              uint32_t rest = grp;
+#pragma unroll 1
+              for (int m = 0; m < 4; ++m) rest &= rest - 1u;  // skip leader + 3
+              const double own = v;
+              (void)own;
+#pragma unroll 1
+              for (int m = 4; m < maxmem; ++m) {
+                const int src = (leader && rest) ? __ffs(rest) - 1 : lane;
+                const double w = __shfl_sync(0xffffffffu, gz[k] * wyv[i], src);
+                if (leader && rest) {
+                  v += w;
+                  rest &= rest - 1u;
+                }
+              }
+            }
           }
           if (any_on[i]) rows[i * T.nxp + addr[k]] += v;
         }
