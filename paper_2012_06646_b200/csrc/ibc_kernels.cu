@@ -429,6 +429,11 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
               }
             }
           }
+#ifdef IBC_DEBUG_BOUNDS
+          if (any_on[i] && (addr[k] < 0 || addr[k] >= T.nxp))
+            printf("spread_rows OOB: blk %d warp %d lane %d cx %d cyu %d j %d p %u total %u r %u\n",
+                   blockIdx.x, warp, lane, cx, cyu, j, p, total, r);
+#endif
           if (any_on[i]) rows[i * T.nxp + addr[k]] += v;
         }
         __syncwarp();
