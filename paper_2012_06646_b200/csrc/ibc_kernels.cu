@@ -430,6 +430,9 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
             }
           }
 #ifdef IBC_DEBUG_BOUNDS
+          if (any_on[i] && !(fabs(v) < 1e6))
+            printf("BIG v=%g warp %d lane %d i %d k %d cx %d cyu %d j %d p %u total %u r %u rbj %u pre %u nmem %d maxmem %d gz %g wy %g %g %g %g\n",
+                   v, warp, lane, i, k, cx, cyu, j, p, total, r, rbj, pre, nmem, maxmem, gz[k], wy[0], wy[1], wy[2], wy[3]);
           if (any_on[i] && (addr[k] < 0 || addr[k] >= T.nxp))
             printf("spread_rows OOB: blk %d warp %d lane %d cx %d cyu %d j %d p %u total %u r %u\n",
                    blockIdx.x, warp, lane, cx, cyu, j, p, total, r);
