@@ -306,10 +306,11 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
   const int nrow = min(kRowsPerWarp, ny - ty0);
   for (int i = lane; i < kRowsPerWarp * T.nxp; i += 32) rows[i] = 0.0;
   __syncwarp();
+  const uint32_t le = lanemask_le();
   const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
   const bool px = g.periodic[0] != 0;
-  // Source rows: unwrapped cy = ty0-1+j, j < nsrc (2-D/3-D); the whole grid row for 1-D.
-  const int nsrc = g.dim >= 2 ? nrow + 3 : 1;
+  // Source rows cy in [ty0-1, ty0+nrow+1] (unwrapped); for dim 1 only cy = 0.
+  const int cylo = g.dim >= 2 ? ty0 - 1 : 0, cyhi = g.dim >= 2 ? ty0 + nrow + 1 : 0;
   for (int sz = szlo; sz <= szhi; ++sz) {
     int cz = 0;
     if (g.dim >= 3) {
@@ -317,129 +318,55 @@ __global__ void __launch_bounds__(256) spread_rows_kernel(
       if (g.periodic[2]) cz = wrap_cell(cz, nz);
       else if (cz < -1 || cz > nz) continue;
     }
-    // Sorted ranges of the source rows; lane j holds row j.
-    uint32_t rb = 0, len = 0;
-    if (lane < nsrc) {
-      int cy = g.dim >= 2 ? ty0 - 1 + lane : 0;
-      bool ok = true;
-      if (g.dim >= 2) {
-        if (g.periodic[1]) cy = wrap_cell(cy, ny);
-        else ok = cy >= -1 && cy <= ny;
-      }
-      if (ok) {
-        const uint32_t rid = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
-                             (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(ny + 2) : 0u);
-        rb = __ldg(rowstart + rid);
-        len = __ldg(rowstart + rid + 1) - rb;
-      }
-    }
-    uint32_t incl = len;
-#pragma unroll
-    for (int o = 1; o < 8; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 7);
     const double* wzc = rec + (size_t)(8 + sz + 2) * n;
-    // Batches of 32 consecutive points of the concatenated source rows.
-    for (uint32_t base = 0; base < total; base += 32) {
-      const uint32_t p = base + lane;
-      const bool valid = p < total;
-      int j = 0;
-#pragma unroll
-      for (int q = 0; q < 7; ++q) {
-        const uint32_t end_q = __shfl_sync(0xffffffffu, incl, q);
-        j += (q < nsrc && p >= end_q) ? 1 : 0;
+    for (int cyu = cylo; cyu <= cyhi; ++cyu) {
+      int cy = cyu;
+      if (g.dim >= 2) {
+        if (g.periodic[1]) cy = wrap_cell(cyu, ny);
+        else if (cyu < -1 || cyu > ny) continue;
       }
-      const uint32_t rbj = __shfl_sync(0xffffffffu, rb, j & 31);
-      const uint32_t pre = __shfl_sync(0xffffffffu, incl - len, j & 31);
-      const uint32_t r = rbj + (p - pre);
-      int cx = -0x40000000 - lane;  // distinct per idle lane: never grouped
-      double gz[4] = {0.0, 0.0, 0.0, 0.0}, wy[4] = {0.0, 0.0, 0.0, 0.0};
-      if (valid) {
-        cx = __ldg(rec_cx + r);
-        const double wz = __ldg(wzc + r);
+      const uint32_t rid = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
+                           (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(ny + 2) : 0u);
+      const uint32_t rb = __ldg(rowstart + rid), re = __ldg(rowstart + rid + 1);
+      for (uint32_t base = rb; base < re; base += 32) {
+        const uint32_t r = base + lane;
+        const bool valid = r < re;
+        int cx = -0x40000000;
+        double gz[4] = {0.0, 0.0, 0.0, 0.0}, wy[4] = {0.0, 0.0, 0.0, 0.0};
+        if (valid) {
+          cx = __ldg(rec_cx + r);
+          const double wz = __ldg(wzc + r);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          gz[k] = __ldg(rec + (size_t)k * n + r) * wz;
-          wy[k] = __ldg(rec + (size_t)(4 + k) * n + r);
-        }
-      }
-      const int cyu = ty0 - 1 + j;  // unwrapped source row (2-D/3-D)
-      // Lanes with equal cx feed equal target x: the lowest lane of each group
-      // adds the others' values (fixed lane order) and writes alone.
-      const uint32_t grp = __match_any_sync(0xffffffffu, cx);
-      const bool leader = valid && (__ffs(grp) - 1) == lane;
-      const int nmem = valid ? __popc(grp) : 1;
-      const int maxmem = __reduce_max_sync(0xffffffffu, (unsigned)nmem);
-      int addr[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) addr[k] = skew((kRowPad - 2) + cx + k);
-      double wyv[kRowsPerWarp];
-      bool on[kRowsPerWarp];
-#pragma unroll
-      for (int i = 0; i < kRowsPerWarp; ++i) {
-        const int sy = g.dim >= 2 ? ty0 + i - cyu : 0;
-        on[i] = valid && i < nrow && sy >= -2 && sy <= 1;
-        wyv[i] = !on[i] ? 0.0 : sy == -2 ? wy[0] : sy == -1 ? wy[1] : sy == 0 ? wy[2] : wy[3];
-      }
-      bool any_on[kRowsPerWarp];
-#pragma unroll
-      for (int i = 0; i < kRowsPerWarp; ++i)
-        any_on[i] = leader && (__ballot_sync(0xffffffffu, on[i]) & grp) != 0u;
-      // Group members after the leader, lowest lane first (leaders only).
-      int mem[3] = {lane, lane, lane};
-      {
-        uint32_t rest = leader ? (grp & (grp - 1u)) : 0u;
-#pragma unroll
-        for (int m = 0; m < 3; ++m) {
-          if (rest) {
-            mem[m] = __ffs(rest) - 1;
-            rest &= rest - 1u;
+          for (int k = 0; k < 4; ++k) {
+            gz[k] = __ldg(rec + (size_t)k * n + r) * wz;
+            wy[k] = __ldg(rec + (size_t)(4 + k) * n + r);
           }
         }
-      }
+        const int pcx = __shfl_up_sync(0xffffffffu, cx, 1);
+        const bool head = valid && (lane == 0 || pcx != cx);
+        const bool dup = __ballot_sync(0xffffffffu, valid && !head) != 0u;
+        int rank = 0, maxrank = 0;
+        if (dup) {
+          const uint32_t hm = __ballot_sync(0xffffffffu, head);
+          rank = valid ? lane - (31 - __clz(hm & le)) : 0;
+          maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
+        }
+        for (int rr = 0; rr <= maxrank; ++rr) {
+          const bool on = valid && rank == rr;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+          for (int i = 0; i < kRowsPerWarp; ++i) {
+            const int sy = g.dim >= 2 ? ty0 + i - cyu : 0;  // warp-uniform
+            if (i >= nrow || sy < -2 || sy > 1) continue;
+            const double wyv = sy == -2 ? wy[0] : sy == -1 ? wy[1] : sy == 0 ? wy[2] : wy[3];
+            double* rowi = rows + i * T.nxp;
+            const int xi = (kRowPad - 2) + cx;
 #pragma unroll
-        for (int i = 0; i < kRowsPerWarp; ++i) {
-          double v = gz[k] * wyv[i];
-          if (maxmem > 1) {
-            // Groups of up to 4 lanes through registers, larger ones by a
-            // serial walk over the group (rare: clustered points).
-#pragma unroll
-            for (int m = 0; m < 3; ++m) {
-              const double w = __shfl_sync(0xffffffffu, v, mem[m]);
-              if (leader && m + 1 < nmem) v += w;
-            }
-            if (maxmem > 4) {
-              uint32_t rest = grp;
-#pragma unroll 1
-              for (int m = 0; m < 4; ++m) rest &= rest - 1u;  // skip leader + 3
-              const double own = v;
-              (void)own;
-#pragma unroll 1
-              for (int m = 4; m < maxmem; ++m) {
-                const int src = (leader && rest) ? __ffs(rest) - 1 : lane;
-                const double w = __shfl_sync(0xffffffffu, gz[k] * wyv[i], src);
-                if (leader && rest) {
-                  v += w;
-                  rest &= rest - 1u;
-                }
-              }
+            for (int k = 0; k < 4; ++k) {
+              if (on) rowi[skew(xi + k)] += gz[k] * wyv;
+              __syncwarp();
             }
           }
-#ifdef IBC_DEBUG_BOUNDS
-          if (any_on[i] && !(fabs(v) < 1e6))
-            printf("BIG v=%g warp %d lane %d i %d k %d cx %d cyu %d j %d p %u total %u r %u rbj %u pre %u nmem %d maxmem %d gz %g wy %g %g %g %g\n",
-                   v, warp, lane, i, k, cx, cyu, j, p, total, r, rbj, pre, nmem, maxmem, gz[k], wy[0], wy[1], wy[2], wy[3]);
-          if (any_on[i] && (addr[k] < 0 || addr[k] >= T.nxp))
-            printf("spread_rows OOB: blk %d warp %d lane %d cx %d cyu %d j %d p %u total %u r %u\n",
-                   blockIdx.x, warp, lane, cx, cyu, j, p, total, r);
-#endif
-          if (any_on[i]) rows[i * T.nxp + addr[k]] += v;
         }
-        __syncwarp();
       }
     }
   }
