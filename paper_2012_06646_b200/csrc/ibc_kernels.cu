@@ -18,6 +18,8 @@
 #include "ibc_internal.h"
 #include "ibc_sort.cuh"
 #include "ibc_zsweep.cuh"
+#include "ibc_sweep.cuh"
+#include "ibc_tma.cuh"
 
 namespace ibc {
 
@@ -799,9 +801,98 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   ++ctx.spread_calls;
 }
 
+namespace {
+
+// Tiling of the TMA interpolation sweep (3-D, nx % 16 == 0, nx <= 4096).
+bool interp_tma_tiling(const DevGrid& g, sw::InterpTiling& T) {
+  if (g.dim != 3) return false;
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  if (nx % 16 != 0 || nx > 4096) return false;
+  T.pitch = (uint32_t)((nx * 8 + 1023) & ~1023);
+  auto frmax_for = [&](int ty) {
+    const int nty = (ny + ty - 1) / ty;
+    const int ghosts = g.periodic[1] ? 0 : (nty == 1 ? 2 : 1);
+    return ty + 3 + ghosts;
+  };
+  // Two CTAs per SM when the slots allow it.
+  int ty = 16;
+  while (ty > 1 && (size_t)sw::kISlots * frmax_for(ty) * T.pitch > 110 * 1024) --ty;
+  ty = std::min(ty, ny);
+  T.ty = ty;
+  T.frmax = frmax_for(ty);
+  T.slot_bytes = (uint32_t)T.frmax * T.pitch;
+  if ((size_t)sw::kISlots * T.slot_bytes + 2048 > 227 * 1024) return false;
+  T.nty = (ny + ty - 1) / ty;
+  const long per_sm = std::max<long>(1, (227L * 1024) / ((long)sw::kISlots * T.slot_bytes + 2048));
+  const long want = 148L * per_sm;
+  int zc = (int)std::max<long>(4, ((long)nz * T.nty + want - 1) / want);
+  zc = std::min(zc, nz);
+  T.zc = zc;
+  T.nzc = (nz + zc - 1) / zc;
+  return true;
+}
+
+size_t interp_tma_smem(const sw::InterpTiling& T) {
+  return 8 * sw::kISlots + 1024 + (size_t)sw::kISlots * T.slot_bytes;
+}
+
+}  // namespace
+
+namespace tma {
+bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        !p)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  if (reinterpret_cast<uintptr_t>(field) % 16 != 0) return false;
+  const cuuint64_t dims[4] = {16, (cuuint64_t)(nx / 16), (cuuint64_t)ny, (cuuint64_t)nz};
+  const cuuint64_t strides[3] = {128, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+  const cuuint32_t box[4] = {16, (cuuint32_t)(nx / 16), 1, 1};
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(field), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace tma
+
+namespace {
+bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
+                     size_t n, PointScratch& s, double* d_out) {
+  sw::InterpTiling T;
+  if (!interp_tma_tiling(g, T)) return false;
+  CUtensorMap map;
+  if (!tma::encode_rows_map(&map, d_field, g.n[0], g.n[1], g.n[2])) return false;
+  cudaStream_t st = ctx.stream;
+  sort_points(ctx, g, d_points, n, s, true, sort::kPayloadInterp);
+  row_table(ctx, g, n, s);
+  const size_t smem = interp_tma_smem(T);
+  static bool attr_set[64] = {};
+  if (!attr_set[ctx.device & 63]) {
+    IBC_CUDA(cudaFuncSetAttribute(sw::interp_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  227 * 1024));
+    attr_set[ctx.device & 63] = true;
+  }
+  cudaEvent_t ev = nullptr;
+  ctx.prof_begin(kProfInterp, &ev);
+  sw::interp_tma_kernel<<<(unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st>>>(
+      g, T, map, s.rowstart.p, s.rec.p, d_out);
+  ++ctx.launches;
+  ctx.prof_end(kProfInterp, ev);
+  IBC_CUDA(cudaGetLastError());
+  ++ctx.interp_calls;
+  return true;
+}
+}  // namespace
+
 void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
                      size_t n, PointScratch& s, double* d_out) {
   if (n == 0) return;
+  if (interp_tma_path(ctx, g, d_field, d_points, n, s, d_out)) return;
   cudaStream_t st = ctx.stream;
   zs::Tiling Z;
   const bool zsweep = zsweep_tiling(g, true, Z);

@@ -1,0 +1,83 @@
+// ibc_tma.cuh -- TMA / mbarrier helpers for sm_100a and the host-side
+// tensor-map encoder (driver entry point fetched through the runtime, so the
+// library does not link libcuda directly).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <cstdint>
+
+namespace ibc {
+namespace tma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// Order earlier generic-proxy shared-memory accesses before later async-proxy
+// (TMA) writes to the same buffer.
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// 4-D tiled TMA load (coordinates innermost first) completing on `bar`.
+__device__ __forceinline__ void load_4d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                        int c3, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+// 1-D bulk copy global -> shared completing on `bar` (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+// Byte offset of double x inside a 1024-byte-aligned row written by a TMA box
+// with CU_TENSOR_MAP_SWIZZLE_128B: 16-byte chunk c of 128-byte line L lands at
+// chunk c ^ (L & 7).  Rows are placed at multiples of 1024 bytes, so L & 7
+// depends on x alone.
+__device__ __forceinline__ uint32_t swz128(int x) {
+  const uint32_t line = (uint32_t)x >> 4, chunk = ((uint32_t)x >> 1) & 7u;
+  return (line << 7) | ((chunk ^ (line & 7u)) << 4) | (((uint32_t)x & 1u) << 3);
+}
+
+// Host: field rows of an (nx, ny, nz) colex FP64 grid as a 4-D tensor
+// (16, nx/16, ny, nz) with a one-row box (16, nx/16, 1, 1), 128-byte swizzle,
+// zero fill out of bounds.  Requires nx % 16 == 0, nx <= 4096.
+bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz);
+
+}  // namespace tma
+}  // namespace ibc
