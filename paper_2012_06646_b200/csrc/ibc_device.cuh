@@ -68,6 +68,45 @@ __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double
   return (int)ceil(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]));
 }
 
+// One axis of a DevGrid picked with a runtime index (selects, so the grid
+// stays in the parameter bank instead of being copied to local memory).
+struct Axis {
+  double o, len, alpha;
+  int n, periodic;
+};
+
+__device__ __forceinline__ Axis axis_of(const DevGrid& g, int a) {
+  Axis r;
+  r.o = a == 0 ? g.origin[0] : (a == 1 ? g.origin[1] : g.origin[2]);
+  r.len = a == 0 ? g.len[0] : (a == 1 ? g.len[1] : g.len[2]);
+  r.alpha = a == 0 ? g.alpha[0] : (a == 1 ? g.alpha[1] : g.alpha[2]);
+  r.n = a == 0 ? g.n[0] : (a == 1 ? g.n[1] : g.n[2]);
+  r.periodic = a == 0 ? g.periodic[0] : (a == 1 ? g.periodic[1] : g.periodic[2]);
+  return r;
+}
+
+// cell_of + displacement for an Axis: returns the home cell (wrapped on a
+// periodic axis) and u = -t in [0, 1) (t = displacement ratio).
+__device__ __forceinline__ int cell_and_u(const Axis& A, double h, double inv_h, double x, double* u) {
+  double w = x;
+  if (A.periodic) {
+    const double d = __dsub_rn(x, A.o);
+    double r = fabs(d) < A.len ? d : fmod(d, A.len);
+    if (r < 0.0) r = __dadd_rn(r, A.len);
+    w = __dadd_rn(A.o, r);
+  }
+  const double d = __dsub_rn(w, A.o);
+  const double q = __dmul_rn(d, inv_h);
+  const double t = __dsub_rn(q, A.alpha);
+  double c = ceil(t);
+  const double margin = 1e-13 * (fabs(q) + 1.0);
+  if (!(c - t > margin && t - (c - 1.0) > margin)) c = ceil(__dsub_rn(__ddiv_rn(d, h), A.alpha));
+  const int ci = (int)c;
+  const double hp = __dadd_rn(__dmul_rn(h, __dadd_rn(c, A.alpha)), A.o);
+  *u = -((w - hp) * inv_h);
+  return A.periodic ? wrap_cell(ci, A.n) : ci;
+}
+
 // displacement_ratio (support_window.hpp:48-55): (xw - h*(i+alpha) - o) / h.
 // Only feeds the weights (not bit-exact anyway): multiply by 1/h.
 __device__ __forceinline__ double displacement(const DevGrid& g, int a, double xw, int c) {

@@ -14,6 +14,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstdio>
 
 #include "ibc_internal.h"
 #include "ibc_sort.cuh"
@@ -804,42 +806,65 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
 namespace {
 
 // Tiling of the TMA interpolation sweep (3-D, nx % 16 == 0, nx <= 4096).
-bool interp_tma_tiling(const DevGrid& g, sw::InterpTiling& T) {
+bool interp_tma_tiling(const DevGrid& g, size_t n, sw::InterpTiling& T) {
   if (g.dim != 3) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   if (nx % 16 != 0 || nx > 4096) return false;
-  T.pitch = (uint32_t)((nx * 8 + 1023) & ~1023);
-  auto frmax_for = [&](int ty) {
+  const uint32_t pitch = (uint32_t)((nx * 8 + 1023) & ~1023);
+  const int sms = 148;
+  // Pick TY (home rows per CTA) minimising the bytes one SM streams, with at
+  // least 3 planes in flight (slots >= 7) when possible and one CTA per SM.
+  double best = 1e300;
+  bool found = false;
+  for (int ty = 1; ty <= std::min(ny, 32); ++ty) {
     const int nty = (ny + ty - 1) / ty;
     const int ghosts = g.periodic[1] ? 0 : (nty == 1 ? 2 : 1);
-    return ty + 3 + ghosts;
-  };
-  // Two CTAs per SM when the slots allow it.
-  int ty = 16;
-  while (ty > 1 && (size_t)sw::kISlots * frmax_for(ty) * T.pitch > 110 * 1024) --ty;
-  ty = std::min(ty, ny);
-  T.ty = ty;
-  T.frmax = frmax_for(ty);
-  T.slot_bytes = (uint32_t)T.frmax * T.pitch;
-  if ((size_t)sw::kISlots * T.slot_bytes + 2048 > 227 * 1024) return false;
-  T.nty = (ny + ty - 1) / ty;
-  const long per_sm = std::max<long>(1, (227L * 1024) / ((long)sw::kISlots * T.slot_bytes + 2048));
-  const long want = 148L * per_sm;
-  int zc = (int)std::max<long>(4, ((long)nz * T.nty + want - 1) / want);
-  zc = std::min(zc, nz);
-  T.zc = zc;
-  T.nzc = (nz + zc - 1) / zc;
+    const int fr = ty + 3 + ghosts;
+    const long chunks = std::max<long>(1, sms / nty);
+    int zc = (int)std::max<long>(4, (nz + chunks - 1) / chunks);
+    zc = std::min(zc, nz);
+    const int hmax = zc + 2;
+    // Records staged per step: twice the mean points per step, 64..1024.
+    const double mean = (double)n * (ty + ghosts) / ((double)(ny + 2) * (nz + 2));
+    int cap = (int)std::min(1024.0, std::max(64.0, 2.0 * mean + 32.0));
+    cap = (cap + 31) & ~31;
+    const uint32_t stride = (uint32_t)(((size_t)fr * pitch + (size_t)cap * 32 + 1023) & ~size_t(1023));
+    const size_t budget = 226 * 1024 - 16 * sw::kMaxSlots - 12 * (size_t)hmax - 1024;
+    const int slots = (int)std::min<size_t>(sw::kMaxSlots, budget / stride);
+    if (slots < 5) continue;
+    const long ctas = (long)nty * ((nz + zc - 1) / zc);
+    const long waves = (ctas + sms - 1) / sms;
+    double cost = (double)waves * (zc + 3) * fr;
+    if (slots < 7) cost *= 1.0 + 0.15 * (7 - slots);  // shallow ring: exposed TMA latency
+    if (cost < best) {
+      best = cost;
+      found = true;
+      T.ty = ty;
+      T.frmax = fr;
+      T.slots = slots;
+      T.nty = nty;
+      T.zc = zc;
+      T.nzc = (nz + zc - 1) / zc;
+      T.rec_cap = cap;
+      T.hmax = hmax;
+      T.slot_stride = stride;
+    }
+  }
+  if (!found) return false;
+  T.pitch = pitch;
+  T.slot_bytes = (uint32_t)T.frmax * pitch;
+  T.box_ok = nx % 128 == 0 ? 1 : 0;  // box rows keep the 128B-swizzle phase
   return true;
 }
 
 size_t interp_tma_smem(const sw::InterpTiling& T) {
-  return 8 * sw::kISlots + 1024 + (size_t)sw::kISlots * T.slot_bytes;
+  return 16 * sw::kMaxSlots + 12 * (size_t)T.hmax + 1024 + (size_t)T.slots * T.slot_stride;
 }
 
 }  // namespace
 
 namespace tma {
-bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz) {
+bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz, int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -852,7 +877,7 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
   if (reinterpret_cast<uintptr_t>(field) % 16 != 0) return false;
   const cuuint64_t dims[4] = {16, (cuuint64_t)(nx / 16), (cuuint64_t)ny, (cuuint64_t)nz};
   const cuuint64_t strides[3] = {128, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
-  const cuuint32_t box[4] = {16, (cuuint32_t)(nx / 16), 1, 1};
+  const cuuint32_t box[4] = {16, (cuuint32_t)(nx / 16), (cuuint32_t)box_rows, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(field), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -864,9 +889,11 @@ namespace {
 bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
                      size_t n, PointScratch& s, double* d_out) {
   sw::InterpTiling T;
-  if (!interp_tma_tiling(g, T)) return false;
+  if (!interp_tma_tiling(g, n, T)) return false;
   CUtensorMap map;
   if (!tma::encode_rows_map(&map, d_field, g.n[0], g.n[1], g.n[2])) return false;
+  CUtensorMap map_box;
+  if (!tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax)) return false;
   cudaStream_t st = ctx.stream;
   sort_points(ctx, g, d_points, n, s, true, sort::kPayloadInterp);
   row_table(ctx, g, n, s);
@@ -880,7 +907,7 @@ bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, cons
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfInterp, &ev);
   sw::interp_tma_kernel<<<(unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st>>>(
-      g, T, map, s.rowstart.p, s.rec.p, d_out);
+      g, T, map, map_box, s.rowstart.p, s.rec.p, d_out);
   ++ctx.launches;
   ctx.prof_end(kProfInterp, ev);
   IBC_CUDA(cudaGetLastError());

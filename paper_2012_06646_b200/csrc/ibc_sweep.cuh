@@ -4,16 +4,25 @@
 // Alg. 3).  Points arrive sorted by their home row (cy, cz), each as a 32-byte
 // record {x, y, z, input index} written by the last radix pass.
 //
-// A CTA owns TY home rows [y0, y0 + TY) of a z-chunk [z0, z1) and sweeps its
-// home planes in order.  The field planes a home plane s needs (s-2 .. s+1,
-// rows y0-2 .. y0+TY) live in a ring of kISlots shared-memory slots, each
-// filled by one TMA tensor load per field row (128-byte swizzle; periodic
-// rows/planes are wrapped by the producer, non-periodic ones fall outside the
-// tensor and arrive zero-filled -- exactly the reference's skipped
-// `invalid_offset` terms).  While the CTA gathers plane s, the TMA engine
-// streams plane s+3 into the slot plane s-2 vacates; the CTA's only barrier
-// per plane is the one that frees that slot.  Every field value is read from
-// HBM once per CTA column (plus the 3-row y halo), every point once.
+// A CTA (one per SM) owns TY home rows [y0, y0 + TY) of a z-chunk [z0, z1)
+// and sweeps its home planes in order.  The field planes a home plane s needs
+// (s-2 .. s+1, rows y0-2 .. y0+TY) live in a ring of `slots` shared-memory
+// slots.  A dedicated producer warp fills slot i % slots with field plane i --
+// one TMA tensor load per plane (128-byte swizzle; per field row where the
+// rows wrap around a periodic y boundary), plus one bulk copy of the point
+// records of the step that plane completes -- and signals a `full` mbarrier.
+// Periodic rows/planes are wrapped by the producer; non-periodic ones fall
+// outside the tensor and arrive zero-filled, exactly the reference's skipped
+// `invalid_offset` terms.  Consumer warps release a plane on its `empty`
+// mbarrier after the last step that reads it; there is no CTA-wide barrier
+// in the sweep, so warps drift across steps and the TMA engine streams
+// slots - 4 planes ahead of the slowest warp.
+//
+// Gather layout: four lanes per point, lane k reading x = cx + k - 2 of every
+// (y, z) window row; the quad's partial sums are combined with two
+// xor-shuffles.  Lanes 0..2 of a quad compute the cell and sin/cos of one axis
+// each and share them.  Groups of 8 points are dealt round-robin to the
+// consumer warps across steps, so no warp is systematically the last one.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -24,39 +33,45 @@
 namespace ibc {
 namespace sw {
 
-constexpr int kIThreads = 256;
-constexpr int kISlots = 5;  // 4 planes in use + 1 in flight
+constexpr int kIConsumers = 16;                    // consumer warps
+constexpr int kIThreads = 32 * (kIConsumers + 1);  // + 1 producer warp
+constexpr int kMaxSlots = 16;
 
 struct InterpTiling {
   int ty, zc, nty, nzc;
-  int frmax;            // field rows per slot (ty + 3, + 1 ghost row on closed y)
-  uint32_t pitch;       // bytes per field row in shared memory (multiple of 1024)
-  uint32_t slot_bytes;  // frmax * pitch
+  int frmax;             // field rows per slot (ty + 3, + ghost rows on closed y)
+  int slots;             // ring depth (>= 5)
+  uint32_t pitch;        // bytes per field row in shared memory (multiple of 1024)
+  uint32_t slot_bytes;   // frmax * pitch
+  int rec_cap;           // point records staged per step (32 B each)
+  int hmax;              // max home planes per CTA (row-range table entries)
+  uint32_t slot_stride;  // slot_bytes + rec_cap * 32, rounded up to 1024
+  int box_ok;            // one TMA per plane allowed (nx % 128 == 0)
 };
 
 __device__ __forceinline__ uint32_t row_id(const DevGrid& g, int cyw, int czw) {
   return (uint32_t)(cyw + 1) + (uint32_t)(czw + 1) * (uint32_t)(g.n[1] + 2);
 }
 
-// Cell (unwrapped) and the four delta weights phi(sigma - t) / h of one axis.
-__device__ __forceinline__ int axis_weights(const DevGrid& g, int a, double x, double w[4]) {
-  double xw;
-  const int c = cell_of(g, a, x, &xw);
-  cosine_weights(displacement(g, a, xw, c), g.inv_h, w);
-  return c;
+__device__ __forceinline__ double shfl_d(double v, int src) {
+  return __shfl_sync(0xffffffffu, v, src);
 }
 
-__global__ void __launch_bounds__(kIThreads) interp_tma_kernel(
-    DevGrid g, InterpTiling T, const __grid_constant__ CUtensorMap tmap,
-    const uint32_t* __restrict__ rowstart, const double* __restrict__ rec,
-    double* __restrict__ out) {
+__global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
+    DevGrid g, InterpTiling T, const __grid_constant__ CUtensorMap tmap_row,
+    const __grid_constant__ CUtensorMap tmap_box, const uint32_t* __restrict__ rowstart,
+    const double* __restrict__ rec, double* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // Layout: full[kMaxSlots] | empty[kMaxSlots] | step table [3][hmax] |
+  // ring of 1024-aligned slots (field rows of one plane + records of one step).
   const uint32_t raw = tma::smem_u32(smem_raw);
-  const uint32_t bar0 = raw;  // kISlots mbarriers
-  const uint32_t base = (raw + 8u * kISlots + 1023u) & ~1023u;
+  const uint32_t full0 = raw, empty0 = raw + 8u * kMaxSlots;
+  uint32_t* rs = reinterpret_cast<uint32_t*>(smem_raw + 16 * kMaxSlots);
+  const uint32_t base = (raw + 16u * kMaxSlots + 12u * T.hmax + 1023u) & ~1023u;
   const unsigned char* slots = smem_raw + (base - raw);
+  const int NS = T.slots;
 
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int by = blockIdx.x % T.nty, bz = blockIdx.x / T.nty;
   const int y0 = by * T.ty, y1 = min(y0 + T.ty, ny);
@@ -67,96 +82,153 @@ __global__ void __launch_bounds__(kIThreads) interp_tma_kernel(
   const int hy1 = (!g.periodic[1] && y1 == ny) ? ny + 1 : y1;
   const int hz0 = (!g.periodic[2] && z0 == 0) ? -1 : z0;
   const int hz1 = (!g.periodic[2] && z1 == nz) ? nz + 1 : z1;
-  const int fr = hy1 - hy0 + 3;           // field rows hy0-2 .. hy1
-  const int nplanes = hz1 - hz0 + 3;      // field planes hz0-2 .. hz1
-  const uint32_t plane_bytes = (uint32_t)fr * (uint32_t)nx * 8u;
+  const int fr = hy1 - hy0 + 3;       // field rows hy0-2 .. hy1
+  const int nplanes = hz1 - hz0 + 3;  // field planes hz0-2 .. hz1
+  const int H = hz1 - hz0;            // home planes (steps)
+  // One box load per plane unless the rows wrap around a periodic y edge.
+  const bool box = T.box_ok && (!g.periodic[1] || (hy0 - 2 >= 0 && hy1 < ny));
+  const uint32_t plane_bytes = (uint32_t)(box ? T.frmax : fr) * (uint32_t)nx * 8u;
 
   if (tid == 0) {
-    for (int i = 0; i < kISlots; ++i) tma::mbar_init(bar0 + 8u * i, 1);
+    for (int i = 0; i < NS; ++i) {
+      tma::mbar_init(full0 + 8u * i, 1);
+      tma::mbar_init(empty0 + 8u * i, kIConsumers);
+    }
     tma::fence_mbar_init();
+  }
+  // Sorted point range of every home plane (its rows [hy0, hy1) are
+  // contiguous) and the running count of 8-point groups before it.
+  for (int jj = tid; jj < H; jj += kIThreads) {
+    const int s = hz0 + jj;
+    const int sw = g.periodic[2] ? wrap_cell(s, nz) : s;
+    rs[jj] = __ldg(rowstart + row_id(g, hy0, sw));
+    rs[T.hmax + jj] = __ldg(rowstart + row_id(g, hy1 - 1, sw) + 1);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t acc = 0;
+    for (int jj = 0; jj < H; ++jj) {
+      rs[2 * T.hmax + jj] = acc;
+      acc += (rs[T.hmax + jj] - rs[jj] + 7u) >> 3;
+    }
   }
   __syncthreads();
 
-  // Producer: field plane index i (plane hz0 - 2 + i) into slot i % kISlots.
-  auto issue = [&](int i) {
-    if (i >= nplanes) return;
-    const int slot = i % kISlots;
-    int t = hz0 - 2 + i;
-    if (g.periodic[2]) t = wrap_cell(t, nz);
-    const uint32_t bar = bar0 + 8u * slot;
-    tma::mbar_expect_tx(bar, plane_bytes);
-    const uint32_t dst = base + (uint32_t)slot * T.slot_bytes;
-    for (int f = 0; f < fr; ++f) {
-      int y = hy0 - 2 + f;
-      if (g.periodic[1]) y = wrap_cell(y, ny);
-      tma::load_4d(dst + (uint32_t)f * T.pitch, &tmap, 0, 0, y, t, bar);
-    }
-  };
-  if (tid == 0)
-    for (int i = 0; i < kISlots; ++i) issue(i);
-
-  const bool px = g.periodic[0] != 0;
-  for (int j = 0; j < hz1 - hz0; ++j) {
-    if (j > 0) {
-      __syncthreads();  // step j-1 is done with plane j-1: refill its slot
-      if (tid == 0) {
-        tma::fence_proxy_async();
-        issue(j + kISlots - 1);
+  if (warp == kIConsumers) {
+    // ------------------------------------------------------------ producer
+    for (int i = 0; i < nplanes; ++i) {
+      const int slot = i % NS;
+      if (i >= NS) tma::mbar_wait(empty0 + 8u * slot, ((i / NS) - 1) & 1);
+      int t = hz0 - 2 + i;
+      if (g.periodic[2]) t = wrap_cell(t, nz);
+      const uint32_t bar = full0 + 8u * slot;
+      const int jr = i - 3;  // step whose records ride with this plane
+      uint32_t nrec = 0, ra = 0;
+      if (jr >= 0 && jr < H) {
+        ra = rs[jr];
+        nrec = min(rs[T.hmax + jr] - ra, (uint32_t)T.rec_cap);
+      }
+      const uint32_t dst = base + (uint32_t)slot * T.slot_stride;
+      tma::fence_proxy_async();
+      if (lane == 0) {
+        tma::mbar_expect_tx(bar, plane_bytes + nrec * 32u);
+        if (nrec) tma::bulk_g2s(dst + T.slot_bytes, rec + 4 * (size_t)ra, nrec * 32u, bar);
+        if (box) tma::load_4d(dst, &tmap_box, 0, 0, hy0 - 2, t, bar);
+      }
+      __syncwarp();
+      if (!box) {
+        for (int f = lane; f < fr; f += 32) {
+          int y = hy0 - 2 + f;
+          if (g.periodic[1]) y = wrap_cell(y, ny);
+          tma::load_4d(dst + (uint32_t)f * T.pitch, &tmap_row, 0, 0, y, t, bar);
+        }
       }
     }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  // Quad layout: point p = lane / 4 of an 8-point group, kx = lane % 4.
+  const int kx = lane & 3, qbase = lane & ~3;
+  const int ax = kx < 3 ? kx : 0;  // axis this lane evaluates (lane 3 repeats x)
+  const Axis A = axis_of(g, ax);
+  const bool px = g.periodic[0] != 0;
+  for (int j = 0; j < H; ++j) {
     // Planes j .. j+3 are this step's window; j+3 is the only new one.
     if (j == 0)
-      for (int i = 0; i < 3; ++i) tma::mbar_wait(bar0 + 8u * (i % kISlots), (i / kISlots) & 1);
-    tma::mbar_wait(bar0 + 8u * ((j + 3) % kISlots), ((j + 3) / kISlots) & 1);
-
-    const int s = hz0 + j;
-    const int sw = g.periodic[2] ? wrap_cell(s, nz) : s;
-    const uint32_t rb = __ldg(rowstart + row_id(g, hy0, sw));
-    const uint32_t re = __ldg(rowstart + row_id(g, hy1 - 1, sw) + 1);
+      for (int i = 0; i < 3; ++i) tma::mbar_wait(full0 + 8u * (i % NS), (i / NS) & 1);
+    tma::mbar_wait(full0 + 8u * ((j + 3) % NS), ((j + 3) / NS) & 1);
+    const uint32_t a = rs[j], b = rs[T.hmax + j];
+    const uint32_t gfirst = rs[2 * T.hmax + j];
     const unsigned char* sl[4];
 #pragma unroll
-    for (int kz = 0; kz < 4; ++kz) sl[kz] = slots + (size_t)((j + kz) % kISlots) * T.slot_bytes;
+    for (int kz = 0; kz < 4; ++kz) sl[kz] = slots + (size_t)((j + kz) % NS) * T.slot_stride;
+    const double2* srec = reinterpret_cast<const double2*>(sl[3] + T.slot_bytes);
+    // This warp's groups: k with (gfirst + k) % kIConsumers == warp.
+    const uint32_t k0 =
+        (uint32_t)(warp - (int)(gfirst % kIConsumers) + kIConsumers) % kIConsumers;
 
-    for (uint32_t r = rb + tid; r < re; r += kIThreads) {
-      const double2 q0 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r);
-      const double2 q1 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r + 1);
-      const uint32_t idx = (uint32_t)__double_as_longlong(q1.y);
-      double wx[4], wy[4], wz[4];
-      int cx = axis_weights(g, 0, q0.x, wx);
-      int cy = axis_weights(g, 1, q0.y, wy);
-      axis_weights(g, 2, q1.x, wz);
-      if (px) cx = wrap_cell(cx, nx);
-      if (g.periodic[1]) cy = wrap_cell(cy, ny);
-      uint32_t xo[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int x = cx + k - 2;
-        if (px) {
-          x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
-        } else if (x < 0 || x >= nx) {
-          wx[k] = 0.0;  // off the closed grid: the reference skips the term
-          x = 0;
+    for (uint32_t g0 = a + 8u * k0; g0 < b; g0 += 8u * kIConsumers) {
+      const uint32_t r = g0 + (uint32_t)(lane >> 2);
+      const bool valid = r < b;
+      double2 q0 = make_double2(0.0, 0.0), q1 = q0;
+      if (valid) {
+        if (r - a < (uint32_t)T.rec_cap) {
+          q0 = srec[2 * (r - a)];
+          q1 = srec[2 * (r - a) + 1];
+        } else {
+          q0 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r);
+          q1 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r + 1);
         }
-        xo[k] = tma::swz128(x);
       }
-      const uint32_t f0 = (uint32_t)(cy - hy0) * T.pitch;
+      // This lane's axis: home cell and sin/cos(pi u / 2), u = -t.
+      const double xa = ax == 0 ? q0.x : (ax == 1 ? q0.y : q1.x);
+      double u = 0.0;
+      const int ca = valid ? cell_and_u(A, g.h, g.inv_h, xa, &u) : 0;
+      double sn, cs;
+      sincos_half_pi(u, &sn, &cs);
+      // Gather the three axes from lanes qbase + 0..2.
+      const int cx = __shfl_sync(0xffffffffu, ca, qbase);
+      const int cy = __shfl_sync(0xffffffffu, ca, qbase + 1);
+      const double sx = shfl_d(sn, qbase), cxs = shfl_d(cs, qbase);
+      const double sy = shfl_d(sn, qbase + 1), cys = shfl_d(cs, qbase + 1);
+      const double sz = shfl_d(sn, qbase + 2), czs = shfl_d(cs, qbase + 2);
+      const double q = 0.25 * g.inv_h;
+      // phi(sigma - t)/h for sigma = -2..1: (1-c), (1+s), (1+c), (1-s) over 4h.
+      const double wy[4] = {q * (1.0 - cys), q * (1.0 + sy), q * (1.0 + cys), q * (1.0 - sy)};
+      const double wz[4] = {q * (1.0 - czs), q * (1.0 + sz), q * (1.0 + czs), q * (1.0 - sz)};
+      double wxk = kx == 0 ? (1.0 - cxs) : kx == 1 ? (1.0 + sx) : kx == 2 ? (1.0 + cxs) : (1.0 - sx);
+      wxk *= q;
+      int x = cx + kx - 2;
+      if (px) {
+        x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+      } else if (x < 0 || x >= nx) {
+        wxk = 0.0;  // off the closed grid: the reference skips the term
+        x = 0;
+      }
+      const uint32_t xo = tma::swz128(x) + (uint32_t)(valid ? cy - hy0 : 0) * T.pitch;
       double acc = 0.0;
+      if (valid) {
 #pragma unroll
-      for (int kz = 0; kz < 4; ++kz) {
-        double az = 0.0;
+        for (int kz = 0; kz < 4; ++kz) {
+          const unsigned char* p = sl[kz] + xo;
+          double az = 0.0;
 #pragma unroll
-        for (int ky = 0; ky < 4; ++ky) {
-          const unsigned char* row = sl[kz] + f0 + (uint32_t)ky * T.pitch;
-          double ar = 0.0;
-#pragma unroll
-          for (int kx = 0; kx < 4; ++kx)
-            ar = fma(wx[kx], *reinterpret_cast<const double*>(row + xo[kx]), ar);
-          az = fma(wy[ky], ar, az);
+          for (int ky = 0; ky < 4; ++ky)
+            az = fma(wy[ky], *reinterpret_cast<const double*>(p + (uint32_t)ky * T.pitch), az);
+          acc = fma(wz[kz], az, acc);
         }
-        acc = fma(wz[kz], az, acc);
+        acc *= wxk;
       }
-      out[idx] = acc * g.hd;
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (valid && kx == 0) out[(uint32_t)__double_as_longlong(q1.y)] = acc * g.hd;
     }
+    // Plane j is not read by any later step.
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8u * (j % NS))
+                   : "memory");
   }
 }
 

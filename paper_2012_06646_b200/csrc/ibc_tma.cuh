@@ -56,6 +56,29 @@ __device__ __forceinline__ void load_4d(uint32_t dst, const CUtensorMap* map, in
       : "memory");
 }
 
+__device__ __forceinline__ void load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                        uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
+// L2 prefetch of one 4-D box (no shared-memory destination).
+__device__ __forceinline__ void prefetch_4d(const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+// L2 prefetch of a contiguous byte range (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void prefetch_bytes(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // 1-D bulk copy global -> shared completing on `bar` (16-byte aligned, size % 16 == 0).
 __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile(
@@ -77,7 +100,7 @@ __device__ __forceinline__ uint32_t swz128(int x) {
 // Host: field rows of an (nx, ny, nz) colex FP64 grid as a 4-D tensor
 // (16, nx/16, ny, nz) with a one-row box (16, nx/16, 1, 1), 128-byte swizzle,
 // zero fill out of bounds.  Requires nx % 16 == 0, nx <= 4096.
-bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz);
+bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz, int box_rows = 1);
 
 }  // namespace tma
 }  // namespace ibc
