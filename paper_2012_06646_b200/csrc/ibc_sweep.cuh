@@ -153,16 +153,22 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
   const int ax = kx < 3 ? kx : 0;  // axis this lane evaluates (lane 3 repeats x)
   const Axis A = axis_of(g, ax);
   const bool px = g.periodic[0] != 0;
+  // Slot of plane j (j % NS) and fill parity of plane j + 3, advanced
+  // incrementally (no integer division in the loop).
+  int slot_j = 0, slot_3 = 3 % NS;
+  uint32_t par_3 = (3 / NS) & 1;
+  for (int i = 0; i < 3; ++i) tma::mbar_wait(full0 + 8u * (i % NS), (i / NS) & 1);
   for (int j = 0; j < H; ++j) {
     // Planes j .. j+3 are this step's window; j+3 is the only new one.
-    if (j == 0)
-      for (int i = 0; i < 3; ++i) tma::mbar_wait(full0 + 8u * (i % NS), (i / NS) & 1);
-    tma::mbar_wait(full0 + 8u * ((j + 3) % NS), ((j + 3) / NS) & 1);
+    tma::mbar_wait(full0 + 8u * slot_3, par_3);
     const uint32_t a = rs[j], b = rs[T.hmax + j];
     const uint32_t gfirst = rs[2 * T.hmax + j];
     const unsigned char* sl[4];
 #pragma unroll
-    for (int kz = 0; kz < 4; ++kz) sl[kz] = slots + (size_t)((j + kz) % NS) * T.slot_stride;
+    for (int kz = 0; kz < 4; ++kz) {
+      const int sk = slot_j + kz;
+      sl[kz] = slots + (size_t)(sk >= NS ? sk - NS : sk) * T.slot_stride;
+    }
     const double2* srec = reinterpret_cast<const double2*>(sl[3] + T.slot_bytes);
     // This warp's groups: k with (gfirst + k) % kIConsumers == warp.
     const uint32_t k0 =
@@ -227,8 +233,13 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
     // Plane j is not read by any later step.
     __syncwarp();
     if (lane == 0)
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8u * (j % NS))
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(empty0 + 8u * slot_j)
                    : "memory");
+    slot_j = slot_j + 1 == NS ? 0 : slot_j + 1;
+    if (++slot_3 == NS) {
+      slot_3 = 0;
+      par_3 ^= 1u;
+    }
   }
 }
 
