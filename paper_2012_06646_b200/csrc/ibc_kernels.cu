@@ -57,20 +57,27 @@ __device__ __forceinline__ uint32_t key_of(const DevGrid& g, const double* x, bo
   return key;
 }
 
-// One CTA per 4096-key sort tile (the input order): cell keys of its points
-// and the tile's digit histogram for the first radix pass (hist0[d][tile]).
-constexpr int kKeysThreads = 1024;
+// One CTA per 2048-key sort tile (the input order): cell keys of its points,
+// their digit counts for EVERY radix pass added to gcount[p][d], and the
+// tile's pass-0 digit counts cnt0[tile][d].
+constexpr int kKeysThreads = sort::kThreads;
+
+struct KeyDigits {
+  int passes;
+  int shift[sort::kMaxPasses];
+  int bits[sort::kMaxPasses];
+};
 
 template <int D>
 __global__ void __launch_bounds__(kKeysThreads) keys_hist_kernel(
     DevGrid g, const double* __restrict__ X, uint32_t n, uint32_t* __restrict__ keys,
-    uint32_t* __restrict__ hist0, int ntiles, int shift0, int bits0, int row_only) {
-  __shared__ uint32_t sh[sort::kMaxRadix];
-  const uint32_t radix = 1u << bits0, mask = radix - 1u;
-  for (uint32_t t = threadIdx.x; t < radix; t += blockDim.x) sh[t] = 0u;
+    uint32_t* __restrict__ gcount, uint32_t* __restrict__ cnt0, KeyDigits kd, int row_only) {
+  __shared__ uint32_t sh[sort::kMaxPasses][sort::kMaxRadix];
+  for (int t = threadIdx.x; t < sort::kMaxPasses * sort::kMaxRadix; t += blockDim.x)
+    (&sh[0][0])[t] = 0u;
   __syncthreads();
   const uint32_t base = blockIdx.x * (uint32_t)sort::kTile;
-  constexpr int kPer = sort::kTile / kKeysThreads;  // 4 points per thread
+  constexpr int kPer = sort::kTile / kKeysThreads;  // 8 points per thread
   static_assert(kPer % kKeysUnroll == 0, "tile split");
   for (int j0 = 0; j0 < kPer; j0 += kKeysUnroll) {
     double x[kKeysUnroll][D];
@@ -86,13 +93,24 @@ __global__ void __launch_bounds__(kKeysThreads) keys_hist_kernel(
       if (i < n) {
         const uint32_t key = key_of<D>(g, x[u], row_only != 0);
         keys[i] = key;
-        atomicAdd(&sh[(key >> shift0) & mask], 1u);
+#pragma unroll
+        for (int p = 0; p < sort::kMaxPasses; ++p)
+          if (p < kd.passes) atomicAdd(&sh[p][(key >> kd.shift[p]) & ((1u << kd.bits[p]) - 1u)], 1u);
       }
     }
   }
   __syncthreads();
-  for (uint32_t t = threadIdx.x; t < radix; t += blockDim.x)
-    hist0[(size_t)t * ntiles + blockIdx.x] = sh[t];
+  for (int t = threadIdx.x; t < (1 << kd.bits[0]); t += blockDim.x)
+    cnt0[(size_t)blockIdx.x * sort::kMaxRadix + t] = sh[0][t];
+#pragma unroll
+  for (int p = 0; p < sort::kMaxPasses; ++p) {
+    if (p >= kd.passes) break;
+    const int radix = 1 << kd.bits[p];
+    for (int t = threadIdx.x; t < radix; t += blockDim.x) {
+      const uint32_t c = sh[p][t];
+      if (c) atomicAdd(gcount + p * sort::kMaxRadix + t, c);
+    }
+  }
 }
 
 // ---------------------------------------------------------------- K3
@@ -539,6 +557,10 @@ inline unsigned grid_for(size_t n, int block) { return (unsigned)((n + block - 1
 
 size_t sort_smem() { return sizeof(sort::PassSmem); }
 
+// Sort scratch (s.hist): gcount[kMaxPasses][kMaxRadix] | offsets [ntiles][kMaxRadix] |
+// per-pass tile counts [kMaxPasses][ntiles][kMaxRadix].
+constexpr size_t kOffOff = (size_t)sort::kMaxPasses * sort::kMaxRadix;
+
 // Keys + stable sort.  Leaves s.sorted_keys / s.sorted_perm (and, with a
 // payload, s.rec: 32-byte sorted records).  row_only sorts by extended row id
 // alone (enough for the interpolation's row grouping).
@@ -548,11 +570,13 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
   cudaStream_t st = ctx.stream;
   const sort::DigitPlan plan = sort::plan_digits(key_bits(g, row_only));
   const int ntiles = (int)((n + sort::kTile - 1) / sort::kTile);
-  size_t hoff[kMaxPasses + 1] = {0};
-  for (int p = 0; p < plan.passes; ++p) hoff[p + 1] = hoff[p] + ((size_t)ntiles << plan.bits[p]);
+  const size_t table = (size_t)ntiles * sort::kMaxRadix;
+  uint32_t* gcount = s.hist.p;
+  uint32_t* offs = s.hist.p + kOffOff;
+  auto cnt = [&](int p) { return s.hist.p + kOffOff + table * (size_t)(1 + p); };
+  IBC_CUDA(cudaMemsetAsync(gcount, 0, kOffOff * 4, st));
   if (plan.passes > 1)
-    IBC_CUDA(cudaMemsetAsync(s.hist.p + hoff[1], 0, (hoff[plan.passes] - hoff[1]) * 4, st));
-  IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
+    IBC_CUDA(cudaMemsetAsync(cnt(1), 0, table * (size_t)(plan.passes - 1) * 4, st));
 
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
@@ -566,33 +590,37 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
   const int ro = row_only ? 1 : 0;
+  KeyDigits kd{};
+  kd.passes = plan.passes;
+  for (int p = 0; p < plan.passes; ++p) {
+    kd.shift[p] = plan.shift[p];
+    kd.bits[p] = plan.bits[p];
+  }
   if (g.dim == 3)
-    keys_hist_kernel<3><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
-                                                   ntiles, plan.shift[0], plan.bits[0], ro);
+    keys_hist_kernel<3><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p,
+                                                         gcount, cnt(0), kd, ro);
   else if (g.dim == 2)
-    keys_hist_kernel<2><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
-                                                   ntiles, plan.shift[0], plan.bits[0], ro);
+    keys_hist_kernel<2><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p,
+                                                         gcount, cnt(0), kd, ro);
   else
-    keys_hist_kernel<1><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p, s.hist.p,
-                                                   ntiles, plan.shift[0], plan.bits[0], ro);
+    keys_hist_kernel<1><<<ntiles, kKeysThreads, 0, st>>>(g, d_points, (uint32_t)n, s.keys[0].p,
+                                                         gcount, cnt(0), kd, ro);
   ++ctx.launches;
   ctx.prof_end(kProfKeys, ev);
 
   ctx.prof_begin(kProfSort, &ev);
   int src = 0;
   for (int p = 0; p < plan.passes; ++p) {
-    uint32_t* hp = s.hist.p + hoff[p];
-    uint32_t* tot = s.base.p + (size_t)p * sort::kMaxRadix;
-    sort::tile_scan<<<1u << plan.bits[p], sort::kThreads, 0, st>>>(hp, tot, ntiles);
     const bool last = p + 1 == plan.passes;
-    uint32_t* nh = last ? nullptr : s.hist.p + hoff[p + 1];
-    const int nshift = last ? 0 : plan.shift[p + 1], nbits = last ? 1 : plan.bits[p + 1];
     const int pl = last ? payload : sort::kPayloadNone;
+    const int radix = 1 << plan.bits[p];
+    sort::tile_offsets_kernel<<<(radix + 31) / 32, sort::kThreads, 0, st>>>(
+        cnt(p), offs, gcount + (size_t)p * sort::kMaxRadix, radix, ntiles);
     auto args = [&](auto kern) {
       kern<<<ntiles, sort::kThreads, sort_smem(), st>>>(
           s.keys[src].p, p == 0 ? nullptr : s.vals[src].p, s.keys[src ^ 1].p, s.vals[src ^ 1].p,
-          (uint32_t)n, plan.shift[p], plan.bits[p], hp, tot, ntiles, nh, nshift, nbits, d_points,
-          d_values, s.rec.p);
+          (uint32_t)n, plan.shift[p], plan.bits[p], offs, last ? nullptr : cnt(p + 1),
+          last ? 0 : plan.shift[p + 1], last ? 1 : plan.bits[p + 1], d_points, d_values, s.rec.p);
     };
     if (pl == sort::kPayloadSpread) args(sort::onesweep_pass<sort::kPayloadSpread>);
     else if (pl == sort::kPayloadInterp) args(sort::onesweep_pass<sort::kPayloadInterp>);
@@ -725,7 +753,7 @@ void PointScratch::reserve_points(size_t n, bool spread) {
     keys[b].ensure(n);
     vals[b].ensure(n);
   }
-  hist.ensure((size_t)kMaxPasses * sort::kMaxRadix * std::max<size_t>(tiles, 1));
+  hist.ensure(kOffOff + (size_t)(kMaxPasses + 1) * sort::kMaxRadix * std::max<size_t>(tiles, 1));
   base.ensure((size_t)kMaxPasses * sort::kMaxRadix);
   counters.ensure(kCounters);
   rec.ensure(12 * std::max<size_t>(n, 1));  // 12 doubles (V1 weights) or 4 (sorted records)
