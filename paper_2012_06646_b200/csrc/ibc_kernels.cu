@@ -21,6 +21,7 @@
 #include "ibc_sort.cuh"
 #include "ibc_zsweep.cuh"
 #include "ibc_sweep.cuh"
+#include "ibc_bucket.cuh"
 #include "ibc_tma.cuh"
 
 namespace ibc {
@@ -769,7 +770,7 @@ void PointScratch::release_all() {
     vals[b].release();
   }
   hist.release(); base.release(); counters.release(); rowstart.release();
-  rec_cx.release(); rec.release(); run_keys.release(); block_counts.release();
+  rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
   cap = 0;
 }
 
@@ -914,6 +915,41 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
 }  // namespace tma
 
 namespace {
+// Row bucketing of the interpolation points (ibc_bucket.cuh): s.rowstart and
+// 32-byte records in s.rec, grouped by row.
+void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, size_t n, PointScratch& s) {
+  cudaStream_t st = ctx.stream;
+  const uint32_t nrows = g.nrows;
+  const uint32_t nchunks = (nrows + bucket::kChunk - 1) / bucket::kChunk;
+  s.rowaux.ensure((size_t)nrows + nchunks + 8);
+  uint32_t* count = s.rowaux.p;
+  uint32_t* status = s.rowaux.p + nrows;
+  uint32_t* ticket = status + nchunks;
+  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 1) * 4, st));
+  cudaEvent_t ev = nullptr;
+  ctx.prof_begin(kProfKeys, &ev);
+  const unsigned blocks = grid_for(n, bucket::kThreads);
+  if (g.dim == 3)
+    bucket::row_keys_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n,
+                                                                    s.keys[0].p, s.vals[0].p, count);
+  else if (g.dim == 2)
+    bucket::row_keys_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n,
+                                                                    s.keys[0].p, s.vals[0].p, count);
+  else
+    bucket::row_keys_kernel<1><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n,
+                                                                    s.keys[0].p, s.vals[0].p, count);
+  ctx.prof_end(kProfKeys, ev);
+  ctx.prof_begin(kProfSort, &ev);
+  bucket::row_scan_kernel<<<nchunks, bucket::kScanThreads, 0, st>>>(count, s.rowstart.p, nrows,
+                                                                    status, ticket);
+  bucket::scatter_kernel<<<blocks, bucket::kThreads, 0, st>>>(
+      d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+  ctx.prof_end(kProfSort, ev);
+  ctx.launches += 3;
+  IBC_CUDA(cudaGetLastError());
+  s.last_n = 0;  // interpolation leaves no observable sort
+}
+
 bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
                      size_t n, PointScratch& s, double* d_out) {
   sw::InterpTiling T;
@@ -923,8 +959,7 @@ bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, cons
   CUtensorMap map_box;
   if (!tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax)) return false;
   cudaStream_t st = ctx.stream;
-  sort_points(ctx, g, d_points, n, s, true, sort::kPayloadInterp);
-  row_table(ctx, g, n, s);
+  bucket_points(ctx, g, d_points, n, s);
   const size_t smem = interp_tma_smem(T);
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
