@@ -22,6 +22,7 @@
 #include "ibc_zsweep.cuh"
 #include "ibc_sweep.cuh"
 #include "ibc_bucket.cuh"
+#include "ibc_spread.cuh"
 #include "ibc_tma.cuh"
 
 namespace ibc {
@@ -585,6 +586,7 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
     IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
     attr_set[ctx.device & 63] = true;
   }
 
@@ -621,9 +623,11 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
       kern<<<ntiles, sort::kThreads, sort_smem(), st>>>(
           s.keys[src].p, p == 0 ? nullptr : s.vals[src].p, s.keys[src ^ 1].p, s.vals[src ^ 1].p,
           (uint32_t)n, plan.shift[p], plan.bits[p], offs, last ? nullptr : cnt(p + 1),
-          last ? 0 : plan.shift[p + 1], last ? 1 : plan.bits[p + 1], d_points, d_values, s.rec.p);
+          last ? 0 : plan.shift[p + 1], last ? 1 : plan.bits[p + 1], d_points, d_values, s.rec.p,
+          g, s.rec_cx.p);
     };
-    if (pl == sort::kPayloadSpread) args(sort::onesweep_pass<sort::kPayloadSpread>);
+    if (pl == sort::kPayloadWeights) args(sort::onesweep_pass<sort::kPayloadWeights>);
+    else if (pl == sort::kPayloadSpread) args(sort::onesweep_pass<sort::kPayloadSpread>);
     else if (pl == sort::kPayloadInterp) args(sort::onesweep_pass<sort::kPayloadInterp>);
     else args(sort::onesweep_pass<sort::kPayloadNone>);
     ctx.launches += 2;
@@ -774,13 +778,43 @@ void PointScratch::release_all() {
   cap = 0;
 }
 
+namespace {
+// Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
+bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
+  if (g.dim < 2) return false;
+  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
+  const int xi = nx + sp::kPadL + sp::kPadR;
+  int rl = xi + (xi >> 4) + 1;
+  rl += rl & 1;
+  const int slots = g.dim == 3 ? 4 : 1;
+  const size_t per_warp = (size_t)slots * rl * sizeof(double);
+  if (per_warp > 200 * 1024) return false;
+  int wpc = 8;
+  while (wpc > 1 && wpc * per_warp > 200 * 1024) --wpc;
+  T.wpc = wpc;
+  T.rl = rl;
+  T.nyg = (ny + wpc - 1) / wpc;
+  if (g.dim == 3) {
+    const long per_sm = std::max<long>(1, std::min<long>(2048 / (32 * wpc), (227L * 1024) / (long)(wpc * per_warp)));
+    const long chunks = std::max<long>(1, (148L * per_sm) / T.nyg);
+    T.zc = (int)std::max<long>(1, (nz + chunks - 1) / chunks);
+    T.nzc = (nz + T.zc - 1) / T.zc;
+  } else {
+    T.zc = T.nzc = 1;
+  }
+  return true;
+}
+}  // namespace
+
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
+  sp::SweepTiling W;
+  const bool sweep = sweep_tiling(g, W);
   if (n > 0) {
-    sort_points(ctx, g, d_points, n, s, false);
+    sort_points(ctx, g, d_points, n, s, false, sweep ? sort::kPayloadWeights : sort::kPayloadNone,
+                d_values);
   } else {
-    IBC_CUDA(cudaMemsetAsync(s.counters.p, 0, kCounters * 4, st));
     s.last_n = 0;
     s.sorted_keys = s.keys[0].p;
     s.sorted_perm = s.vals[0].p;
@@ -793,32 +827,32 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   if (!attr_set[ctx.device & 63]) {
     IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(spread_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  210 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(spread_rows_kernel,
-                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
-                                  cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    IBC_CUDA(cudaFuncSetAttribute(sp::spread_sweep_kernel<2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    IBC_CUDA(cudaFuncSetAttribute(sp::spread_sweep_kernel<3>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[ctx.device & 63] = true;
   }
-  if (n > 0) {
-    ctx.prof_begin(kProfPrep, &ev);
-    prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
-        g, d_points, d_values, s.sorted_perm, (uint32_t)n, s.rec_cx.p, s.rec.p);
-    ++ctx.launches;
-    ctx.prof_end(kProfPrep, ev);
-  }
-  RowTiling R;
-  if (rows_tiling(g, R)) {
+  if (sweep) {
     ctx.prof_begin(kProfSpread, &ev);
-    const size_t smem = (size_t)R.warps * kRowsPerWarp * R.nxp * sizeof(double);
-    spread_rows_kernel<<<(unsigned)(R.nty * R.ntz), 32 * R.warps, smem, st>>>(
-        g, R, s.rowstart.p, s.rec_cx.p, s.rec.p, (uint32_t)n, d_out);
+    const size_t smem = (size_t)W.wpc * (g.dim == 3 ? 4 : 1) * W.rl * sizeof(double);
+    const unsigned blocks = (unsigned)(W.nyg * W.nzc);
+    if (g.dim == 3)
+      sp::spread_sweep_kernel<3><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, s.rec.p,
+                                                                   s.rec_cx.p, d_out);
+    else
+      sp::spread_sweep_kernel<2><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, s.rec.p,
+                                                                   s.rec_cx.p, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   } else {
+    if (n > 0) {
+      ctx.prof_begin(kProfPrep, &ev);
+      prep_records_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
+          g, d_points, d_values, s.sorted_perm, (uint32_t)n, s.rec_cx.p, s.rec.p);
+      ++ctx.launches;
+      ctx.prof_end(kProfPrep, ev);
+    }
     const SpreadTiling T = choose_tiling(g);
     const size_t smem = (size_t)T.tx * T.ty * T.tz * sizeof(double);
     ctx.prof_begin(kProfSpread, &ev);

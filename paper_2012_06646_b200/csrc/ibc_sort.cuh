@@ -25,6 +25,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "ibc_device.cuh"
+
 namespace ibc {
 namespace sort {
 
@@ -38,7 +40,12 @@ constexpr int kWarpSpan = 32 * kItems;    // 256 consecutive keys per warp
 constexpr int kMaxPasses = 4;
 
 // Payload gathered by the last pass, one 32-byte record per sorted position.
-enum Payload { kPayloadNone = 0, kPayloadSpread = 1, kPayloadInterp = 2 };
+//   kPayloadSpread  {x, y, z, G}          (32 B)
+//   kPayloadInterp  {x, y, z, index}      (32 B)
+//   kPayloadWeights {G wx[4], sin/cos(pi u_y / 2), sin/cos(pi u_z / 2)} (64 B)
+//                   + the home cell along x in rec_cx: everything the
+//                   spread sweep needs, computed once per point.
+enum Payload { kPayloadNone = 0, kPayloadSpread = 1, kPayloadInterp = 2, kPayloadWeights = 3 };
 
 struct PassSmem {
   uint32_t wcount[kWarps][kMaxRadix];  // per-warp digit counts, then warp offsets
@@ -173,7 +180,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
     uint32_t* __restrict__ keys_out, uint32_t* __restrict__ vals_out, uint32_t n, int shift,
     int bits, const uint32_t* __restrict__ off, uint32_t* __restrict__ next_cnt, int next_shift,
     int next_bits, const double* __restrict__ pts, const double* __restrict__ gvals,
-    double* __restrict__ rec) {
+    double* __restrict__ rec, DevGrid g, int* __restrict__ rec_cx) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PassSmem& S = *reinterpret_cast<PassSmem*>(smem_raw);
   const uint32_t radix = 1u << bits, mask = radix - 1u;
@@ -269,7 +276,27 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
       o = S.gofs[(k >> shift) & mask] + i;
       keys_out[o] = k;
       vals_out[o] = v;
-      if (PAYLOAD != kPayloadNone) {
+      if (PAYLOAD == kPayloadWeights) {
+        const int D = g.dim;
+        const double* x = pts + (size_t)v * D;
+        double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};  // u = 0 on padded axes
+        int cx = 0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          if (a < D) {
+            double u;
+            const int c = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(x + a), &u);
+            if (a == 0) cx = c;
+            sincos_half_pi(u, &tr[a][0], &tr[a][1]);
+          }
+        }
+        const double gq = __ldg(gvals + v) * (0.25 * g.inv_h);
+        double4* r4 = reinterpret_cast<double4*>(rec) + 2 * (size_t)o;
+        r4[0] = make_double4(gq * (1.0 - tr[0][1]), gq * (1.0 + tr[0][0]), gq * (1.0 + tr[0][1]),
+                             gq * (1.0 - tr[0][0]));
+        r4[1] = make_double4(tr[1][0], tr[1][1], tr[2][0], tr[2][1]);
+        rec_cx[o] = cx;
+      } else if (PAYLOAD != kPayloadNone) {
         const double* x = pts + (size_t)v * 3;
         double4 r;
         r.x = __ldg(x);

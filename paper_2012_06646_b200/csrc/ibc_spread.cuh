@@ -1,0 +1,194 @@
+// ibc_spread.cuh -- write-once spreading sweep (sm_100a), 2-D and 3-D grids.
+//
+// Replaces ib::spread_fused (spread.hpp:165-216, Alg. 4): the same operator
+// l_m = sum_sigma sum_{p in cell(m - sigma)} w_sigma(t_p) G_p, with every grid
+// value written to HBM exactly once and no global atomics.
+//
+// Inputs: the points sorted by cell key (ibc_sort.cuh, stable), each with a
+// 64-byte weight record written by the last radix pass -- G * phi_x(k-2-t_x)/h
+// for k = 0..3 and sin/cos(pi u / 2) of the y and z displacements -- plus its
+// home cell along x; and the row start table (rows of the sorted keys are
+// contiguous).
+//
+// Each warp owns ONE target row (ty) of a z-chunk [z0, z1) and sweeps the
+// source planes z0-1 .. z1+1.  Its private shared-memory window holds the row
+// in the four target planes a source plane reaches (s-2 .. s+1), padded and
+// skewed (x index xi lives at xi + xi/16, so points ~16 cells apart hit
+// distinct banks).  For source plane s the warp pulls the points of the four
+// source rows that reach ty (cy = ty+2 .. ty-1, concatenated into full
+// 32-lane batches) and adds their 16 contributions (4 x 4 z) per lane.
+// Lanes that share a home cx -- same cell, or different source rows -- would
+// hit the same address: all but the first (match_any) are deferred to the
+// next batch, so batches stay full, adds never collide, and the summation
+// order is the sequence order -- results are bitwise reproducible.  When plane s is done, target plane s-2 is complete:
+// the warp folds the periodic x pad, stores the row once (coalesced) and
+// clears the slot for plane s+2.  No CTA barrier anywhere: warps are
+// independent, which is what lets 24 of them per SM hide the record loads.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "ibc_device.cuh"
+
+namespace ibc {
+namespace sp {
+
+constexpr int kPadL = 4;  // padded x index xi = x + kPadL
+constexpr int kPadR = 2;
+
+struct SweepTiling {
+  int wpc;       // warps (target rows) per CTA
+  int nyg;       // CTAs along y
+  int zc, nzc;   // z-chunk length, chunks
+  int rl;        // doubles per window row (padded + skewed, even)
+};
+
+__device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
+
+template <int D>
+__global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTiling T,
+                                                           const uint32_t* __restrict__ rowstart,
+                                                           const double* __restrict__ rec,
+                                                           const int* __restrict__ rcx,
+                                                           double* __restrict__ out) {
+  extern __shared__ __align__(16) double win[];
+  constexpr int kSlots = D == 3 ? 4 : 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nx = g.n[0], ny = g.n[1], nz = D == 3 ? g.n[2] : 1;
+  const int yg = blockIdx.x % T.nyg, zi = blockIdx.x / T.nyg;
+  const int ty = yg * T.wpc + warp;
+  if (ty >= ny) return;  // warp-uniform; the kernel has no CTA barriers
+  const int z0 = D == 3 ? zi * T.zc : 0;
+  const int z1 = D == 3 ? min(z0 + T.zc, nz) : 1;
+  double* W = win + (size_t)warp * kSlots * T.rl;
+  for (int i = lane; i < kSlots * T.rl; i += 32) W[i] = 0.0;
+  __syncwarp();
+
+  const bool px = g.periodic[0] != 0, py = g.periodic[1] != 0;
+  const bool pz = D == 3 && g.periodic[2] != 0;
+  const double q = 0.25 * g.inv_h;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int s_lo = D == 3 ? z0 - 1 : 0, s_hi = D == 3 ? z1 + 1 : 0;
+
+  for (int s = s_lo; s <= s_hi; ++s) {
+    const bool zok = D != 3 || pz || (s >= -1 && s <= nz);
+    if (zok) {
+      const int szw = D == 3 ? (pz ? wrap_cell(s, nz) : s) : 0;
+      // Lane j < 4: source row cy = ty + 2 - j (sigma_y = j - 2).
+      uint32_t rb = 0, len = 0;
+      if (lane < 4) {
+        int cy = ty + 2 - lane;
+        bool ok = true;
+        if (py) cy = wrap_cell(cy, ny);
+        else ok = cy >= -1 && cy <= ny;
+        if (ok) {
+          const uint32_t rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
+          rb = __ldg(rowstart + rid);
+          len = __ldg(rowstart + rid + 1) - rb;
+        }
+      }
+      uint32_t incl = len;
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const uint32_t e0 = __shfl_sync(0xffffffffu, incl, 0), e1 = __shfl_sync(0xffffffffu, incl, 1);
+      const uint32_t e2 = __shfl_sync(0xffffffffu, incl, 2), total = __shfl_sync(0xffffffffu, incl, 3);
+      // Batches of 32 distinct home cx: a lane whose cx already occurs in the
+      // batch (same cell, or another source row) is deferred to the front of
+      // the next batch, so every batch's adds hit distinct addresses and the
+      // summation order (sequence order) is fixed.
+      uint32_t next = 0;   // next unread position in the concatenated rows
+      int ndef = 0;        // deferred lanes carried into this batch
+      uint32_t p_def = 0;  // this lane's deferred position (lanes < ndef)
+      while (next < total || ndef > 0) {
+        const uint32_t p = lane < ndef ? p_def : next + (uint32_t)(lane - ndef);
+        const bool valid = lane < ndef || p < total;
+        const int j = (p >= e0) + (p >= e1) + (p >= e2);
+        const uint32_t rbj = __shfl_sync(0xffffffffu, rb, j & 3);
+        const uint32_t pre = __shfl_sync(0xffffffffu, incl - len, j & 3);
+        const uint32_t r = rbj + (p - pre);
+        int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
+        double4 gx = make_double4(0.0, 0.0, 0.0, 0.0), tyz = gx;
+        if (valid) {
+          const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
+          const double2 g01 = __ldg(r2), g23 = __ldg(r2 + 1), ty2 = __ldg(r2 + 2), tz2 = __ldg(r2 + 3);
+          gx = make_double4(g01.x, g01.y, g23.x, g23.y);
+          tyz = make_double4(ty2.x, ty2.y, tz2.x, tz2.y);
+          cx = __ldg(rcx + r);
+        }
+        const uint32_t peers = __match_any_sync(0xffffffffu, cx);
+        const bool first = (peers & lt) == 0u;
+        const bool on = valid && first;
+        // Carry the deferred lanes (in lane order) to the next batch.
+        const uint32_t defm = __ballot_sync(0xffffffffu, valid && !first);
+        const int newdef = __popc(defm);
+        {
+          // Lane k of the next batch takes the k-th deferred position.
+          int src = 0;
+          uint32_t m = defm;
+          for (int k = 0; k < lane && m; ++k) m &= m - 1u;
+          src = m ? __ffs(m) - 1 : 0;
+          const uint32_t pd = __shfl_sync(0xffffffffu, p, src);
+          if (lane < newdef) p_def = pd;
+        }
+        next += (uint32_t)(32 - ndef);
+        if (next > total) next = total;
+        ndef = newdef;
+        // phi(sigma - t)/h over sigma = -2..1 is (1-c), (1+s), (1+c), (1-s) / 4h.
+        const int sy = j - 2;
+        const double wy = q * (sy == -2 ? 1.0 - tyz.y : sy == -1 ? 1.0 + tyz.x : sy == 0 ? 1.0 + tyz.y : 1.0 - tyz.x);
+        double a[4];
+        if (D == 3) {
+          a[0] = wy * (q * (1.0 - tyz.w));
+          a[1] = wy * (q * (1.0 + tyz.z));
+          a[2] = wy * (q * (1.0 + tyz.w));
+          a[3] = wy * (q * (1.0 - tyz.z));
+        } else {
+          a[0] = a[1] = a[3] = 0.0;
+          a[2] = wy;
+        }
+        const double gk[4] = {gx.x, gx.y, gx.z, gx.w};
+        const int xb = cx + (kPadL - 2);
+#pragma unroll
+        for (int kx = 0; kx < 4; ++kx) {
+          if (on) {
+            const int addr = skew(xb + kx);
+            const double v = gk[kx];
+#pragma unroll
+            for (int kz = 0; kz < 4; ++kz) {
+              if (D == 3) {
+                const int tz = s + kz - 2;
+                if (tz >= z0 && tz < z1) W[(tz & 3) * T.rl + addr] += v * a[kz];
+              } else if (kz == 2) {
+                W[addr] += v * a[2];
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+    }
+    // Target plane s - 2 has all its sources: fold, store once, clear.
+    const int t = D == 3 ? s - 2 : 0;
+    if (t >= z0 && t < z1) {
+      double* Wr = W + (D == 3 ? (t & 3) * T.rl : 0);
+      double* orow = out + ((size_t)t * ny + ty) * nx;
+      for (int x = lane; x < nx; x += 32) {
+        double v = Wr[skew(x + kPadL)];
+        if (px) {
+          for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[skew(qx + kPadL)];
+          for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[skew(qx + kPadL)];
+        }
+        orow[x] = v;
+      }
+      __syncwarp();
+      for (int i = lane; i < T.rl; i += 32) Wr[i] = 0.0;
+      __syncwarp();
+    }
+  }
+}
+
+}  // namespace sp
+}  // namespace ibc
