@@ -1,18 +1,24 @@
-// ibc_bucket.cuh -- row bucketing of interpolation points (sm_100a).
+// ibc_bucket.cuh -- row bucket sort of the Lagrangian points (sm_100a).
 //
-// The interpolation gather (interpolate.hpp:22-58) needs the points grouped
-// by home row (cy, cz) -- each point's result is written to its own input
-// slot and summed in a fixed order by one quad of lanes, so the order of the
-// points inside a row does not change any result.  That makes a one-pass
-// counting bucket sort enough:
-//   K1 row keys + per-row counts; the atomic's return value is the point's
-//      rank inside its row, kept for K3,
-//   K2 single-pass scan of the row counts with decoupled look-back over
-//      4096-row chunks -> the row start table the sweep reads,
-//   K3 scatter: each point writes its 32-byte record {x, y, z, input index}
-//      to row start + rank (no atomics).
-// Three kernels instead of a key sort + row table; the spread keeps the
-// stable radix sort because its sums (and ws.keys / ws.perm) depend on order.
+// Both operators consume the points grouped by home row (cy, cz) -- the
+// contiguous ranges of the reference's sorted cell keys that share a row
+// (spread.hpp:88-122).  A one-pass counting sort by row does the grouping:
+//   K1 cell key (bit-exact, grid.hpp:121-170) of every point, its row, and
+//      its arrival rank in the row (the row-count atomic's return value);
+//   K2 single-pass scan of the row counts (decoupled look-back over 4096-row
+//      chunks) -> the row start table;
+//   K3 atomic-free scatter to row start + rank, writing the operator's
+//      per-point record (interpolation: {x, y, z, index}; spread: the 64-byte
+//      weight record + home cx + key + index).
+// Interpolation results do not depend on the order inside a row (each point
+// is summed alone, into its own slot), so K1-K3 are all it needs.  The spread
+// sums many points into each grid value, and the reference exposes the stable
+// key order (ws.keys / ws.perm, spread.hpp:33-34), so a fourth kernel puts
+// every row into stable (key, index) order -- which makes the result exactly
+// the reference's stable key-value sort -- and records where each sorted
+// element's record sits:
+//   K4 rows of <= 32 points: one warp, rank by 32 shuffled compares;
+//      longer rows (listed by K2): one CTA, bitonic sort in shared memory.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -29,26 +35,31 @@ constexpr int kChunk = kScanThreads * kScanItems;  // rows per scan CTA
 constexpr uint32_t kFlagAggregate = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
+constexpr int kShortRow = 32;       // rows up to this length are sorted by one warp
+constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
-// Row id (cell_key / (n0 + 2)) of every point, its rank in the row, and the
-// per-row counts.
+// Cell key of every point (or just its row when full_key == 0), its arrival
+// rank in its row, and the per-row counts.
 template <int D>
-__global__ void __launch_bounds__(kThreads) row_keys_kernel(DevGrid g, const double* __restrict__ X,
-                                                            uint32_t n, uint32_t* __restrict__ rows,
-                                                            uint32_t* __restrict__ rank,
-                                                            uint32_t* __restrict__ count) {
+__global__ void __launch_bounds__(kThreads) keys_kernel(DevGrid g, const double* __restrict__ X,
+                                                        uint32_t n, int full_key,
+                                                        uint32_t* __restrict__ keys,
+                                                        uint32_t* __restrict__ rank,
+                                                        uint32_t* __restrict__ count) {
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   uint64_t k = 0;
 #pragma unroll
-  for (int a = 1; a < D; ++a) {
+  for (int a = 0; a < D; ++a) {
+    if (a == 0 && !full_key) continue;
     double xw;
     int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
     if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
-    k += (uint64_t)(int64_t)(c + 1) * (g.kstride[a] / g.rowdiv);
+    k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
   }
-  const uint32_t row = (uint32_t)k;
-  rows[i] = row;
+  const uint32_t key = (uint32_t)k;
+  const uint32_t row = key / g.rowdiv;
+  keys[i] = full_key ? key : row;
   rank[i] = atomicAdd(count + row, 1u);
 }
 
@@ -62,11 +73,14 @@ __device__ __forceinline__ uint32_t ld_flag(const uint32_t* p) {
 }
 
 // Exclusive scan of count[0..nrows) into start[0..nrows] (start[nrows] = total).
-// status: one zeroed word per chunk; ticket: zeroed counter.
-__global__ void __launch_bounds__(kScanThreads) row_scan_kernel(uint32_t* __restrict__ count,
+// status: one zeroed word per chunk; ticket: zeroed counter.  Rows longer than
+// kShortRow are appended to long_rows (count in *nlong) when long_rows != null.
+__global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* __restrict__ count,
                                                                 uint32_t* __restrict__ start,
                                                                 uint32_t nrows, uint32_t* status,
-                                                                uint32_t* ticket) {
+                                                                uint32_t* ticket,
+                                                                uint32_t* __restrict__ long_rows,
+                                                                uint32_t* nlong) {
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_chunk, s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -79,6 +93,7 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(uint32_t* __rest
   for (int q = 0; q < kScanItems; ++q) {
     v[q] = r0 + q < nrows ? count[r0 + q] : 0u;
     sum += v[q];
+    if (long_rows && v[q] > (uint32_t)kShortRow) long_rows[atomicAdd(nlong, 1u)] = r0 + q;
   }
   // Block scan of the per-thread sums.
   uint32_t x = sum;
@@ -108,18 +123,16 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(uint32_t* __rest
         const uint32_t sv = cc >= 0 ? ld_flag(status + cc) : kFlagPrefix;
         const uint32_t ready = __ballot_sync(0xffffffffu, (sv & (kFlagPrefix | kFlagAggregate)) != 0u);
         const uint32_t pref = __ballot_sync(0xffffffffu, (sv & kFlagPrefix) != 0u);
-        // Lanes up to the first prefix (or first not-ready lane) are usable.
-        const uint32_t stop_ready = ~ready;  // first not-ready lane
         const int first_pref = pref ? __ffs(pref) - 1 : 32;
-        const int first_nr = stop_ready ? __ffs(stop_ready) - 1 : 32;
-        if (first_pref < first_nr) {
+        const int first_nr = ~ready ? __ffs(~ready) - 1 : 32;
+        if (first_pref < first_nr) {  // every lane up to the prefix is usable
           uint32_t add = lane <= first_pref ? (sv & kValueMask) : 0u;
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
           excl += add;
           break;
         }
-        uint32_t add = lane < first_nr ? (sv & kValueMask) : 0u;
+        uint32_t add = lane < first_nr ? (sv & kValueMask) : 0u;  // aggregates only
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) add += __shfl_xor_sync(0xffffffffu, add, o);
         excl += add;
@@ -141,12 +154,10 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(uint32_t* __rest
   }
 }
 
-// Each point writes {x, y, z, index} to its row's start + its rank.
-__global__ void __launch_bounds__(kThreads) scatter_kernel(const double* __restrict__ X,
-                                                           const uint32_t* __restrict__ rows,
-                                                           const uint32_t* __restrict__ rank, uint32_t n,
-                                                           const uint32_t* __restrict__ start,
-                                                           double* __restrict__ rec) {
+// K3, interpolation: {x, y, z, index} at row start + rank.
+__global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
+    const double* __restrict__ X, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ rank,
+    uint32_t n, const uint32_t* __restrict__ start, double* __restrict__ rec) {
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const uint32_t slot = __ldg(start + __ldg(rows + i)) + __ldg(rank + i);
@@ -156,6 +167,127 @@ __global__ void __launch_bounds__(kThreads) scatter_kernel(const double* __restr
   r.z = __ldg(X + (size_t)i * 3 + 2);
   r.w = __longlong_as_double((long long)i);
   reinterpret_cast<double4*>(rec)[slot] = r;
+}
+
+// K3, spread: key, index and the 64-byte weight record at row start + rank:
+//   {G phi_x(k-2-t_x)/h (k = 0..3), sin/cos(pi u_y/2), sin/cos(pi u_z/2)},
+// and the home cell along x (wrapped on periodic x).
+template <int D>
+__global__ void __launch_bounds__(kThreads) scatter_spread_kernel(
+    DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
+    const uint32_t* __restrict__ start, uint32_t* __restrict__ bkey, uint32_t* __restrict__ bidx,
+    double* __restrict__ brec, int* __restrict__ bcx) {
+  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t key = __ldg(keys + i);
+  const uint32_t slot = __ldg(start + key / g.rowdiv) + __ldg(rank + i);
+  double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};  // u = 0 on padded axes
+  int cx = 0;
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double u;
+    const int c = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &u);
+    if (a == 0) cx = c;
+    sincos_half_pi(u, &tr[a][0], &tr[a][1]);
+  }
+  const double gq = __ldg(G + i) * (0.25 * g.inv_h);
+  double4* r4 = reinterpret_cast<double4*>(brec) + 2 * (size_t)slot;
+  r4[0] = make_double4(gq * (1.0 - tr[0][1]), gq * (1.0 + tr[0][0]), gq * (1.0 + tr[0][1]),
+                       gq * (1.0 - tr[0][0]));
+  r4[1] = make_double4(tr[1][0], tr[1][1], tr[2][0], tr[2][1]);
+  bcx[slot] = cx;
+  bkey[slot] = key;
+  bidx[slot] = i;
+}
+
+// K4, short rows: one warp per row puts (key, index) in stable order.
+// sorted position -> (key, index, bucket slot of its record).
+__global__ void __launch_bounds__(kThreads) row_sort_kernel(
+    const uint32_t* __restrict__ start, uint32_t nrows, const uint32_t* __restrict__ bkey,
+    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
+    uint32_t* __restrict__ smap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warps = gridDim.x * (kThreads / 32);
+  for (uint32_t r = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
+    const uint32_t a = __ldg(start + r), len = __ldg(start + r + 1) - a;
+    if (len == 0 || len > (uint32_t)kShortRow) continue;  // empty, or a long row (K4b)
+    const bool valid = (uint32_t)lane < len;
+    const uint32_t k = valid ? __ldg(bkey + a + lane) : 0xffffffffu;
+    const uint32_t ix = valid ? __ldg(bidx + a + lane) : 0xffffffffu;
+    uint32_t rk = 0;
+    for (uint32_t j = 0; j < len; ++j) {
+      const uint32_t kj = __shfl_sync(0xffffffffu, k, j), ij = __shfl_sync(0xffffffffu, ix, j);
+      rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
+    }
+    if (valid) {
+      skey[a + rk] = k;
+      sidx[a + rk] = ix;
+      smap[a + rk] = a + lane;
+    }
+  }
+}
+
+// K4b, long rows: one CTA per listed row, bitonic sort of (key << 32 | index)
+// in shared memory (rows up to kLongSortMax; longer rows rank by counting).
+constexpr int kLongThreads = 1024;
+__global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
+    const uint32_t* __restrict__ start, const uint32_t* __restrict__ long_rows,
+    const uint32_t* __restrict__ nlong, const uint32_t* __restrict__ bkey,
+    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
+    uint32_t* __restrict__ smap) {
+  extern __shared__ unsigned long long sk[];  // [kLongSortMax] keys, then [kLongSortMax] slots
+  uint32_t* sslot = reinterpret_cast<uint32_t*>(sk + kLongSortMax);
+  const uint32_t count = *nlong;
+  for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
+    const uint32_t r = long_rows[li];
+    const uint32_t a = start[r], len = start[r + 1] - a;
+    if (len <= (uint32_t)kLongSortMax) {
+      uint32_t m = 1;
+      while (m < len) m <<= 1;
+      for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
+        sk[e] = e < len ? ((unsigned long long)bkey[a + e] << 32) | bidx[a + e] : ~0ull;
+        sslot[e] = a + e;
+      }
+      __syncthreads();
+      for (uint32_t size = 2; size <= m; size <<= 1) {
+        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+          for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
+            const uint32_t p = e ^ stride;
+            if (p > e) {
+              const bool up = (e & size) == 0;
+              const unsigned long long x = sk[e], y = sk[p];
+              if ((x > y) == up) {
+                sk[e] = y;
+                sk[p] = x;
+                const uint32_t t = sslot[e];
+                sslot[e] = sslot[p];
+                sslot[p] = t;
+              }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
+        skey[a + e] = (uint32_t)(sk[e] >> 32);
+        sidx[a + e] = (uint32_t)sk[e];
+        smap[a + e] = sslot[e];
+      }
+      __syncthreads();
+    } else {
+      // Very long row: rank every element by counting (correct, quadratic).
+      for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
+        const unsigned long long ce = ((unsigned long long)bkey[a + e] << 32) | bidx[a + e];
+        uint32_t rk = 0;
+        for (uint32_t f = 0; f < len; ++f)
+          rk += (((unsigned long long)bkey[a + f] << 32) | bidx[a + f]) < ce ? 1u : 0u;
+        skey[a + rk] = (uint32_t)(ce >> 32);
+        sidx[a + rk] = (uint32_t)ce;
+        smap[a + rk] = a + e;
+      }
+    }
+  }
 }
 
 }  // namespace bucket

@@ -48,7 +48,8 @@ struct PointScratch {
   DevBuf<uint32_t> keys[2], vals[2];
   DevBuf<uint32_t> hist, base, counters;  // per-tile digit histograms, digit totals
   DevBuf<uint32_t> rowstart;
-  DevBuf<uint32_t> rowaux;  // bucket sort: row counts/cursors | scan status | ticket
+  DevBuf<uint32_t> rowaux;  // bucket sort: row counts | scan status | ticket | long rows
+  DevBuf<uint32_t> smap;    // bucket sort: sorted position -> record slot
   DevBuf<int> rec_cx;
   DevBuf<double> rec;         // 12 x cap weight records (spread)
   DevBuf<uint32_t> run_keys;  // lazily filled

@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstdio>
+#include <string>
 
 #include "ibc_internal.h"
 #include "ibc_sort.cuh"
@@ -775,10 +776,14 @@ void PointScratch::release_all() {
   }
   hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
+  smap.release();
   cap = 0;
 }
 
 namespace {
+void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
+                   size_t n, PointScratch& s, bool spread);
+
 // Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
 bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
   if (g.dim < 2) return false;
@@ -811,17 +816,23 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   cudaStream_t st = ctx.stream;
   sp::SweepTiling W;
   const bool sweep = sweep_tiling(g, W);
-  if (n > 0) {
-    sort_points(ctx, g, d_points, n, s, false, sweep ? sort::kPayloadWeights : sort::kPayloadNone,
-                d_values);
+  const bool radix = getenv("IBC_SORT") && std::string(getenv("IBC_SORT")) == "radix";
+  if (sweep && !radix) {
+    bucket_points(ctx, g, d_points, d_values, n, s, true);
   } else {
-    s.last_n = 0;
-    s.sorted_keys = s.keys[0].p;
-    s.sorted_perm = s.vals[0].p;
-    s.run_keys_valid = false;
-    s.keys_are_rows = false;
+    if (n > 0) {
+      sort_points(ctx, g, d_points, n, s, false, sweep ? sort::kPayloadWeights : sort::kPayloadNone,
+                  d_values);
+    } else {
+      s.last_n = 0;
+      s.sorted_keys = s.keys[0].p;
+      s.sorted_perm = s.vals[0].p;
+      s.run_keys_valid = false;
+      s.keys_are_rows = false;
+    }
+    row_table(ctx, g, n, s);
   }
-  row_table(ctx, g, n, s);
+  const uint32_t* smap = (sweep && !radix) ? s.smap.p : nullptr;
   cudaEvent_t ev = nullptr;
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
@@ -838,11 +849,11 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     const size_t smem = (size_t)W.wpc * (g.dim == 3 ? 4 : 1) * W.rl * sizeof(double);
     const unsigned blocks = (unsigned)(W.nyg * W.nzc);
     if (g.dim == 3)
-      sp::spread_sweep_kernel<3><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, s.rec.p,
-                                                                   s.rec_cx.p, d_out);
+      sp::spread_sweep_kernel<3><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, smap,
+                                                                   s.rec.p, s.rec_cx.p, d_out);
     else
-      sp::spread_sweep_kernel<2><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, s.rec.p,
-                                                                   s.rec_cx.p, d_out);
+      sp::spread_sweep_kernel<2><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, smap,
+                                                                   s.rec.p, s.rec_cx.p, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   } else {
@@ -949,39 +960,81 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
 }  // namespace tma
 
 namespace {
-// Row bucketing of the interpolation points (ibc_bucket.cuh): s.rowstart and
-// 32-byte records in s.rec, grouped by row.
-void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, size_t n, PointScratch& s) {
+// Row bucket sort (ibc_bucket.cuh).  Interpolation: records {x, y, z, index}
+// in s.rec grouped by row.  Spread: the weight records (s.rec, s.rec_cx) in
+// bucket slots, plus the stable key order -- s.sorted_keys / s.sorted_perm
+// (the reference's ws.keys / ws.perm) and s.smap (sorted position -> slot).
+void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
+                   size_t n, PointScratch& s, bool spread) {
   cudaStream_t st = ctx.stream;
   const uint32_t nrows = g.nrows;
   const uint32_t nchunks = (nrows + bucket::kChunk - 1) / bucket::kChunk;
-  s.rowaux.ensure((size_t)nrows + nchunks + 8);
+  s.rowaux.ensure(2 * (size_t)nrows + nchunks + 8);
   uint32_t* count = s.rowaux.p;
-  uint32_t* status = s.rowaux.p + nrows;
+  uint32_t* status = count + nrows;
   uint32_t* ticket = status + nchunks;
-  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 1) * 4, st));
+  uint32_t* nlong = ticket + 1;
+  uint32_t* long_rows = nlong + 1;
+  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 2) * 4, st));
+  if (n == 0) {
+    IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)nrows + 1) * 4, st));
+    return;
+  }
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
   const unsigned blocks = grid_for(n, bucket::kThreads);
+  const int full = spread ? 1 : 0;
   if (g.dim == 3)
-    bucket::row_keys_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n,
-                                                                    s.keys[0].p, s.vals[0].p, count);
+    bucket::keys_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
+                                                                s.keys[0].p, s.vals[0].p, count);
   else if (g.dim == 2)
-    bucket::row_keys_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n,
-                                                                    s.keys[0].p, s.vals[0].p, count);
+    bucket::keys_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
+                                                                s.keys[0].p, s.vals[0].p, count);
   else
-    bucket::row_keys_kernel<1><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n,
-                                                                    s.keys[0].p, s.vals[0].p, count);
+    bucket::keys_kernel<1><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
+                                                                s.keys[0].p, s.vals[0].p, count);
   ctx.prof_end(kProfKeys, ev);
   ctx.prof_begin(kProfSort, &ev);
-  bucket::row_scan_kernel<<<nchunks, bucket::kScanThreads, 0, st>>>(count, s.rowstart.p, nrows,
-                                                                    status, ticket);
-  bucket::scatter_kernel<<<blocks, bucket::kThreads, 0, st>>>(
-      d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+  bucket::row_scan_kernel<<<nchunks, bucket::kScanThreads, 0, st>>>(
+      count, s.rowstart.p, nrows, status, ticket, spread ? long_rows : nullptr, nlong);
+  ctx.launches += 2;
+  if (!spread) {
+    bucket::scatter_interp_kernel<<<blocks, bucket::kThreads, 0, st>>>(
+        d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+    ctx.launches += 1;
+    s.last_n = 0;  // interpolation leaves no observable sort
+  } else {
+    s.smap.ensure(n);
+    if (g.dim == 3)
+      bucket::scatter_spread_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
+          g, d_points, d_values, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.keys[1].p,
+          s.vals[1].p, s.rec.p, s.rec_cx.p);
+    else
+      bucket::scatter_spread_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
+          g, d_points, d_values, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.keys[1].p,
+          s.vals[1].p, s.rec.p, s.rec_cx.p);
+    const unsigned rblocks = std::min<unsigned>(grid_for(nrows, bucket::kThreads / 32), 148u * 16u);
+    bucket::row_sort_kernel<<<rblocks, bucket::kThreads, 0, st>>>(
+        s.rowstart.p, nrows, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p, s.smap.p);
+    static bool attr_set[64] = {};
+    const size_t lsm = (size_t)bucket::kLongSortMax * 12;
+    if (!attr_set[ctx.device & 63]) {
+      IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+      attr_set[ctx.device & 63] = true;
+    }
+    bucket::long_row_sort_kernel<<<148, bucket::kLongThreads, lsm, st>>>(
+        s.rowstart.p, long_rows, nlong, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p,
+        s.smap.p);
+    ctx.launches += 3;
+    s.sorted_keys = s.keys[0].p;
+    s.sorted_perm = s.vals[0].p;
+    s.last_n = n;
+    s.run_keys_valid = false;
+    s.keys_are_rows = false;
+  }
   ctx.prof_end(kProfSort, ev);
-  ctx.launches += 3;
   IBC_CUDA(cudaGetLastError());
-  s.last_n = 0;  // interpolation leaves no observable sort
 }
 
 bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
@@ -993,7 +1046,7 @@ bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, cons
   CUtensorMap map_box;
   if (!tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax)) return false;
   cudaStream_t st = ctx.stream;
-  bucket_points(ctx, g, d_points, n, s);
+  bucket_points(ctx, g, d_points, nullptr, n, s, false);
   const size_t smem = interp_tma_smem(T);
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {

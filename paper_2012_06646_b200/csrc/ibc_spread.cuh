@@ -48,6 +48,7 @@ __device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
 template <int D>
 __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTiling T,
                                                            const uint32_t* __restrict__ rowstart,
+                                                           const uint32_t* __restrict__ smap,
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
@@ -108,10 +109,11 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
         const int j = (p >= e0) + (p >= e1) + (p >= e2);
         const uint32_t rbj = __shfl_sync(0xffffffffu, rb, j & 3);
         const uint32_t pre = __shfl_sync(0xffffffffu, incl - len, j & 3);
-        const uint32_t r = rbj + (p - pre);
+        const uint32_t rs = rbj + (p - pre);
         int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
         double4 gx = make_double4(0.0, 0.0, 0.0, 0.0), tyz = gx;
         if (valid) {
+          const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
           const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
           const double2 g01 = __ldg(r2), g23 = __ldg(r2 + 1), ty2 = __ldg(r2 + 2), tz2 = __ldg(r2 + 3);
           gx = make_double4(g01.x, g01.y, g23.x, g23.y);
