@@ -4,11 +4,10 @@
 // l_m = sum_sigma sum_{p in cell(m - sigma)} w_sigma(t_p) G_p, with every grid
 // value written to HBM exactly once and no global atomics.
 //
-// Inputs: the points sorted by cell key (ibc_sort.cuh, stable), each with a
-// 64-byte weight record written by the last radix pass -- G * phi_x(k-2-t_x)/h
-// for k = 0..3 and sin/cos(pi u / 2) of the y and z displacements -- plus its
-// home cell along x; and the row start table (rows of the sorted keys are
-// contiguous).
+// Inputs: the points in stable cell-key order (ibc_bucket.cuh / ibc_sort.cuh),
+// each with a 64-byte weight record -- G * phi_x(k-2-t_x)/h for k = 0..3 and
+// sin/cos(pi u / 2) of the y and z displacements -- and its home cell along x;
+// and the row start table (rows of the sorted keys are contiguous).
 //
 // Each warp owns ONE target row (ty) of a z-chunk [z0, z1) and sweeps the
 // source planes z0-1 .. z1+1.  Its private shared-memory window holds the row
@@ -20,10 +19,13 @@
 // Lanes that share a home cx -- same cell, or different source rows -- would
 // hit the same address: all but the first (match_any) are deferred to the
 // next batch, so batches stay full, adds never collide, and the summation
-// order is the sequence order -- results are bitwise reproducible.  When plane s is done, target plane s-2 is complete:
-// the warp folds the periodic x pad, stores the row once (coalesced) and
-// clears the slot for plane s+2.  No CTA barrier anywhere: warps are
-// independent, which is what lets 24 of them per SM hide the record loads.
+// order is the sequence order -- results are bitwise reproducible.  When plane
+// s is done, target plane s-2 is complete: the warp folds the periodic x pad,
+// stores the row once (coalesced) and clears the slot for plane s+2.  No CTA
+// barrier anywhere: warps are independent, which is what lets 24 of them per
+// SM hide the record loads.  The inner loop is kept lean (the kernel is
+// issue-bound): per-plane slot offsets are hoisted, weights are a handful of
+// FMAs, deferral compaction is a popc binary search.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -44,6 +46,21 @@ struct SweepTiling {
 };
 
 __device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
+
+// Position of the n-th (0-based) set bit of m (popc(m) > n).
+__device__ __forceinline__ int nth_set(uint32_t m, int n) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int c = __popc(m & ((1u << w) - 1u));
+    if (n >= c) {
+      n -= c;
+      m >>= w;
+      pos += w;
+    }
+  }
+  return pos;
+}
 
 template <int D>
 __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTiling T,
@@ -75,6 +92,13 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
     const bool zok = D != 3 || pz || (s >= -1 && s <= nz);
     if (zok) {
       const int szw = D == 3 ? (pz ? wrap_cell(s, nz) : s) : 0;
+      // Window slot offset of target plane s + kz - 2 (-1: outside [z0, z1)).
+      int so[4];
+#pragma unroll
+      for (int kz = 0; kz < 4; ++kz) {
+        const int tz = s + kz - 2;
+        so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * T.rl : -1) : (kz == 2 ? 0 : -1);
+      }
       // Lane j < 4: source row cy = ty + 2 - j (sigma_y = j - 2).
       uint32_t rb = 0, len = 0;
       if (lane < 4) {
@@ -96,10 +120,7 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
       }
       const uint32_t e0 = __shfl_sync(0xffffffffu, incl, 0), e1 = __shfl_sync(0xffffffffu, incl, 1);
       const uint32_t e2 = __shfl_sync(0xffffffffu, incl, 2), total = __shfl_sync(0xffffffffu, incl, 3);
-      // Batches of 32 distinct home cx: a lane whose cx already occurs in the
-      // batch (same cell, or another source row) is deferred to the front of
-      // the next batch, so every batch's adds hit distinct addresses and the
-      // summation order (sequence order) is fixed.
+      const uint32_t rstart = rb - (incl - len);  // sorted index = rstart_j + p
       uint32_t next = 0;   // next unread position in the concatenated rows
       int ndef = 0;        // deferred lanes carried into this batch
       uint32_t p_def = 0;  // this lane's deferred position (lanes < ndef)
@@ -107,66 +128,49 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
         const uint32_t p = lane < ndef ? p_def : next + (uint32_t)(lane - ndef);
         const bool valid = lane < ndef || p < total;
         const int j = (p >= e0) + (p >= e1) + (p >= e2);
-        const uint32_t rbj = __shfl_sync(0xffffffffu, rb, j & 3);
-        const uint32_t pre = __shfl_sync(0xffffffffu, incl - len, j & 3);
-        const uint32_t rs = rbj + (p - pre);
+        const uint32_t rs = __shfl_sync(0xffffffffu, rstart, j & 3) + p;
         int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
-        double4 gx = make_double4(0.0, 0.0, 0.0, 0.0), tyz = gx;
+        double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
         if (valid) {
           const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
           const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
-          const double2 g01 = __ldg(r2), g23 = __ldg(r2 + 1), ty2 = __ldg(r2 + 2), tz2 = __ldg(r2 + 3);
-          gx = make_double4(g01.x, g01.y, g23.x, g23.y);
-          tyz = make_double4(ty2.x, ty2.y, tz2.x, tz2.y);
+          g01 = __ldg(r2);
+          g23 = __ldg(r2 + 1);
+          tr = __ldg(r2 + 2);
+          tz2 = __ldg(r2 + 3);
           cx = __ldg(rcx + r);
         }
-        const uint32_t peers = __match_any_sync(0xffffffffu, cx);
-        const bool first = (peers & lt) == 0u;
-        const bool on = valid && first;
-        // Carry the deferred lanes (in lane order) to the next batch.
-        const uint32_t defm = __ballot_sync(0xffffffffu, valid && !first);
+        const uint32_t peers = __match_any_sync(0xffffffffu, cx);  // every lane takes part
+        const bool on = valid && (peers & lt) == 0u;
+        // Compact the deferred lanes (same cx as an earlier lane) to the front.
+        const uint32_t defm = __ballot_sync(0xffffffffu, valid && !on);
         const int newdef = __popc(defm);
-        {
-          // Lane k of the next batch takes the k-th deferred position.
-          int src = 0;
-          uint32_t m = defm;
-          for (int k = 0; k < lane && m; ++k) m &= m - 1u;
-          src = m ? __ffs(m) - 1 : 0;
-          const uint32_t pd = __shfl_sync(0xffffffffu, p, src);
-          if (lane < newdef) p_def = pd;
-        }
-        next += (uint32_t)(32 - ndef);
-        if (next > total) next = total;
+        const uint32_t pd = __shfl_sync(0xffffffffu, p, lane < newdef ? nth_set(defm, lane) : 0);
+        if (lane < newdef) p_def = pd;
+        next = min(total, next + (uint32_t)(32 - ndef));
         ndef = newdef;
-        // phi(sigma - t)/h over sigma = -2..1 is (1-c), (1+s), (1+c), (1-s) / 4h.
-        const int sy = j - 2;
-        const double wy = q * (sy == -2 ? 1.0 - tyz.y : sy == -1 ? 1.0 + tyz.x : sy == 0 ? 1.0 + tyz.y : 1.0 - tyz.x);
+        // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
+        const double vy = (j & 1) ? tr.x : tr.y;
+        const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
         double a[4];
         if (D == 3) {
-          a[0] = wy * (q * (1.0 - tyz.w));
-          a[1] = wy * (q * (1.0 + tyz.z));
-          a[2] = wy * (q * (1.0 + tyz.w));
-          a[3] = wy * (q * (1.0 - tyz.z));
+          a[0] = fma(-wq, tz2.y, wq);
+          a[1] = fma(wq, tz2.x, wq);
+          a[2] = fma(wq, tz2.y, wq);
+          a[3] = fma(-wq, tz2.x, wq);
         } else {
           a[0] = a[1] = a[3] = 0.0;
-          a[2] = wy;
+          a[2] = wq / q;
         }
-        const double gk[4] = {gx.x, gx.y, gx.z, gx.w};
+        const double gk[4] = {g01.x, g01.y, g23.x, g23.y};
         const int xb = cx + (kPadL - 2);
 #pragma unroll
         for (int kx = 0; kx < 4; ++kx) {
           if (on) {
             const int addr = skew(xb + kx);
-            const double v = gk[kx];
 #pragma unroll
-            for (int kz = 0; kz < 4; ++kz) {
-              if (D == 3) {
-                const int tz = s + kz - 2;
-                if (tz >= z0 && tz < z1) W[(tz & 3) * T.rl + addr] += v * a[kz];
-              } else if (kz == 2) {
-                W[addr] += v * a[2];
-              }
-            }
+            for (int kz = 0; kz < 4; ++kz)
+              if (so[kz] >= 0) W[so[kz] + addr] += gk[kx] * a[kz];
           }
           __syncwarp();
         }
@@ -177,16 +181,26 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
     if (t >= z0 && t < z1) {
       double* Wr = W + (D == 3 ? (t & 3) * T.rl : 0);
       double* orow = out + ((size_t)t * ny + ty) * nx;
-      for (int x = lane; x < nx; x += 32) {
-        double v = Wr[skew(x + kPadL)];
-        if (px) {
+      if (px && nx < 8) {
+        for (int x = lane; x < nx; x += 32) {
+          double v = Wr[skew(x + kPadL)];
           for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[skew(qx + kPadL)];
           for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[skew(qx + kPadL)];
+          orow[x] = v;
         }
-        orow[x] = v;
+      } else {
+        for (int x = lane; x < nx; x += 32) {
+          double v = Wr[skew(x + kPadL)];
+          if (px) {  // pads x' = -4..-1 fold onto nx-4.., x' = nx, nx+1 onto 0, 1
+            if (x >= nx - kPadL) v += Wr[skew(x - nx + kPadL)];
+            if (x < kPadR) v += Wr[skew(x + nx + kPadL)];
+          }
+          orow[x] = v;
+        }
       }
       __syncwarp();
-      for (int i = lane; i < T.rl; i += 32) Wr[i] = 0.0;
+      double2* Z = reinterpret_cast<double2*>(Wr);
+      for (int i = lane; i < T.rl / 2; i += 32) Z[i] = make_double2(0.0, 0.0);
       __syncwarp();
     }
   }
