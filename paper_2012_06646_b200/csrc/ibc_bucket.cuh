@@ -7,18 +7,19 @@
 //      its arrival rank in the row (the row-count atomic's return value);
 //   K2 single-pass scan of the row counts (decoupled look-back over 4096-row
 //      chunks) -> the row start table;
-//   K3 atomic-free scatter to row start + rank, writing the operator's
-//      per-point record (interpolation: {x, y, z, index}; spread: the 64-byte
-//      weight record + home cx + key + index).
+//   K3 atomic-free scatter to row start + rank (interpolation: the record
+//      {x, y, z, index}; spread: the (key, index) pair).
 // Interpolation results do not depend on the order inside a row (each point
 // is summed alone, into its own slot), so K1-K3 are all it needs.  The spread
 // sums many points into each grid value, and the reference exposes the stable
 // key order (ws.keys / ws.perm, spread.hpp:33-34), so a fourth kernel puts
 // every row into stable (key, index) order -- which makes the result exactly
-// the reference's stable key-value sort -- and records where each sorted
-// element's record sits:
+// the reference's stable key-value sort -- and a fifth writes the weight
+// records in that order:
 //   K4 rows of <= 32 points: one warp, rank by 32 shuffled compares;
-//      longer rows (listed by K2): one CTA, bitonic sort in shared memory.
+//      longer rows (listed by K2): one CTA, bitonic sort in shared memory;
+//   K5 per sorted position: cell + one sin/cos pair per axis -> the 64-byte
+//      record the spread sweep streams (coalesced writes).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -169,19 +170,33 @@ __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
   reinterpret_cast<double4*>(rec)[slot] = r;
 }
 
-// K3, spread: key, index and the 64-byte weight record at row start + rank:
-//   {G phi_x(k-2-t_x)/h (k = 0..3), sin/cos(pi u_y/2), sin/cos(pi u_z/2)},
-// and the home cell along x (wrapped on periodic x).
-template <int D>
-__global__ void __launch_bounds__(kThreads) scatter_spread_kernel(
-    DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
+// K3, spread: (key, index) at row start + rank (the rows' stable order comes
+// from K4; the weight records are then written in that order by K5).
+__global__ void __launch_bounds__(kThreads) scatter_pairs_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
-    const uint32_t* __restrict__ start, uint32_t* __restrict__ bkey, uint32_t* __restrict__ bidx,
-    double* __restrict__ brec, int* __restrict__ bcx) {
+    uint32_t rowdiv, const uint32_t* __restrict__ start, uint32_t* __restrict__ bkey,
+    uint32_t* __restrict__ bidx) {
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const uint32_t key = __ldg(keys + i);
-  const uint32_t slot = __ldg(start + key / g.rowdiv) + __ldg(rank + i);
+  const uint32_t slot = __ldg(start + key / rowdiv) + __ldg(rank + i);
+  bkey[slot] = key;
+  bidx[slot] = i;
+}
+
+// K5, spread: the 64-byte weight record of every sorted position, written in
+// sorted order (coalesced):
+//   {G phi_x(k-2-t_x)/h (k = 0..3), sin/cos(pi u_y/2), sin/cos(pi u_z/2)},
+// and the home cell along x (wrapped on periodic x).
+template <int D>
+__global__ void __launch_bounds__(kThreads) records_kernel(DevGrid g, const double* __restrict__ X,
+                                                           const double* __restrict__ G,
+                                                           const uint32_t* __restrict__ perm,
+                                                           uint32_t n, double* __restrict__ rec,
+                                                           int* __restrict__ rcx) {
+  const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
+  if (o >= n) return;
+  const uint32_t i = __ldg(perm + o);
   double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};  // u = 0 on padded axes
   int cx = 0;
 #pragma unroll
@@ -192,21 +207,18 @@ __global__ void __launch_bounds__(kThreads) scatter_spread_kernel(
     sincos_half_pi(u, &tr[a][0], &tr[a][1]);
   }
   const double gq = __ldg(G + i) * (0.25 * g.inv_h);
-  double4* r4 = reinterpret_cast<double4*>(brec) + 2 * (size_t)slot;
+  double4* r4 = reinterpret_cast<double4*>(rec) + 2 * (size_t)o;
   r4[0] = make_double4(gq * (1.0 - tr[0][1]), gq * (1.0 + tr[0][0]), gq * (1.0 + tr[0][1]),
                        gq * (1.0 - tr[0][0]));
   r4[1] = make_double4(tr[1][0], tr[1][1], tr[2][0], tr[2][1]);
-  bcx[slot] = cx;
-  bkey[slot] = key;
-  bidx[slot] = i;
+  rcx[o] = cx;
 }
 
 // K4, short rows: one warp per row puts (key, index) in stable order.
 // sorted position -> (key, index, bucket slot of its record).
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     const uint32_t* __restrict__ start, uint32_t nrows, const uint32_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
-    uint32_t* __restrict__ smap) {
+    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (kThreads / 32);
   for (uint32_t r = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
@@ -223,7 +235,6 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     if (valid) {
       skey[a + rk] = k;
       sidx[a + rk] = ix;
-      smap[a + rk] = a + lane;
     }
   }
 }
@@ -234,10 +245,8 @@ constexpr int kLongThreads = 1024;
 __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     const uint32_t* __restrict__ start, const uint32_t* __restrict__ long_rows,
     const uint32_t* __restrict__ nlong, const uint32_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
-    uint32_t* __restrict__ smap) {
-  extern __shared__ unsigned long long sk[];  // [kLongSortMax] keys, then [kLongSortMax] slots
-  uint32_t* sslot = reinterpret_cast<uint32_t*>(sk + kLongSortMax);
+    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx) {
+  extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
   const uint32_t count = *nlong;
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = long_rows[li];
@@ -247,7 +256,6 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
       while (m < len) m <<= 1;
       for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
         sk[e] = e < len ? ((unsigned long long)bkey[a + e] << 32) | bidx[a + e] : ~0ull;
-        sslot[e] = a + e;
       }
       __syncthreads();
       for (uint32_t size = 2; size <= m; size <<= 1) {
@@ -260,9 +268,6 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
               if ((x > y) == up) {
                 sk[e] = y;
                 sk[p] = x;
-                const uint32_t t = sslot[e];
-                sslot[e] = sslot[p];
-                sslot[p] = t;
               }
             }
           }
@@ -272,7 +277,6 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
         skey[a + e] = (uint32_t)(sk[e] >> 32);
         sidx[a + e] = (uint32_t)sk[e];
-        smap[a + e] = sslot[e];
       }
       __syncthreads();
     } else {
@@ -284,7 +288,6 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
           rk += (((unsigned long long)bkey[a + f] << 32) | bidx[a + f]) < ce ? 1u : 0u;
         skey[a + rk] = (uint32_t)(ce >> 32);
         sidx[a + rk] = (uint32_t)ce;
-        smap[a + rk] = a + e;
       }
     }
   }

@@ -832,7 +832,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     }
     row_table(ctx, g, n, s);
   }
-  const uint32_t* smap = (sweep && !radix) ? s.smap.p : nullptr;
+  const uint32_t* smap = nullptr;  // records are in sorted order on both sort paths
   cudaEvent_t ev = nullptr;
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
@@ -1004,29 +1004,27 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
-    s.smap.ensure(n);
-    if (g.dim == 3)
-      bucket::scatter_spread_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
-          g, d_points, d_values, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.keys[1].p,
-          s.vals[1].p, s.rec.p, s.rec_cx.p);
-    else
-      bucket::scatter_spread_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
-          g, d_points, d_values, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.keys[1].p,
-          s.vals[1].p, s.rec.p, s.rec_cx.p);
+    bucket::scatter_pairs_kernel<<<blocks, bucket::kThreads, 0, st>>>(
+        s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.keys[1].p, s.vals[1].p);
     const unsigned rblocks = std::min<unsigned>(grid_for(nrows, bucket::kThreads / 32), 148u * 16u);
     bucket::row_sort_kernel<<<rblocks, bucket::kThreads, 0, st>>>(
-        s.rowstart.p, nrows, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p, s.smap.p);
+        s.rowstart.p, nrows, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p);
     static bool attr_set[64] = {};
-    const size_t lsm = (size_t)bucket::kLongSortMax * 12;
+    const size_t lsm = (size_t)bucket::kLongSortMax * 8;
     if (!attr_set[ctx.device & 63]) {
       IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
       attr_set[ctx.device & 63] = true;
     }
     bucket::long_row_sort_kernel<<<148, bucket::kLongThreads, lsm, st>>>(
-        s.rowstart.p, long_rows, nlong, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p,
-        s.smap.p);
-    ctx.launches += 3;
+        s.rowstart.p, long_rows, nlong, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p);
+    if (g.dim == 3)
+      bucket::records_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
+          g, d_points, d_values, s.vals[0].p, (uint32_t)n, s.rec.p, s.rec_cx.p);
+    else
+      bucket::records_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
+          g, d_points, d_values, s.vals[0].p, (uint32_t)n, s.rec.p, s.rec_cx.p);
+    ctx.launches += 4;
     s.sorted_keys = s.keys[0].p;
     s.sorted_perm = s.vals[0].p;
     s.last_n = n;
