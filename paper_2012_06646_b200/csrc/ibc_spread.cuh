@@ -88,29 +88,38 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
   const uint32_t lt = (1u << lane) - 1u;
   const int s_lo = D == 3 ? z0 - 1 : 0, s_hi = D == 3 ? z1 + 1 : 0;
 
-  for (int s = s_lo; s <= s_hi; ++s) {
+  // Lane j < 4: sorted range of source row cy = ty + 2 - j (sigma_y = j - 2)
+  // of source plane s; the next plane's ranges are loaded while this one runs.
+  auto ranges = [&](int s, uint32_t& rb, uint32_t& len) {
+    rb = 0;
+    len = 0;
     const bool zok = D != 3 || pz || (s >= -1 && s <= nz);
-    if (zok) {
+    if (lane < 4 && zok && s <= s_hi) {
       const int szw = D == 3 ? (pz ? wrap_cell(s, nz) : s) : 0;
+      int cy = ty + 2 - lane;
+      bool ok = true;
+      if (py) cy = wrap_cell(cy, ny);
+      else ok = cy >= -1 && cy <= ny;
+      if (ok) {
+        const uint32_t rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
+        rb = __ldg(rowstart + rid);
+        len = __ldg(rowstart + rid + 1) - rb;
+      }
+    }
+  };
+  uint32_t rb_n, len_n;
+  ranges(s_lo, rb_n, len_n);
+
+  for (int s = s_lo; s <= s_hi; ++s) {
+    const uint32_t rb = rb_n, len = len_n;
+    ranges(s + 1, rb_n, len_n);
+    {
       // Window slot offset of target plane s + kz - 2 (-1: outside [z0, z1)).
       int so[4];
 #pragma unroll
       for (int kz = 0; kz < 4; ++kz) {
         const int tz = s + kz - 2;
         so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * T.rl : -1) : (kz == 2 ? 0 : -1);
-      }
-      // Lane j < 4: source row cy = ty + 2 - j (sigma_y = j - 2).
-      uint32_t rb = 0, len = 0;
-      if (lane < 4) {
-        int cy = ty + 2 - lane;
-        bool ok = true;
-        if (py) cy = wrap_cell(cy, ny);
-        else ok = cy >= -1 && cy <= ny;
-        if (ok) {
-          const uint32_t rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
-          rb = __ldg(rowstart + rid);
-          len = __ldg(rowstart + rid + 1) - rb;
-        }
       }
       uint32_t incl = len;
 #pragma unroll
