@@ -145,6 +145,36 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
                                   const double* d_field, const double* d_points, size_t n,
                                   double* d_out);
 
+/* Multi-GPU z-slab decomposition (no reference analog: the
+ * paper defers multi-device runs).  A rank owns home planes
+ * [z0, z1) of the last axis of a global grid and works on a LOCAL grid of
+ * planes [z0 - 2, z1 + 1): same extents/spacing/staggering/origin as the
+ * global grid except extent[dim-1] = z1 - z0 + 3 and periodic[dim-1] = 0.
+ * Cells along that axis are computed in global coordinates (bit-identical to
+ * the single-grid keys) and shifted by z_first = z0 - 2, so a point homed in
+ * [z0, z1) spreads into local planes [0, z1 - z0 + 3) with no loss, and reads
+ * them when interpolating.  The ghost-plane sum after spreading and the halo
+ * fill before interpolating are the caller's exchange (paper_2012_06646_b200/
+ * slab.py, NCCL send/recv between ring neighbours). */
+typedef struct {
+  int z_first;          /* global plane of local plane 0 (z0 - 2) */
+  int nz_global;        /* global extent of the last axis */
+  int periodic_global;  /* global periodicity of the last axis */
+} ibc_slab;
+
+ibc_status ibc_spread_slab_device(ibc_context* ctx, const ibc_grid* local_grid,
+                                  const ibc_slab* slab, ibc_kernel kernel, const double* d_points,
+                                  const double* d_values, size_t n, ibc_workspace* ws,
+                                  double* d_out);
+ibc_status ibc_interpolate_slab_device(ibc_context* ctx, const ibc_grid* local_grid,
+                                       const ibc_slab* slab, ibc_kernel kernel,
+                                       const double* d_field, const double* d_points, size_t n,
+                                       double* d_out);
+/* Wrapped home cell along the last axis (cell_index + wrap, grid.hpp:121-151)
+ * of every point of a global grid: the slab each point belongs to. */
+ibc_status ibc_home_planes_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                  const double* d_points, size_t n, int32_t* d_planes);
+
 /* ib::stats (stats.hpp:9-25): every operation adds n_points * 4^dim. */
 uint64_t ibc_delta_evaluations(void);
 void ibc_reset_delta_evaluations(void);

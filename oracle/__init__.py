@@ -72,6 +72,7 @@ _ORACLE_SIGS = {
     "or_grid_check": (C.c_int, [_G]),
     "or_cell_key": (C.c_uint32, [_G, C.POINTER(C.c_int)]),
     "or_cell_index": (None, [_G, C.POINTER(C.c_double), C.c_int, C.POINTER(C.c_int)]),
+    "or_wrap_position": (None, [_G, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "or_grid_index": (C.c_uint32, [_G, C.POINTER(C.c_int)]),
     "or_cell_key_inverse": (None, [_G, C.c_uint32, C.POINTER(C.c_int)]),
     "or_cosine_phi": (C.c_double, [C.c_double]),
@@ -173,6 +174,28 @@ def interpolate(g, field, points):
     n = p.size // g.dim
     out = np.zeros(n, np.float64)
     lib().or_interpolate(C.byref(g), f, p, n, out)
+    return out
+
+
+def home_cells(g, points, wrap=True):
+    """cell_index(wrap_position(x)) with periodic axes wrapped into [0, n)
+    (grid.hpp:121-151, 197-207): the home cell of every point, (n, dim) ints.
+    wrap=False leaves the cell unwrapped (it can equal n on a periodic axis)."""
+    p = _pts(points, g.dim).reshape(-1, g.dim)
+    out = np.zeros((p.shape[0], g.dim), np.int64)
+    x = (C.c_double * 3)()
+    w = (C.c_double * 3)()
+    c = (C.c_int * 3)()
+    for i in range(p.shape[0]):
+        for a in range(g.dim):
+            x[a] = p[i, a]
+        lib().or_wrap_position(C.byref(g), x, w)
+        lib().or_cell_index(C.byref(g), w, 4, c)
+        for a in range(g.dim):
+            v = c[a]
+            if g.periodic[a] and wrap:
+                v %= g.extent[a]
+            out[i, a] = v
     return out
 
 

@@ -50,6 +50,14 @@ class IbcProfile(C.Structure):
     ]
 
 
+class IbcSlab(C.Structure):
+    _fields_ = [
+        ("z_first", C.c_int),
+        ("nz_global", C.c_int),
+        ("periodic_global", C.c_int),
+    ]
+
+
 _vp = C.c_void_p
 _sz = C.c_size_t
 _G = C.POINTER(IbcGrid)
@@ -79,6 +87,9 @@ SIGNATURES = {
     "ibc_interpolate": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, C.c_int, _vp]),
     "ibc_spread_device": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, _vp, _vp]),
     "ibc_interpolate_device": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, _vp]),
+    "ibc_spread_slab_device": (_st, [_vp, _G, C.POINTER(IbcSlab), C.c_int, _vp, _vp, _sz, _vp, _vp]),
+    "ibc_interpolate_slab_device": (_st, [_vp, _G, C.POINTER(IbcSlab), C.c_int, _vp, _vp, _sz, _vp]),
+    "ibc_home_planes_device": (_st, [_vp, _G, C.c_int, _vp, _sz, _vp]),
     "ibc_delta_evaluations": (C.c_uint64, []),
     "ibc_reset_delta_evaluations": (None, []),
 }

@@ -468,6 +468,72 @@ int ibc_debug_zsweep_trace(int block, long long* out) {
   return (int)ibc::debug_zsweep_trace(block, out);
 }
 
+static void check_slab(const ibc_grid* grid, const ibc_slab* slab) {
+  if (!slab) invalid("slab is null");
+  if (grid->dim < 2) invalid("slab decomposition needs a 2- or 3-dimensional grid");
+  const int a = grid->dim - 1;
+  if (grid->periodic[a]) invalid("the slab axis of a local grid is not periodic");
+  if (slab->nz_global < 1 || grid->extent[a] < 3) invalid("bad slab extents");
+}
+
+ibc_status ibc_spread_slab_device(ibc_context* ctx, const ibc_grid* grid, const ibc_slab* slab,
+                                  ibc_kernel kernel, const double* d_points,
+                                  const double* d_values, size_t n, ibc_workspace* ws,
+                                  double* d_out) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_grid(grid);
+    check_slab(grid, slab);
+    check_kernel(kernel);
+    check_points(n);
+    if (ws) {
+      if (ws->w.point_count != n) invalid("workspace sized for a different point count");
+      if (ws->w.grid_points != grid_points(grid)) invalid("workspace sized for a different grid");
+    }
+    if (!d_out) invalid("null output buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, *slab);
+    ibc::PointScratch& s = spread_scratch_for(c, ws, n, g);
+    ibc::spread_pipeline(c, g, d_points, d_values, n, s, d_out);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+  });
+}
+
+ibc_status ibc_interpolate_slab_device(ibc_context* ctx, const ibc_grid* grid,
+                                       const ibc_slab* slab, ibc_kernel kernel,
+                                       const double* d_field, const double* d_points, size_t n,
+                                       double* d_out) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_grid(grid);
+    check_slab(grid, slab);
+    check_kernel(kernel);
+    check_points(n);
+    auto& c = ctx->c;
+    use_device(c);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, *slab);
+    c.interp_scratch.reserve_points(n, false);
+    c.interp_scratch.reserve_rows(g.nrows);
+    ibc::interp_pipeline(c, g, d_field, d_points, n, c.interp_scratch, d_out);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+  });
+}
+
+ibc_status ibc_home_planes_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                  const double* d_points, size_t n, int32_t* d_planes) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_grid(grid);
+    check_kernel(kernel);
+    check_points(n);
+    if (n && (!d_points || !d_planes)) invalid("null buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    ibc::home_planes(c, ibc::make_devgrid(*grid), d_points, n, d_planes);
+  });
+}
+
 uint64_t ibc_delta_evaluations(void) { return g_delta_evaluations.load(std::memory_order_relaxed); }
 void ibc_reset_delta_evaluations(void) { g_delta_evaluations.store(0, std::memory_order_relaxed); }
 

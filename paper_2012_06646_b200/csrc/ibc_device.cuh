@@ -31,6 +31,15 @@ struct DevGrid {
   int64_t npts;         // prod(extent)
   double hd;            // pow(h, dim), computed on the host with std::pow
   double inv_h;
+  // z-slab of a larger grid (multi-GPU, ibc_slab): the last axis is local
+  // planes [zfirst, zfirst + n[dim-1]) of a global axis of zg_n planes.  Its
+  // cells are computed in global coordinates -- bit-identical to the single
+  // grid's -- then shifted by zfirst; locally the axis is not periodic.
+  int zslab;            // 0 / 1
+  int zfirst;           // global plane of local plane 0
+  int zg_n;             // global extent of the last axis
+  int zg_periodic;      // global periodicity of the last axis
+  double zg_len;        // global axis length
 };
 
 __device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
@@ -49,7 +58,10 @@ __device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
 // correctly rounded quotient, so unless t = q - alpha lies within 1e-13 (|q|+1)
 // of an integer, ceil(t) is the reference's cell; otherwise (a ~1e-13 fraction
 // of points) the IEEE division is evaluated.
+__device__ __forceinline__ int cell_of_slab(const DevGrid& g, double x, double* xw);
+
 __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double* xw) {
+  if (g.zslab && a == g.dim - 1) return cell_of_slab(g, x, xw);
   double w = x;
   if (g.periodic[a]) {
     const double d = __dsub_rn(x, g.origin[a]);
@@ -68,11 +80,37 @@ __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double
   return (int)ceil(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]));
 }
 
+// Last axis of a slab grid: global wrap and cell (same arithmetic as
+// cell_of), wrapped into [0, zg_n) on a periodic global axis, then shifted to
+// the local plane.  *xw moves with the wrap (by whole periods) so the
+// displacement (xw - h (c + alpha) - o) / h is unchanged.
+__device__ __forceinline__ int cell_of_slab(const DevGrid& g, double x, double* xw) {
+  const int a = g.dim - 1;
+  double w = x;
+  if (g.zg_periodic) {
+    const double d = __dsub_rn(x, g.origin[a]);
+    double r = fabs(d) < g.zg_len ? d : fmod(d, g.zg_len);
+    if (r < 0.0) r = __dadd_rn(r, g.zg_len);
+    w = __dadd_rn(g.origin[a], r);
+  }
+  const double d = __dsub_rn(w, g.origin[a]);
+  const double q = __dmul_rn(d, g.inv_h);
+  const double t = __dsub_rn(q, g.alpha[a]);
+  double c = ceil(t);
+  const double margin = 1e-13 * (fabs(q) + 1.0);
+  if (!(c - t > margin && t - (c - 1.0) > margin)) c = ceil(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]));
+  const int cu = (int)c;
+  const int cw = g.zg_periodic ? wrap_cell(cu, g.zg_n) : cu;
+  *xw = w - (double)(cu - cw) * g.h;
+  return cw - g.zfirst;
+}
+
 // One axis of a DevGrid picked with a runtime index (selects, so the grid
 // stays in the parameter bank instead of being copied to local memory).
 struct Axis {
   double o, len, alpha;
   int n, periodic;
+  int shift;  // slab axis: local = global - shift
 };
 
 __device__ __forceinline__ Axis axis_of(const DevGrid& g, int a) {
@@ -82,6 +120,13 @@ __device__ __forceinline__ Axis axis_of(const DevGrid& g, int a) {
   r.alpha = a == 0 ? g.alpha[0] : (a == 1 ? g.alpha[1] : g.alpha[2]);
   r.n = a == 0 ? g.n[0] : (a == 1 ? g.n[1] : g.n[2]);
   r.periodic = a == 0 ? g.periodic[0] : (a == 1 ? g.periodic[1] : g.periodic[2]);
+  r.shift = 0;
+  if (g.zslab && a == g.dim - 1) {  // global wrap, then the local shift
+    r.len = g.zg_len;
+    r.n = g.zg_n;
+    r.periodic = g.zg_periodic;
+    r.shift = g.zfirst;
+  }
   return r;
 }
 
@@ -104,12 +149,13 @@ __device__ __forceinline__ int cell_and_u(const Axis& A, double h, double inv_h,
   const int ci = (int)c;
   const double hp = __dadd_rn(__dmul_rn(h, __dadd_rn(c, A.alpha)), A.o);
   *u = -((w - hp) * inv_h);
-  return A.periodic ? wrap_cell(ci, A.n) : ci;
+  return (A.periodic ? wrap_cell(ci, A.n) : ci) - A.shift;
 }
 
 // displacement_ratio (support_window.hpp:48-55): (xw - h*(i+alpha) - o) / h.
 // Only feeds the weights (not bit-exact anyway): multiply by 1/h.
 __device__ __forceinline__ double displacement(const DevGrid& g, int a, double xw, int c) {
+  if (g.zslab && a == g.dim - 1) c += g.zfirst;  // local plane -> global cell
   const double hp = __dadd_rn(__dmul_rn(g.h, __dadd_rn((double)c, g.alpha[a])), g.origin[a]);
   return (xw - hp) * g.inv_h;
 }

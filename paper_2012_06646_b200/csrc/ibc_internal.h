@@ -91,6 +91,9 @@ struct Workspace {
 
 // Pipelines (ibc_kernels.cu).  All enqueue on ctx.stream; no host sync.
 DevGrid make_devgrid(const ibc_grid& g);
+DevGrid make_devgrid(const ibc_grid& g, const ibc_slab& slab);  // z-slab of a larger grid
+// Wrapped home cell along the last axis of every point (slab binning key).
+void home_planes(Context& ctx, const DevGrid& g, const double* d_points, size_t n, int* d_planes);
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points,
                      const double* d_values, size_t n, PointScratch& s, double* d_out);
 void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field,

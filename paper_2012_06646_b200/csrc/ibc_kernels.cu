@@ -753,6 +753,39 @@ DevGrid make_devgrid(const ibc_grid& gi) {
   return g;
 }
 
+DevGrid make_devgrid(const ibc_grid& gi, const ibc_slab& slab) {
+  DevGrid g = make_devgrid(gi);
+  const int a = gi.dim - 1;
+  g.zslab = 1;
+  g.zfirst = slab.z_first;
+  g.zg_n = slab.nz_global;
+  g.zg_periodic = slab.periodic_global ? 1 : 0;
+  g.zg_len = slab.nz_global * gi.spacing;  // axis_length of the global grid (grid.hpp:72)
+  g.periodic[a] = 0;
+  return g;
+}
+
+namespace {
+__global__ void __launch_bounds__(kBlock) home_planes_kernel(DevGrid g, const double* __restrict__ X,
+                                                             uint32_t n, int* __restrict__ planes) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int a = g.dim - 1;
+  double xw;
+  int c = cell_of(g, a, __ldg(X + (size_t)i * g.dim + a), &xw);
+  if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
+  planes[i] = c;
+}
+}  // namespace
+
+void home_planes(Context& ctx, const DevGrid& g, const double* d_points, size_t n, int* d_planes) {
+  if (n == 0) return;
+  home_planes_kernel<<<grid_for(n, kBlock), kBlock, 0, ctx.stream>>>(g, d_points, (uint32_t)n,
+                                                                      d_planes);
+  ++ctx.launches;
+  IBC_CUDA(cudaGetLastError());
+}
+
 void PointScratch::reserve_points(size_t n, bool spread) {
   const size_t tiles = (n + sort::kTile - 1) / sort::kTile;
   for (int b = 0; b < 2; ++b) {

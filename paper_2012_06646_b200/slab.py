@@ -1,0 +1,276 @@
+"""Multi-GPU z-slab decomposition of the spread / interpolate path.
+
+The reference runs on one shared-memory node (parallel.hpp:25-36); the paper
+defers multi-device runs.  Here the grid's last axis (the slowest
+in the colex layout, grid.hpp:136-151, so a slab is one contiguous range of a
+GridField) is split into contiguous slabs, one per rank.  A rank owns home
+planes [z0, z1) and the Lagrangian points homed there; it works on a LOCAL
+grid of planes [z0 - 2, z1 + 1) (``ibc_slab``, include/ibcuda.h): cells are
+computed in global coordinates, so keys and weights are those of the single
+grid.
+
+* spread: local spread into the z1 - z0 + 3 planes, then a **ghost-plane sum**:
+  planes z0-2, z0-1 go to the rank below, plane z1 to the rank above, and each
+  rank adds what it receives into the planes it owns;
+* interpolate: a **halo fill** -- the two planes below the slab from the rank
+  below, one plane above from the rank above -- then a local gather.
+
+These two exchanges are the only collective on the path (NCCL send/recv
+between ring neighbours; a ``gloo`` group stages through host memory, which is
+what the CPU tests use).  On a closed (non-periodic) axis the outer ghost
+planes fall off the grid, exactly like the reference's dropped out-of-grid
+targets, and the outer halos are zero.
+
+The local operators are injectable (``local_spread`` / ``local_interpolate``)
+so the decomposition logic can be checked on CPU against the oracle; by
+default they are the device operators of ``device.py``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _capi
+from ._capi import check, load
+from .ib import StaggeredGrid
+
+
+@dataclass
+class SlabLayout:
+    """Where one rank's slab sits in the global grid."""
+
+    rank: int
+    world: int
+    nz: int          # global extent of the last axis
+    z0: int          # first owned plane
+    z1: int          # one past the last owned plane
+    plane: int       # values per plane (prod of the other extents)
+    periodic: bool   # global periodicity of the last axis
+
+    @property
+    def nloc(self) -> int:
+        return self.z1 - self.z0
+
+    @property
+    def local_planes(self) -> int:
+        return self.nloc + 3
+
+    @property
+    def z_first(self) -> int:
+        return self.z0 - 2
+
+
+def slab_bounds(nz: int, world: int) -> list[int]:
+    """Balanced contiguous split of nz planes over `world` ranks."""
+    if world < 1 or nz < 2 * world:
+        raise ValueError(f"cannot split {nz} planes over {world} ranks (need >= 2 each)")
+    return [nz * r // world for r in range(world + 1)]
+
+
+def layout(grid: StaggeredGrid, rank: int, world: int) -> SlabLayout:
+    ext = list(grid.extents)
+    b = slab_bounds(ext[-1], world)
+    plane = 1
+    for e in ext[:-1]:
+        plane *= e
+    return SlabLayout(rank, world, ext[-1], b[rank], b[rank + 1], plane, grid.is_periodic(grid.dim - 1))
+
+
+def local_grid(grid: StaggeredGrid, lay: SlabLayout) -> StaggeredGrid:
+    """The rank's local grid: planes [z0 - 2, z1 + 1), closed along the slab
+    axis, same origin (the slab shift travels in ibc_slab, not in the origin)."""
+    ext = list(grid.extents)
+    ext[-1] = lay.local_planes
+    per = list(grid.periodic)
+    per[-1] = False
+    return StaggeredGrid(ext, grid.spacing(), list(grid.staggerings), per, list(grid.origin))
+
+
+def c_slab(lay: SlabLayout) -> _capi.IbcSlab:
+    s = _capi.IbcSlab()
+    s.z_first = lay.z_first
+    s.nz_global = lay.nz
+    s.periodic_global = int(lay.periodic)
+    return s
+
+
+class SlabDecomposition:
+    """One rank's share of a z-slab decomposed spread / interpolate.
+
+    Arrays are torch tensors (CUDA for the device operators; any device for
+    injected local operators).  ``group`` is a torch.distributed process group
+    (None = default group); with world == 1 the exchanges are local copies.
+    """
+
+    def __init__(self, grid: StaggeredGrid, rank: int, world: int, group=None,
+                 local_spread=None, local_interpolate=None, ops=None):
+        self.grid = grid
+        self.lay = layout(grid, rank, world)
+        self.local = local_grid(grid, self.lay)
+        self.group = group
+        self._ops = ops
+        self._spread = local_spread or self._device_spread
+        self._interp = local_interpolate or self._device_interpolate
+
+    # ---------------------------------------------------------- neighbours
+    @property
+    def down(self) -> int:
+        return (self.lay.rank - 1) % self.lay.world
+
+    @property
+    def up(self) -> int:
+        return (self.lay.rank + 1) % self.lay.world
+
+    def _has_down(self) -> bool:
+        return self.lay.periodic or self.lay.rank > 0
+
+    def _has_up(self) -> bool:
+        return self.lay.periodic or self.lay.rank < self.lay.world - 1
+
+    def _exchange(self, send_down, send_up, recv_from_up_shape, recv_from_down_shape):
+        """send_down -> rank below, send_up -> rank above; returns (from_up, from_down).
+
+        Every rank posts the same four operations in the same order, so the
+        two messages between a pair of ranks (world == 2: down == up) match in
+        order."""
+        import torch
+        import torch.distributed as dist
+
+        lay = self.lay
+        like = send_down if send_down is not None else send_up
+        if lay.world == 1:  # periodic ring of one: the neighbour is this rank
+            return (send_down.clone() if self._has_up() else None,
+                    send_up.clone() if self._has_down() else None)
+        staged = dist.get_backend(self.group) != "nccl" and like.is_cuda
+        dev = like.device
+
+        def wire(t):
+            return t.cpu().contiguous() if staged else t.contiguous()
+
+        ops, from_up, from_down = [], None, None
+        if self._has_down():
+            ops.append(dist.P2POp(dist.isend, wire(send_down), self.down, self.group, tag=1))
+        if self._has_up():
+            ops.append(dist.P2POp(dist.isend, wire(send_up), self.up, self.group, tag=2))
+        if self._has_up():
+            from_up = torch.empty(recv_from_up_shape, dtype=like.dtype,
+                                  device="cpu" if staged else dev)
+            ops.append(dist.P2POp(dist.irecv, from_up, self.up, self.group, tag=1))
+        if self._has_down():
+            from_down = torch.empty(recv_from_down_shape, dtype=like.dtype,
+                                    device="cpu" if staged else dev)
+            ops.append(dist.P2POp(dist.irecv, from_down, self.down, self.group, tag=2))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        if staged:
+            from_up = from_up.to(dev) if from_up is not None else None
+            from_down = from_down.to(dev) if from_down is not None else None
+        return from_up, from_down
+
+    # ------------------------------------------------------------- spread
+    def ghost_sum(self, local_out):
+        """Local spread output (local_planes x plane) -> the owned slab
+        (nloc x plane): ghost planes to their owners, received ghosts added."""
+        lay, P = self.lay, self.lay.plane
+        L = local_out.view(lay.local_planes, P)
+        from_up, from_down = self._exchange(L[0:2], L[lay.nloc + 2:lay.nloc + 3], (2, P), (1, P))
+        own = L[2:lay.nloc + 2]
+        if from_up is not None:    # the rank above's planes z1-2, z1-1
+            own[lay.nloc - 2:lay.nloc] += from_up
+        if from_down is not None:  # the rank below's plane z0
+            own[0:1] += from_down
+        return own.reshape(-1)
+
+    def spread(self, points, values, out=None):
+        """Points homed in this slab -> this rank's owned planes of the field."""
+        return self.ghost_sum(self._spread(points, values))
+
+    # -------------------------------------------------------- interpolate
+    def halo_fill(self, owned):
+        """Owned planes (nloc x plane) -> local field with halos (local_planes x plane)."""
+        import torch
+
+        lay, P = self.lay, self.lay.plane
+        O = owned.view(lay.nloc, P)
+        from_up, from_down = self._exchange(O[0:1], O[lay.nloc - 2:lay.nloc], (1, P), (2, P))
+        L = torch.zeros((lay.local_planes, P), dtype=owned.dtype, device=owned.device)
+        L[2:lay.nloc + 2] = O
+        if from_down is not None:  # planes z0-2, z0-1
+            L[0:2] = from_down
+        if from_up is not None:    # plane z1
+            L[lay.nloc + 2] = from_up[0]
+        return L.reshape(-1)
+
+    def interpolate(self, owned_field, points, out=None):
+        return self._interp(self.halo_fill(owned_field), points)
+
+    # ---------------------------------------------------- device operators
+    def _device_ops(self):
+        if self._ops is None:
+            import torch
+
+            from .device import DeviceOperators
+
+            self._ops = DeviceOperators(torch.cuda.current_device())
+        return self._ops
+
+    def _device_spread(self, points, values):
+        import torch
+
+        from .device import _ptr, _require
+
+        ops = self._device_ops()
+        n = points.shape[0]
+        _require(points, "points", n * self.grid.dim)
+        _require(values, "values", n)
+        out = torch.empty(self.local.point_count(), dtype=torch.float64, device=points.device)
+        ws = ops.workspace(n, self.local)
+        ops._sync_stream()
+        slab = c_slab(self.lay)
+        check(load().ibc_spread_slab_device(ops.context.handle, C.byref(self.local.c_grid),
+                                            C.byref(slab), _capi.IBC_KERNEL_COSINE4,
+                                            _ptr(points), _ptr(values), n, ws.handle, _ptr(out)))
+        return out
+
+    def _device_interpolate(self, field_local, points):
+        import torch
+
+        from .device import _ptr, _require
+
+        ops = self._device_ops()
+        n = points.shape[0]
+        _require(field_local, "field", self.local.point_count())
+        _require(points, "points", n * self.grid.dim)
+        out = torch.empty(n, dtype=torch.float64, device=points.device)
+        ops._sync_stream()
+        slab = c_slab(self.lay)
+        check(load().ibc_interpolate_slab_device(ops.context.handle, C.byref(self.local.c_grid),
+                                                 C.byref(slab), _capi.IBC_KERNEL_COSINE4,
+                                                 _ptr(field_local), _ptr(points), n, _ptr(out)))
+        return out
+
+
+def home_planes(grid: StaggeredGrid, points, ops=None):
+    """Wrapped home cell along the last axis of every point (device): the
+    slab-binning key, bit-identical to the reference's cell_index + wrap."""
+    import torch
+
+    from .device import DeviceOperators, _ptr, _require
+
+    ops = ops or DeviceOperators(torch.cuda.current_device())
+    n = points.shape[0]
+    _require(points, "points", n * grid.dim)
+    out = torch.empty(n, dtype=torch.int32, device=points.device)
+    ops._sync_stream()
+    check(load().ibc_home_planes_device(ops.context.handle, C.byref(grid.c_grid),
+                                        _capi.IBC_KERNEL_COSINE4, _ptr(points), n, _ptr(out)))
+    return out
+
+
+def owner_of_planes(planes, nz: int, world: int):
+    """Rank owning each home plane (torch int tensor in, int64 out)."""
+    import torch
+
+    b = torch.tensor(slab_bounds(nz, world)[1:-1], dtype=planes.dtype, device=planes.device)
+    return torch.bucketize(planes.contiguous(), b, right=True)

@@ -1,0 +1,189 @@
+"""Multi-rank z-slab decomposition (paper_2012_06646_b200/slab.py).
+
+CPU (gloo, world size 2 and 3): the decomposition logic -- slab bounds, point
+binning by home plane, ghost-plane sum after spreading, halo fill before
+interpolating -- with the oracle as each rank's local operator, checked
+against the single-grid oracle (max_rel_deviation <= 1e-12).
+
+GPU (2 ranks on one device, gloo staging through host memory): the same with
+the device slab operators (ibc_spread_slab_device / ibc_interpolate_slab_device,
+global-coordinate cells), checked against the single-grid oracle.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2012_06646_b200 import ib
+from paper_2012_06646_b200 import slab as S
+
+TOL = 1e-12
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASES = {
+    # extents, spacing, staggering, periodic, n points
+    "periodic": ((8, 6, 12), 0.5, (0.5, 0.25, 0.0), (True, True, True), 400),
+    "closed_z": ((7, 6, 12), 0.5, (0.0, 0.5, 0.0), (True, False, False), 300),
+    "planes2d": ((9, 10), 0.5, (0.25, 0.0), (True, True), 200),
+}
+
+
+def _inputs(case):
+    ext, h, alpha, per, n = CASES[case]
+    rng = np.random.default_rng(11)
+    d = len(ext)
+    pts = np.empty((n, d))
+    for a in range(d):
+        pts[:, a] = rng.uniform(0.0, ext[a] * h, n)  # wrapped, dyadic-exact slab shifts
+    vals = rng.uniform(-1, 1, n)
+    field = rng.uniform(-1, 1, int(np.prod(ext)))
+    return ext, h, alpha, per, pts, vals, field
+
+
+def _oracle_local_ops(dec, ext, h, alpha, per):
+    """Each rank's local operator on CPU: the oracle on an ordinary grid equal
+    to the slab's local grid (exact here: h = 0.5 and the shift is dyadic)."""
+    lay = dec.lay
+    lext = list(ext[:-1]) + [lay.local_planes]
+    lper = list(per[:-1]) + [False]
+    origin = [0.0] * len(ext)
+    origin[-1] = (lay.z0 - 2) * h
+    og = O.make_grid(lext, h, alpha, lper, origin)
+
+    g_global = O.make_grid(list(ext), h, list(alpha), list(per))
+
+    def shifted(points):
+        # A point whose (unwrapped) home cell is n on a periodic slab axis is
+        # homed in plane 0: move it down one period, as the device's
+        # global-coordinate slab cells do (ibc_device.cuh cell_of_slab).
+        p = points.numpy().copy()
+        if per[-1]:
+            cu = O.home_cells(g_global, p, wrap=False)[:, -1]
+            p[:, -1] -= (cu // ext[-1]) * ext[-1] * h
+        return p
+
+    def spread(points, values):
+        return torch.from_numpy(O.spread_serial(og, shifted(points), values.numpy()))
+
+    def interp(field, points):
+        return torch.from_numpy(O.interpolate(og, field.numpy(), shifted(points)))
+
+    return spread, interp
+
+
+def _cpu_worker(rank, world, port, case, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ext, h, alpha, per, pts, vals, field = _inputs(case)
+        grid = ib.StaggeredGrid(list(ext), h, list(alpha), list(per))
+        dec = S.SlabDecomposition(grid, rank, world)
+        dec._spread, dec._interp = _oracle_local_ops(dec, ext, h, alpha, per)
+        og = O.make_grid(list(ext), h, list(alpha), list(per))
+        planes = torch.from_numpy(O.home_cells(og, pts)[:, -1])
+        mine = (S.owner_of_planes(planes, ext[-1], world) == rank).numpy()
+        lay, P = dec.lay, dec.lay.plane
+        # spread: owned planes == the single-grid oracle's planes [z0, z1)
+        own = dec.spread(torch.from_numpy(pts[mine]), torch.from_numpy(vals[mine]))
+        want = O.spread_serial(og, pts, vals)[lay.z0 * P:lay.z1 * P]
+        dev = O.max_rel_deviation(own.numpy(), want)
+        assert dev <= TOL, f"rank {rank} spread dev {dev}"
+        # interpolate: owned planes of the field in, my points' values out
+        owned = torch.from_numpy(field[lay.z0 * P:lay.z1 * P].copy())
+        e = dec.interpolate(owned, torch.from_numpy(pts[mine]))
+        want_e = O.interpolate(og, field, pts)[mine]
+        dev = O.max_rel_deviation(e.numpy(), want_e)
+        assert dev <= TOL, f"rank {rank} interp dev {dev}"
+        dist.destroy_process_group()
+    except BaseException as exc:  # pragma: no cover - reported to the parent
+        errq.put(f"rank {rank}: {exc!r}")
+
+
+def _spawn(fn, world, *args):
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=fn, args=(r, world, port, *args, errq)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert not errs, errs
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+
+
+def test_slab_bounds_and_layout():
+    assert S.slab_bounds(12, 2) == [0, 6, 12]
+    assert S.slab_bounds(256, 3) == [0, 85, 170, 256]
+    with pytest.raises(ValueError):
+        S.slab_bounds(5, 3)
+    g = ib.StaggeredGrid([8, 6, 12], 0.5, [0.5, 0.5, 0.0], [True] * 3)
+    lay = S.layout(g, 1, 2)
+    assert (lay.z0, lay.z1, lay.plane, lay.local_planes, lay.z_first) == (6, 12, 48, 9, 4)
+    loc = S.local_grid(g, lay)
+    assert loc.extents == (8, 6, 9) and loc.periodic == (True, True, False)
+    assert loc.origin == g.origin  # the slab shift travels in ibc_slab, not the origin
+    planes = torch.tensor([0, 5, 6, 11, 12], dtype=torch.int32)
+    assert S.owner_of_planes(planes, 12, 2).tolist() == [0, 0, 1, 1, 1]
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_decomposition_matches_single_grid_oracle(case, world):
+    _spawn(_cpu_worker, world, case)
+
+
+def _gpu_worker(rank, world, port, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ext, h, alpha, per, n = (32, 24, 40), 0.5, (0.5, 0.5, 0.0), (True, True, True), 6000
+        rng = np.random.default_rng(5)
+        pts = np.stack([rng.uniform(-2.0, ext[a] * h + 2.0, n) for a in range(3)], axis=1)
+        vals = rng.uniform(-1, 1, n)
+        field = rng.uniform(-1, 1, int(np.prod(ext)))
+        grid = ib.StaggeredGrid(list(ext), h, list(alpha), list(per))
+        og = O.make_grid(list(ext), h, list(alpha), list(per))
+        dec = S.SlabDecomposition(grid, rank, world)
+        X = torch.tensor(pts, device="cuda")
+        planes = S.home_planes(grid, X)
+        assert np.array_equal(planes.cpu().numpy(), O.home_cells(og, pts)[:, -1])
+        mine = (S.owner_of_planes(planes, ext[-1], world) == rank)
+        lay, P = dec.lay, dec.lay.plane
+        own = dec.spread(X[mine].contiguous(), torch.tensor(vals, device="cuda")[mine].contiguous())
+        want = O.spread_serial(og, pts, vals)[lay.z0 * P:lay.z1 * P]
+        dev = O.max_rel_deviation(own.cpu().numpy(), want)
+        assert dev <= TOL, f"rank {rank} spread dev {dev}"
+        owned = torch.tensor(field[lay.z0 * P:lay.z1 * P], device="cuda")
+        e = dec.interpolate(owned, X[mine].contiguous())
+        dev = O.max_rel_deviation(e.cpu().numpy(), O.interpolate(og, field, pts)[mine.cpu().numpy()])
+        assert dev <= TOL, f"rank {rank} interp dev {dev}"
+        torch.cuda.synchronize()
+        dist.destroy_process_group()
+    except BaseException as exc:  # pragma: no cover
+        errq.put(f"rank {rank}: {exc!r}")
+
+
+@pytest.mark.gpu
+def test_device_slab_decomposition_two_ranks_one_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _spawn(_gpu_worker, 2)
