@@ -246,6 +246,7 @@ ibc_status ibc_workspace_create(ibc_context* ctx, size_t n, const ibc_grid* grid
     auto* ws = new ibc_workspace();
     try {
       ws->w.ctx = &ctx->c;
+      ws->w.device = ctx->c.device;
       ws->w.point_count = n;
       ws->w.grid_points = grid_points(grid);
       ws->w.sweep_width = sweep_width;
@@ -263,8 +264,9 @@ ibc_status ibc_workspace_create(ibc_context* ctx, size_t n, const ibc_grid* grid
 ibc_status ibc_workspace_destroy(ibc_workspace* ws) {
   return guarded([&] {
     if (!ws) return;
-    cudaSetDevice(ws->w.ctx->device);
-    cudaStreamSynchronize(ws->w.ctx->stream);
+    // No stream sync through ws->w.ctx: the context may be destroyed first
+    // (e.g. garbage collection at interpreter exit); cudaFree synchronizes.
+    cudaSetDevice(ws->w.device);
     ws->w.s.release_all();
     delete ws;
   });

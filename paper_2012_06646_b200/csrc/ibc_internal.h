@@ -83,6 +83,7 @@ struct Context {
 
 struct Workspace {
   Context* ctx = nullptr;
+  int device = 0;  // destroy must not touch ctx (it may already be gone)
   size_t point_count = 0;
   size_t grid_points = 0;
   int sweep_width = 0;
