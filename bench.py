@@ -13,8 +13,10 @@ scatter_points, seed 1; X* = X^n + U[-0.1h, 0.1h]^3).
 Timing: W untimed warm-up steps; then K steps, each bracketed by CUDA
 events on the operators' stream with a 256 MiB L2 flush between steps
 (outside the events); barrier + synchronize on both sides; max over ranks.
-Under torchrun (N > 1) every rank runs its own config-2 replica (weak
-scaling; each rank's slab of a 256 x 256 x 256N grid holds the same load).
+Under torchrun (N > 1) the grid is 256 x 256 x 256N, split in z-slabs, one
+per GPU, each holding 2^20 points (weak scaling, the same load per GPU as
+config 2); every step runs the slab spread with its NCCL ghost-plane sum and
+the halo fill + slab interpolation (paper_2012_06646_b200/slab.py).
 
 --impl reference times the reference's own OpenMP CPU path (ib::spread_fused
 + ib::interpolate compiled from the reference headers into oracle/_ref) on
@@ -185,28 +187,47 @@ def run_ours(args):
 
     from paper_2012_06646_b200 import ib, synth
     from paper_2012_06646_b200.device import DeviceOperators
+    from paper_2012_06646_b200.slab import SlabDecomposition
 
     world, rank, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())  # >1 rank per GPU only in dev runs
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("IBC_BENCH_BACKEND", "nccl")  # gloo: dev runs on one GPU
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    data = synth.config2(seed_offset=0)
-    n, N, h = data["n"], data["N"], data["h"]
-    grid = ib.StaggeredGrid([N] * 3, h, [0.5, 0.5, 0.0], [True] * 3)
+    # N = 1: BASELINE config 2 on one grid.  N > 1: the same load per GPU as
+    # z-slabs of a 256 x 256 x 256N periodic grid (weak scaling), with the
+    # ghost-plane sum and halo fill over NCCL between ring neighbours.
+    if world == 1:
+        data = synth.config2(seed_offset=0)
+        n, N, h = data["n"], data["N"], data["h"]
+        grid = ib.StaggeredGrid([N] * 3, h, [0.5, 0.5, 0.0], [True] * 3)
+        ops = DeviceOperators(local)
+        dec = None
+    else:
+        data = synth.slab_config(rank, world)
+        n, N, h = data["n"], data["N"], data["h"]
+        grid = ib.StaggeredGrid([N, N, data["nz_global"]], h, [0.5, 0.5, 0.0], [True] * 3)
+        ops = DeviceOperators(local)
+        dec = SlabDecomposition(grid, rank, world, ops=ops)
     xs = torch.tensor(data["x_star"], device=dev)
     xn = torch.tensor(data["x_n"], device=dev)
     gv = torch.tensor(data["values"], device=dev)
     fe = torch.tensor(data["field"], device=dev)
     ell = torch.empty(N ** 3, dtype=torch.float64, device=dev)
     E = torch.empty(n, dtype=torch.float64, device=dev)
-    ops = DeviceOperators(local)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
     def step():
-        ops.spread(xs, gv, grid, out=ell)
-        ops.interpolate(fe, xn, grid, out=E)
+        if dec is None:
+            ops.spread(xs, gv, grid, out=ell)
+            ops.interpolate(fe, xn, grid, out=E)
+        else:
+            dec.spread(xs, gv)
+            dec.interpolate(fe, xn)
 
     for i in range(args.warmup):
         step()
@@ -235,7 +256,7 @@ def run_ours(args):
     ms_per_step = total_ms / K
     value = world * n * K / (total_ms * 1e-3)
 
-    # Per-kernel device times (CUDA events on the operators' stream), separate pass.
+    # Per-kernel-class device times (CUDA events on the operators' stream), separate pass.
     P = max(3, min(K, 10))
     ops.context.set_profiling(True)
     ops.context.reset_profile()
@@ -245,7 +266,7 @@ def run_ours(args):
     prof = ops.context.profile()
     ops.context.set_profiling(False)
     per_launch = {k[:-3]: prof[k] / P * 1e3 for k in prof if k.endswith("_ms")}  # us per step
-    n_omega = N ** 3
+    n_omega = N ** 3  # grid points each rank owns
     alg = {"spread": 32 * n + 8 * n_omega, "interp": 32 * n + 8 * n_omega}
     dom = max(("spread", "interp"), key=lambda k: per_launch.get(k, 0.0))
     peak, peak_src = peaks()
@@ -259,25 +280,55 @@ def run_ours(args):
             traffic = None
     step_bytes = 64 * n + 16 * n_omega
 
-    # End to end through the reference-facing host API (pinned host buffers).
+    # End to end through the public API: pinned host buffers in, results out.
     e2e = None
     if args.e2e_steps > 0:
-        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         hx_s, hx_n, hg, hf = pin(data["x_star"]), pin(data["x_n"]), pin(data["values"]), pin(data["field"])
-        ctx = ib.default_context(local)
-        ws = ib.SpreadWorkspace(n, grid, context=ctx)
-        kern = ib.CosineKernel()
-        ib.spread_fused(hx_s, hg, grid, kern, ws)
-        ib.interpolate(ib.GridField(grid, hf), hx_n, kern)
-        field = ib.GridField(grid, hf)
+        h_ell = torch.empty(n_omega, dtype=torch.float64).pin_memory()
+        h_E = torch.empty(n, dtype=torch.float64).pin_memory()
+        if dec is None:
+            # The reference-facing C ABI with host buffers (ibc_spread /
+            # ibc_interpolate: copies in, operator, copy out, synchronous) --
+            # the call ib::spread_fused / ib::interpolate make through
+            # include/ib_b200/ib.hpp -- on pinned host memory.
+            import ctypes as C
+
+            from paper_2012_06646_b200 import _capi
+
+            lib = _capi.load()
+            ctx = ib.default_context(local)
+            ws = ib.SpreadWorkspace(n, grid, context=ctx)
+            vp = lambda t: C.c_void_p(t.data_ptr())
+
+            def e2e_step():
+                _capi.check(lib.ibc_spread(ctx.handle, C.byref(grid.c_grid), _capi.IBC_KERNEL_COSINE4,
+                                           _capi.IBC_SPREAD_FUSED, vp(hx_s), vp(hg), n, n, 0,
+                                           ws.handle, 0, vp(h_ell)))
+                _capi.check(lib.ibc_interpolate(ctx.handle, C.byref(grid.c_grid),
+                                                _capi.IBC_KERNEL_COSINE4, vp(hf), vp(hx_n), n, 0,
+                                                vp(h_E)))
+            note = ("ibc_spread(FUSED) + ibc_interpolate through the C ABI with pinned host "
+                    "buffers (H2D + operator + D2H per call), wall clock, median")
+        else:
+            def e2e_step():
+                d_xs, d_g = hx_s.to(dev, non_blocking=True), hg.to(dev, non_blocking=True)
+                d_xn, d_f = hx_n.to(dev, non_blocking=True), hf.to(dev, non_blocking=True)
+                h_ell.copy_(dec.spread(d_xs, d_g), non_blocking=True)
+                h_E.copy_(dec.interpolate(d_f, d_xn), non_blocking=True)
+                torch.cuda.synchronize()
+            note = "SlabDecomposition.spread + .interpolate with H2D inputs / D2H outputs (pinned), wall clock, median, max over ranks"
+        e2e_step()
+        torch.cuda.synchronize()
         ts = []
         for i in range(args.e2e_steps):
+            if world > 1:
+                dist.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            ib.spread_fused(hx_s, hg, grid, kern, ws)
-            ib.interpolate(field, hx_n, kern)
+            e2e_step()
+            torch.cuda.synchronize()
             ts.append(time.perf_counter() - t0)
-        tmax = max(ts) if world == 1 else ts
         e2e_s = statistics.median(ts)
         if world > 1:
             t = torch.tensor([e2e_s], device=dev)
@@ -285,8 +336,7 @@ def run_ours(args):
             e2e_s = float(t.item())
         e2e = {"value": world * n / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(hx_s.nbytes + hg.nbytes + hx_n.nbytes + hf.nbytes),
-               "d2h_bytes_per_step": int(n_omega * 8 + n * 8),
-               "note": "ibc_spread + ibc_interpolate (host buffers, pinned), wall clock, median"}
+               "d2h_bytes_per_step": int(n_omega * 8 + n * 8), "note": note}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -305,12 +355,18 @@ def run_ours(args):
                    "sample": f"failed: {exc}"}
 
     if rank == 0:
+        workload = WORKLOAD if world == 1 else (
+            f"config 2 per GPU, weak scaling: {world} z-slabs of a 256 x 256 x {256 * world} "
+            f"periodic grid, 2^20 points homed in each slab; per step one scalar spread (local + "
+            f"NCCL ghost-plane sum) and one scalar interpolation (NCCL halo fill + local gather), FP64")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "n_points": n, "grid": [N, N, N],
-                       "parallelism": "replicas" if world > 1 else "single GPU",
+            "config": {"workload": workload, "n_points_per_gpu": n,
+                       "grid": [N, N, N * world],
+                       "parallelism": f"z-slab x{world} (NCCL ghost/halo exchange)" if world > 1
+                       else "single GPU",
                        "l2": "flushed between steps (256 MiB write outside the events)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
@@ -325,6 +381,7 @@ def run_ours(args):
         }
         print(json.dumps(line))
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
 
 

@@ -138,3 +138,25 @@ def config2(seed_offset: int = 0):
     g = uniform_pm1(n, 2 + seed_offset)
     e = uniform_pm1(N ** 3, 4 + seed_offset)
     return dict(n=n, N=N, edge=edge, h=h, x_n=xn, x_star=xs, values=g, field=e)
+
+
+def slab_config(rank: int, world: int):
+    """Weak-scaling multi-GPU workload (BASELINE config 2 per GPU): a global
+    256 x 256 x 256*world periodic grid split in z-slabs of 256 planes; rank r
+    holds 2^20 points homed in its slab (uniform in x, y and in its planes,
+    kept 0.15 h inside the slab so X* = X^n + U[-0.1h, 0.1h] stays homed)."""
+    n, N, edge = 1 << 20, 256, 16e-4
+    h = edge / N
+    z0, z1 = N * rank, N * (rank + 1)
+    u = MT19937_64(1 + 1000 * rank).next_unit(3 * n).reshape(n, 3)
+    xn = np.empty((n, 3))
+    xn[:, 0] = u[:, 0] * edge
+    xn[:, 1] = u[:, 1] * edge
+    # home plane of z (alpha_z = 0) is ceil(z / h): planes [z0, z1) <-> z in ((z0-1)h, (z1-1)h]
+    lo, hi = (z0 - 1 + 0.15) * h, (z1 - 1 - 0.15) * h
+    xn[:, 2] = lo + u[:, 2] * (hi - lo)
+    xs = perturb(xn, 0.1 * h, 3 + 1000 * rank)
+    g = uniform_pm1(n, 2 + 1000 * rank)
+    e = uniform_pm1(N * N * N, 4 + 1000 * rank)  # this rank's owned planes
+    return dict(n=n, N=N, nz_global=N * world, edge=edge, h=h, x_n=xn, x_star=xs, values=g,
+                field=e, z0=z0, z1=z1)
