@@ -821,9 +821,7 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
 bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
   if (g.dim < 2) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  const int xi = nx + sp::kPadL + sp::kPadR;
-  int rl = xi + (xi >> 4) + 1;
-  rl += rl & 1;
+  const int rl = sp::row_len(nx);
   const int slots = g.dim == 3 ? 4 : 1;
   const size_t per_warp = (size_t)slots * rl * sizeof(double);
   if (per_warp > 200 * 1024) return false;
@@ -871,22 +869,33 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   if (!attr_set[ctx.device & 63]) {
     IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(sp::spread_sweep_kernel<2>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    IBC_CUDA(cudaFuncSetAttribute(sp::spread_sweep_kernel<3>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (const void* k : {(const void*)sp::spread_sweep_kernel<2, 0>,
+                          (const void*)sp::spread_sweep_kernel<3, 0>,
+                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64)>,
+                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128)>,
+                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256)>,
+                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512)>})
+      IBC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[ctx.device & 63] = true;
   }
   if (sweep) {
     ctx.prof_begin(kProfSpread, &ev);
     const size_t smem = (size_t)W.wpc * (g.dim == 3 ? 4 : 1) * W.rl * sizeof(double);
     const unsigned blocks = (unsigned)(W.nyg * W.nzc);
-    if (g.dim == 3)
-      sp::spread_sweep_kernel<3><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, smap,
-                                                                   s.rec.p, s.rec_cx.p, d_out);
-    else
-      sp::spread_sweep_kernel<2><<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, smap,
-                                                                   s.rec.p, s.rec_cx.p, d_out);
+    // Compile-time window row length for the common x extents.
+    auto launch = [&](auto kern) {
+      kern<<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, smap, s.rec.p, s.rec_cx.p, d_out);
+    };
+    const int nx = g.n[0];
+    if (g.dim == 3) {
+      if (W.rl == sp::row_len(64) && nx == 64) launch(sp::spread_sweep_kernel<3, sp::row_len(64)>);
+      else if (W.rl == sp::row_len(128) && nx == 128) launch(sp::spread_sweep_kernel<3, sp::row_len(128)>);
+      else if (W.rl == sp::row_len(256) && nx == 256) launch(sp::spread_sweep_kernel<3, sp::row_len(256)>);
+      else if (W.rl == sp::row_len(512) && nx == 512) launch(sp::spread_sweep_kernel<3, sp::row_len(512)>);
+      else launch(sp::spread_sweep_kernel<3, 0>);
+    } else {
+      launch(sp::spread_sweep_kernel<2, 0>);
+    }
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   } else {

@@ -47,6 +47,12 @@ struct SweepTiling {
 
 __device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
 
+// Doubles per window row for nx: padded, skewed, even.
+__host__ __device__ constexpr int row_len(int nx) {
+  return ((nx + kPadL + kPadR) + ((nx + kPadL + kPadR) >> 4) + 1) +
+         (((nx + kPadL + kPadR) + ((nx + kPadL + kPadR) >> 4) + 1) & 1);
+}
+
 // Position of the n-th (0-based) set bit of m (popc(m) > n).
 __device__ __forceinline__ int nth_set(uint32_t m, int n) {
   int pos = 0;
@@ -62,7 +68,81 @@ __device__ __forceinline__ int nth_set(uint32_t m, int n) {
   return pos;
 }
 
-template <int D>
+// The batches of one source plane (see the file comment).  R >= 0: target
+// plane s + kz - 2 sits in slot (R + kz + 2) & 3 of a compile-time row length
+// RL and is inside the z-chunk; R < 0: runtime slot offsets so[kz] (-1 = skip).
+template <int D, int RL, int R>
+__device__ __forceinline__ void plane_batches(double* __restrict__ W, const int so[4], uint32_t e0,
+                                              uint32_t e1, uint32_t e2, uint32_t total,
+                                              uint32_t rstart, const uint32_t* __restrict__ smap,
+                                              const double* __restrict__ rec,
+                                              const int* __restrict__ rcx, double q) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  uint32_t next = 0;   // next unread position in the concatenated rows
+  int ndef = 0;        // deferred lanes carried into this batch
+  uint32_t p_def = 0;  // this lane's deferred position (lanes < ndef)
+  while (next < total || ndef > 0) {
+    const uint32_t p = lane < ndef ? p_def : next + (uint32_t)(lane - ndef);
+    const bool valid = lane < ndef || p < total;
+    const int j = (p >= e0) + (p >= e1) + (p >= e2);
+    const uint32_t rs = __shfl_sync(0xffffffffu, rstart, j & 3) + p;
+    int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
+    double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
+    if (valid) {
+      const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
+      const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
+      g01 = __ldg(r2);
+      g23 = __ldg(r2 + 1);
+      tr = __ldg(r2 + 2);
+      tz2 = __ldg(r2 + 3);
+      cx = __ldg(rcx + r);
+    }
+    const uint32_t peers = __match_any_sync(0xffffffffu, cx);  // every lane takes part
+    const bool on = valid && (peers & lt) == 0u;
+    // Compact the deferred lanes (same cx as an earlier lane) to the front.
+    const uint32_t defm = __ballot_sync(0xffffffffu, valid && !on);
+    const int newdef = __popc(defm);
+    if (newdef) {
+      const uint32_t pd = __shfl_sync(0xffffffffu, p, lane < newdef ? nth_set(defm, lane) : 0);
+      if (lane < newdef) p_def = pd;
+    }
+    next = min(total, next + (uint32_t)(32 - ndef));
+    ndef = newdef;
+    // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
+    const double vy = (j & 1) ? tr.x : tr.y;
+    const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
+    double a[4];
+    if (D == 3) {
+      a[0] = fma(-wq, tz2.y, wq);
+      a[1] = fma(wq, tz2.x, wq);
+      a[2] = fma(wq, tz2.y, wq);
+      a[3] = fma(-wq, tz2.x, wq);
+    } else {
+      a[0] = a[1] = a[3] = 0.0;
+      a[2] = wq / q;
+    }
+    const double gk[4] = {g01.x, g01.y, g23.x, g23.y};
+    const int xb = cx + (kPadL - 2);
+#pragma unroll
+    for (int kx = 0; kx < 4; ++kx) {
+      if (on) {
+        double* wa = W + skew(xb + kx);
+        if (R >= 0) {
+#pragma unroll
+          for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * RL] += gk[kx] * a[kz];
+        } else {
+#pragma unroll
+          for (int kz = 0; kz < 4; ++kz)
+            if (so[kz] >= 0) wa[so[kz]] += gk[kx] * a[kz];
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+template <int D, int RL>
 __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTiling T,
                                                            const uint32_t* __restrict__ rowstart,
                                                            const uint32_t* __restrict__ smap,
@@ -71,6 +151,7 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
   constexpr int kSlots = D == 3 ? 4 : 1;
+  const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nx = g.n[0], ny = g.n[1], nz = D == 3 ? g.n[2] : 1;
   const int yg = blockIdx.x % T.nyg, zi = blockIdx.x / T.nyg;
@@ -78,8 +159,8 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
   if (ty >= ny) return;  // warp-uniform; the kernel has no CTA barriers
   const int z0 = D == 3 ? zi * T.zc : 0;
   const int z1 = D == 3 ? min(z0 + T.zc, nz) : 1;
-  double* W = win + (size_t)warp * kSlots * T.rl;
-  for (int i = lane; i < kSlots * T.rl; i += 32) W[i] = 0.0;
+  double* W = win + (size_t)warp * kSlots * rl;
+  for (int i = lane; i < kSlots * rl; i += 32) W[i] = 0.0;
   __syncwarp();
 
   const bool px = g.periodic[0] != 0, py = g.periodic[1] != 0;
@@ -119,7 +200,7 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
 #pragma unroll
       for (int kz = 0; kz < 4; ++kz) {
         const int tz = s + kz - 2;
-        so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * T.rl : -1) : (kz == 2 ? 0 : -1);
+        so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * rl : -1) : (kz == 2 ? 0 : -1);
       }
       uint32_t incl = len;
 #pragma unroll
@@ -130,65 +211,24 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
       const uint32_t e0 = __shfl_sync(0xffffffffu, incl, 0), e1 = __shfl_sync(0xffffffffu, incl, 1);
       const uint32_t e2 = __shfl_sync(0xffffffffu, incl, 2), total = __shfl_sync(0xffffffffu, incl, 3);
       const uint32_t rstart = rb - (incl - len);  // sorted index = rstart_j + p
-      uint32_t next = 0;   // next unread position in the concatenated rows
-      int ndef = 0;        // deferred lanes carried into this batch
-      uint32_t p_def = 0;  // this lane's deferred position (lanes < ndef)
-      while (next < total || ndef > 0) {
-        const uint32_t p = lane < ndef ? p_def : next + (uint32_t)(lane - ndef);
-        const bool valid = lane < ndef || p < total;
-        const int j = (p >= e0) + (p >= e1) + (p >= e2);
-        const uint32_t rs = __shfl_sync(0xffffffffu, rstart, j & 3) + p;
-        int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
-        double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
-        if (valid) {
-          const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
-          const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
-          g01 = __ldg(r2);
-          g23 = __ldg(r2 + 1);
-          tr = __ldg(r2 + 2);
-          tz2 = __ldg(r2 + 3);
-          cx = __ldg(rcx + r);
+      // Interior planes with a compile-time row length take the static path:
+      // slot offsets are immediates, no per-add range checks.
+      const bool interior = D == 3 && s - 2 >= z0 && s + 1 < z1;
+      if (RL > 0 && interior) {
+        switch (s & 3) {
+          case 0: plane_batches<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          case 1: plane_batches<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          case 2: plane_batches<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          default: plane_batches<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
         }
-        const uint32_t peers = __match_any_sync(0xffffffffu, cx);  // every lane takes part
-        const bool on = valid && (peers & lt) == 0u;
-        // Compact the deferred lanes (same cx as an earlier lane) to the front.
-        const uint32_t defm = __ballot_sync(0xffffffffu, valid && !on);
-        const int newdef = __popc(defm);
-        const uint32_t pd = __shfl_sync(0xffffffffu, p, lane < newdef ? nth_set(defm, lane) : 0);
-        if (lane < newdef) p_def = pd;
-        next = min(total, next + (uint32_t)(32 - ndef));
-        ndef = newdef;
-        // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
-        const double vy = (j & 1) ? tr.x : tr.y;
-        const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
-        double a[4];
-        if (D == 3) {
-          a[0] = fma(-wq, tz2.y, wq);
-          a[1] = fma(wq, tz2.x, wq);
-          a[2] = fma(wq, tz2.y, wq);
-          a[3] = fma(-wq, tz2.x, wq);
-        } else {
-          a[0] = a[1] = a[3] = 0.0;
-          a[2] = wq / q;
-        }
-        const double gk[4] = {g01.x, g01.y, g23.x, g23.y};
-        const int xb = cx + (kPadL - 2);
-#pragma unroll
-        for (int kx = 0; kx < 4; ++kx) {
-          if (on) {
-            const int addr = skew(xb + kx);
-#pragma unroll
-            for (int kz = 0; kz < 4; ++kz)
-              if (so[kz] >= 0) W[so[kz] + addr] += gk[kx] * a[kz];
-          }
-          __syncwarp();
-        }
+      } else {
+        plane_batches<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q);
       }
     }
     // Target plane s - 2 has all its sources: fold, store once, clear.
     const int t = D == 3 ? s - 2 : 0;
     if (t >= z0 && t < z1) {
-      double* Wr = W + (D == 3 ? (t & 3) * T.rl : 0);
+      double* Wr = W + (D == 3 ? (t & 3) * rl : 0);
       double* orow = out + ((size_t)t * ny + ty) * nx;
       if (px && nx < 8) {
         for (int x = lane; x < nx; x += 32) {
@@ -209,7 +249,7 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
       }
       __syncwarp();
       double2* Z = reinterpret_cast<double2*>(Wr);
-      for (int i = lane; i < T.rl / 2; i += 32) Z[i] = make_double2(0.0, 0.0);
+      for (int i = lane; i < rl / 2; i += 32) Z[i] = make_double2(0.0, 0.0);
       __syncwarp();
     }
   }
