@@ -14,12 +14,11 @@
 // sums many points into each grid value, and the reference exposes the stable
 // key order (ws.keys / ws.perm, spread.hpp:33-34), so a fourth kernel puts
 // every row into stable (key, index) order -- which makes the result exactly
-// the reference's stable key-value sort -- and a fifth writes the weight
-// records in that order:
+// the reference's stable key-value sort -- and writes the weight records the
+// spread sweep streams in that order:
 //   K4 rows of <= 32 points: one warp, rank by 32 shuffled compares;
 //      longer rows (listed by K2): one CTA, bitonic sort in shared memory;
-//   K5 per sorted position: cell + one sin/cos pair per axis -> the 64-byte
-//      record the spread sweep streams (coalesced writes).
+//      per sorted position: cell + one sin/cos pair per axis -> 64-byte record.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -184,19 +183,13 @@ __global__ void __launch_bounds__(kThreads) scatter_pairs_kernel(
   bidx[slot] = i;
 }
 
-// K5, spread: the 64-byte weight record of every sorted position, written in
-// sorted order (coalesced):
+// The spread's 64-byte weight record of point i at sorted position o:
 //   {G phi_x(k-2-t_x)/h (k = 0..3), sin/cos(pi u_y/2), sin/cos(pi u_z/2)},
-// and the home cell along x (wrapped on periodic x).
+// and its home cell along x (wrapped on periodic x).
 template <int D>
-__global__ void __launch_bounds__(kThreads) records_kernel(DevGrid g, const double* __restrict__ X,
-                                                           const double* __restrict__ G,
-                                                           const uint32_t* __restrict__ perm,
-                                                           uint32_t n, double* __restrict__ rec,
-                                                           int* __restrict__ rcx) {
-  const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
-  if (o >= n) return;
-  const uint32_t i = __ldg(perm + o);
+__device__ __forceinline__ void write_record(const DevGrid& g, const double* __restrict__ X,
+                                             const double* __restrict__ G, uint32_t i, uint32_t o,
+                                             double* __restrict__ rec, int* __restrict__ rcx) {
   double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};  // u = 0 on padded axes
   int cx = 0;
 #pragma unroll
@@ -214,11 +207,14 @@ __global__ void __launch_bounds__(kThreads) records_kernel(DevGrid g, const doub
   rcx[o] = cx;
 }
 
-// K4, short rows: one warp per row puts (key, index) in stable order.
-// sorted position -> (key, index, bucket slot of its record).
+// K4, short rows: one warp per row puts (key, index) in stable order and
+// writes each point's weight record at its sorted position.
+template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     const uint32_t* __restrict__ start, uint32_t nrows, const uint32_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx) {
+    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
+    DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
+    double* __restrict__ rec, int* __restrict__ rcx) {
   const int lane = threadIdx.x & 31;
   const uint32_t warps = gridDim.x * (kThreads / 32);
   for (uint32_t r = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
@@ -235,6 +231,7 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     if (valid) {
       skey[a + rk] = k;
       sidx[a + rk] = ix;
+      write_record<D>(g, X, G, ix, a + rk, rec, rcx);
     }
   }
 }
@@ -242,10 +239,13 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
 // K4b, long rows: one CTA per listed row, bitonic sort of (key << 32 | index)
 // in shared memory (rows up to kLongSortMax; longer rows rank by counting).
 constexpr int kLongThreads = 1024;
+template <int D>
 __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     const uint32_t* __restrict__ start, const uint32_t* __restrict__ long_rows,
     const uint32_t* __restrict__ nlong, const uint32_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx) {
+    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
+    DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
+    double* __restrict__ rec, int* __restrict__ rcx) {
   extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
   const uint32_t count = *nlong;
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
@@ -277,6 +277,7 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
         skey[a + e] = (uint32_t)(sk[e] >> 32);
         sidx[a + e] = (uint32_t)sk[e];
+        write_record<D>(g, X, G, (uint32_t)sk[e], a + e, rec, rcx);
       }
       __syncthreads();
     } else {
@@ -288,6 +289,7 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
           rk += (((unsigned long long)bkey[a + f] << 32) | bidx[a + f]) < ce ? 1u : 0u;
         skey[a + rk] = (uint32_t)(ce >> 32);
         sidx[a + rk] = (uint32_t)ce;
+        write_record<D>(g, X, G, (uint32_t)ce, a + rk, rec, rcx);
       }
     }
   }

@@ -1049,24 +1049,26 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
     bucket::scatter_pairs_kernel<<<blocks, bucket::kThreads, 0, st>>>(
         s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.keys[1].p, s.vals[1].p);
     const unsigned rblocks = std::min<unsigned>(grid_for(nrows, bucket::kThreads / 32), 148u * 16u);
-    bucket::row_sort_kernel<<<rblocks, bucket::kThreads, 0, st>>>(
-        s.rowstart.p, nrows, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p);
     static bool attr_set[64] = {};
     const size_t lsm = (size_t)bucket::kLongSortMax * 8;
     if (!attr_set[ctx.device & 63]) {
-      IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel,
+      IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<2>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+      IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<3>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
       attr_set[ctx.device & 63] = true;
     }
-    bucket::long_row_sort_kernel<<<148, bucket::kLongThreads, lsm, st>>>(
-        s.rowstart.p, long_rows, nlong, s.keys[1].p, s.vals[1].p, s.keys[0].p, s.vals[0].p);
-    if (g.dim == 3)
-      bucket::records_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
-          g, d_points, d_values, s.vals[0].p, (uint32_t)n, s.rec.p, s.rec_cx.p);
-    else
-      bucket::records_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
-          g, d_points, d_values, s.vals[0].p, (uint32_t)n, s.rec.p, s.rec_cx.p);
-    ctx.launches += 4;
+    auto sorts = [&](auto short_k, auto long_k) {
+      short_k<<<rblocks, bucket::kThreads, 0, st>>>(s.rowstart.p, nrows, s.keys[1].p, s.vals[1].p,
+                                                    s.keys[0].p, s.vals[0].p, g, d_points,
+                                                    d_values, s.rec.p, s.rec_cx.p);
+      long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.keys[1].p,
+                                                     s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
+                                                     d_points, d_values, s.rec.p, s.rec_cx.p);
+    };
+    if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
+    else sorts(bucket::row_sort_kernel<2>, bucket::long_row_sort_kernel<2>);
+    ctx.launches += 3;
     s.sorted_keys = s.keys[0].p;
     s.sorted_perm = s.vals[0].p;
     s.last_n = n;
