@@ -11,7 +11,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "_lib" / "libibcuda.so"
 SOURCES = ["ibc_kernels.cu", "ibc_api.cu"]
-HEADERS = ["ibc_device.cuh", "ibc_sort.cuh", "ibc_internal.h", "ibc_zsweep.cuh", "ibc_sweep.cuh", "ibc_tma.cuh", "ibc_bucket.cuh", "ibc_spread.cuh"]
+HEADERS = ["ibc_device.cuh", "ibc_sort.cuh", "ibc_internal.h", "ibc_sweep.cuh", "ibc_tma.cuh", "ibc_bucket.cuh", "ibc_spread.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -465,11 +465,6 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
   });
 }
 
-// Debug hook (not part of ibcuda.h): clock64 timeline of one z-sweep CTA.
-int ibc_debug_zsweep_trace(int block, long long* out) {
-  return (int)ibc::debug_zsweep_trace(block, out);
-}
-
 static void check_slab(const ibc_grid* grid, const ibc_slab* slab) {
   if (!slab) invalid("slab is null");
   if (grid->dim < 2) invalid("slab decomposition needs a 2- or 3-dimensional grid");

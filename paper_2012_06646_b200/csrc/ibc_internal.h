@@ -102,7 +102,5 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field,
 // ws.run_keys on the device; returns q (synchronizes).
 size_t compute_run_keys(Context& ctx, PointScratch& s);
 size_t read_run_count(Context& ctx, PointScratch& s);
-// Debug: set the traced CTA (block >= 0) or read the last trace into out[2*64*8].
-int debug_zsweep_trace(int block, long long* out);
 
 }  // namespace ibc

@@ -1,15 +1,21 @@
-// ibc_kernels.cu -- the spread / interpolate hot path for sm_100a.
+// ibc_kernels.cu -- pipelines of the spread / interpolate hot path (sm_100a).
 //
 // Per operator call:
-//   K1 keys_hist_kernel   wrap -> cell -> 32-bit key per point + the digit
-//                          histograms of every radix pass        (grid.hpp:121-207)
-//   K2 digit_scan + onesweep_pass x P  stable key/index sort     (sort.hpp:17-71)
-//   K3 rowstart_kernel    extended-row start table + run count q (reduce.hpp:36-69)
-//   K4 prep_records_kernel + spread_tiles_kernel  write-once spread
-//                                                                 (spread.hpp:165-216)
-//   K5 interp_kernel      interpolation gather                   (interpolate.hpp:22-58)
-// 3-D grids take the z-sweep kernels of ibc_zsweep.cuh for K4/K5; the
-// kernels here are the general path (1-D/2-D grids, very long x rows).
+//   spread, 2-D/3-D grids:  row bucket sort + in-row stable sort + weight
+//     records (ibc_bucket.cuh) -> write-once sweep (ibc_spread.cuh)
+//   interpolation, 3-D grids with nx % 16 == 0: row bucketing
+//     (ibc_bucket.cuh) -> TMA-fed gather (ibc_sweep.cuh)
+//   general path (1-D grids, rows too long for a shared-memory window, other
+//   x extents, IBC_SORT=radix):
+//     keys_hist_kernel     wrap -> cell -> 32-bit key + pass-0 digit counts
+//                                                          (grid.hpp:121-207)
+//     tile_offsets_kernel + onesweep_pass x P  stable key/index radix sort
+//                                                          (sort.hpp:17-71)
+//     rowstart_kernel      extended-row start table        (reduce.hpp:36-69)
+//     prep_records_kernel + spread_tiles_kernel  write-once spread
+//                                                          (spread.hpp:165-216)
+//     interp_kernel        interpolation gather            (interpolate.hpp:22-58)
+//   run keys / q on demand: head_count / block_scan / head_write.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,7 +26,6 @@
 
 #include "ibc_internal.h"
 #include "ibc_sort.cuh"
-#include "ibc_zsweep.cuh"
 #include "ibc_sweep.cuh"
 #include "ibc_bucket.cuh"
 #include "ibc_spread.cuh"
@@ -120,27 +125,15 @@ __global__ void __launch_bounds__(kKeysThreads) keys_hist_kernel(
 // rowstart[r] = first sorted index whose extended row id is >= r, r in [0, nrows].
 __global__ void __launch_bounds__(kBlock) rowstart_kernel(const uint32_t* __restrict__ sk, uint32_t n,
                                                           uint32_t rowdiv, uint32_t nrows,
-                                                          uint32_t* __restrict__ rowstart,
-                                                          uint32_t* __restrict__ q_out) {
+                                                          uint32_t* __restrict__ rowstart) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  bool head = false;
   if (i < n) {
-    const uint32_t k = sk[i];
-    const uint32_t row = k / rowdiv;
-    if (i == 0) {
-      for (uint32_t r = 0; r <= row; ++r) rowstart[r] = 0u;
-      head = true;
-    } else {
-      const uint32_t pk = sk[i - 1];
-      const uint32_t prow = pk / rowdiv;
-      for (uint32_t r = prow + 1; r <= row; ++r) rowstart[r] = i;
-      head = pk != k;
-    }
+    const uint32_t row = sk[i] / rowdiv;
+    const uint32_t prow = i == 0 ? 0u : sk[i - 1] / rowdiv;
+    for (uint32_t r = i == 0 ? 0u : prow + 1; r <= row; ++r) rowstart[r] = i;
     if (i == n - 1)
       for (uint32_t r = row + 1; r <= nrows; ++r) rowstart[r] = n;
   }
-  (void)head;
-  (void)q_out;  // the run count q is computed lazily (compute_run_keys)
 }
 
 // ---------------------------------------------------------------- K4a
@@ -282,158 +275,6 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
     const int ty = y0 + tr % T.ty, tz = z0 + tr / T.ty, x = x0 + xx;
     if (ty < g.n[1] && tz < g.n[2] && x < g.n[0]) out[tz * sz_ + ty * sy_ + x] = s_acc[i];
   }
-}
-
-// ---------------------------------------------------------------- K4c
-// Barrier-free write-once spread over whole x rows (3-D and 2-D grids).
-// Warp w of a CTA owns ONE target row (ty, tz), kept in a private, padded
-// shared-memory row (x index + 4; periodic x wraps through the pad, folded
-// back at the end).  It pulls, in fixed (sigma_z, sigma_y) order, the sorted
-// points of the 16 source rows that reach it -- rows are contiguous ranges
-// of the key sort -- with each point's delta weights precomputed once
-// (prep_records_kernel).  Lanes in one batch come from one source row, so
-// distinct cells hit distinct targets; equal cells are adjacent lanes and
-// are serialized by rank.  No atomics, no CTA barriers, fixed summation
-// order: bitwise reproducible.  Every grid value is written once.
-struct RowTiling {
-  int ty, tz, nty, ntz, nxp, warps;
-};
-constexpr int kRowPad = 4;
-
-constexpr int kRowsPerWarp = 4;
-
-// Skewed row layout: padded x index xi lives at xi + (xi >> 4).  Points of a
-// sparse row sit ~16 cells apart; without the skew all lanes of a warp would
-// hit the same shared-memory bank pair.
-__device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
-inline int skewed_len(int nxp) { return nxp + (nxp >> 4) + 2; }
-
-__global__ void __launch_bounds__(256) spread_rows_kernel(
-    DevGrid g, RowTiling T, const uint32_t* __restrict__ rowstart,
-    const int* __restrict__ rec_cx, const double* __restrict__ rec, uint32_t n,
-    double* __restrict__ out) {
-  extern __shared__ __align__(16) double srow[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
-  const int by = blockIdx.x % T.nty, bz = blockIdx.x / T.nty;
-  // Warp w owns target rows ty0 .. ty0+3 of plane tz (3-D: warps stack in z;
-  // 2-D: in y).
-  int ty0, tz;
-  if (g.dim >= 3) {
-    ty0 = by * kRowsPerWarp;
-    tz = bz * T.warps + warp;
-  } else {
-    ty0 = (by * T.warps + warp) * kRowsPerWarp;
-    tz = 0;
-  }
-  double* rows = srow + (size_t)warp * kRowsPerWarp * T.nxp;
-  if (ty0 >= ny || tz >= nz) return;  // warp-uniform; no CTA barriers below
-  const int nrow = min(kRowsPerWarp, ny - ty0);
-  for (int i = lane; i < kRowsPerWarp * T.nxp; i += 32) rows[i] = 0.0;
-  __syncwarp();
-  const uint32_t le = lanemask_le();
-  const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
-  const bool px = g.periodic[0] != 0;
-  // Source rows cy in [ty0-1, ty0+nrow+1] (unwrapped); for dim 1 only cy = 0.
-  const int cylo = g.dim >= 2 ? ty0 - 1 : 0, cyhi = g.dim >= 2 ? ty0 + nrow + 1 : 0;
-  for (int sz = szlo; sz <= szhi; ++sz) {
-    int cz = 0;
-    if (g.dim >= 3) {
-      cz = tz - sz;
-      if (g.periodic[2]) cz = wrap_cell(cz, nz);
-      else if (cz < -1 || cz > nz) continue;
-    }
-    const double* wzc = rec + (size_t)(8 + sz + 2) * n;
-    for (int cyu = cylo; cyu <= cyhi; ++cyu) {
-      int cy = cyu;
-      if (g.dim >= 2) {
-        if (g.periodic[1]) cy = wrap_cell(cyu, ny);
-        else if (cyu < -1 || cyu > ny) continue;
-      }
-      const uint32_t rid = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
-                           (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(ny + 2) : 0u);
-      const uint32_t rb = __ldg(rowstart + rid), re = __ldg(rowstart + rid + 1);
-      for (uint32_t base = rb; base < re; base += 32) {
-        const uint32_t r = base + lane;
-        const bool valid = r < re;
-        int cx = -0x40000000;
-        double gz[4] = {0.0, 0.0, 0.0, 0.0}, wy[4] = {0.0, 0.0, 0.0, 0.0};
-        if (valid) {
-          cx = __ldg(rec_cx + r);
-          const double wz = __ldg(wzc + r);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            gz[k] = __ldg(rec + (size_t)k * n + r) * wz;
-            wy[k] = __ldg(rec + (size_t)(4 + k) * n + r);
-          }
-        }
-        const int pcx = __shfl_up_sync(0xffffffffu, cx, 1);
-        const bool head = valid && (lane == 0 || pcx != cx);
-        const bool dup = __ballot_sync(0xffffffffu, valid && !head) != 0u;
-        int rank = 0, maxrank = 0;
-        if (dup) {
-          const uint32_t hm = __ballot_sync(0xffffffffu, head);
-          rank = valid ? lane - (31 - __clz(hm & le)) : 0;
-          maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
-        }
-        for (int rr = 0; rr <= maxrank; ++rr) {
-          const bool on = valid && rank == rr;
-#pragma unroll
-          for (int i = 0; i < kRowsPerWarp; ++i) {
-            const int sy = g.dim >= 2 ? ty0 + i - cyu : 0;  // warp-uniform
-            if (i >= nrow || sy < -2 || sy > 1) continue;
-            const double wyv = sy == -2 ? wy[0] : sy == -1 ? wy[1] : sy == 0 ? wy[2] : wy[3];
-            double* rowi = rows + i * T.nxp;
-            const int xi = (kRowPad - 2) + cx;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              if (on) rowi[skew(xi + k)] += gz[k] * wyv;
-              __syncwarp();
-            }
-          }
-        }
-      }
-    }
-  }
-  // Fold the periodic x pad back and write the rows (each element once).
-  for (int i = 0; i < nrow; ++i) {
-    const double* rowi = rows + i * T.nxp;
-    double* orow = out + ((size_t)tz * ny + (ty0 + i)) * nx;
-    for (int x = lane; x < nx; x += 32) {
-      double v = rowi[skew(x + kRowPad)];
-      if (px) {
-        for (int q = x - nx; q >= -3; q -= nx) v += rowi[skew(q + kRowPad)];
-        for (int q = x + nx; q <= nx + 1; q += nx) v += rowi[skew(q + kRowPad)];
-      }
-      orow[x] = v;
-    }
-  }
-}
-
-bool rows_tiling(const DevGrid& g, RowTiling& T) {
-  if (g.dim < 2) return false;
-  const int nx = g.n[0];
-  T.nxp = skewed_len(nx + kRowPad + 2);
-  if (T.nxp & 1) T.nxp += 1;
-  const size_t per_warp = (size_t)kRowsPerWarp * T.nxp * sizeof(double);
-  int warps = 8;
-  while (warps > 1 && warps * per_warp > 200 * 1024) --warps;
-  if (warps * per_warp > 200 * 1024) return false;
-  T.ty = kRowsPerWarp;
-  T.tz = 1;
-  if (g.dim >= 3) {
-    warps = std::min(warps, g.n[2]);
-    T.warps = warps;
-    T.nty = (g.n[1] + kRowsPerWarp - 1) / kRowsPerWarp;
-    T.ntz = (g.n[2] + warps - 1) / warps;
-  } else {
-    const int blocks_y = (g.n[1] + kRowsPerWarp - 1) / kRowsPerWarp;
-    warps = std::min(warps, blocks_y);
-    T.warps = warps;
-    T.nty = (blocks_y + warps - 1) / warps;
-    T.ntz = 1;
-  }
-  return true;
 }
 
 // ---------------------------------------------------------------- K5
@@ -651,45 +492,10 @@ void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
     IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)g.nrows + 1) * 4, st));
   } else {
     rowstart_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
-        s.sorted_keys, (uint32_t)n, s.keys_are_rows ? 1u : g.rowdiv, g.nrows, s.rowstart.p,
-        s.counters.p + kMaxPasses);
+        s.sorted_keys, (uint32_t)n, s.keys_are_rows ? 1u : g.rowdiv, g.nrows, s.rowstart.p);
     ++ctx.launches;
   }
   ctx.prof_end(kProfRows, ev);
-}
-
-size_t zsweep_smem_bytes(const zs::Tiling& T, bool interp) {
-  return interp ? (size_t)4 * (T.ty + 5) * T.nxp * sizeof(double)
-                : sizeof(zs::SpreadSmem) + ((size_t)4 * T.ty * T.nxp + zs::kSThreads) * sizeof(double);
-}
-
-// z-sweep tiling for 3-D grids with rows short enough for shared memory.
-// spread: window of 4 planes x ty rows (small, ~6 CTAs / SM);
-// interp: window of 4 planes x (ty + 5) rows.
-bool zsweep_tiling(const DevGrid& g, bool interp, zs::Tiling& T) {
-  if (g.dim != 3 || !interp) return false;
-  const int nx = g.n[0];
-  const int rowlen = nx + zs::kPadL + zs::kPadR;
-  T.nxp = rowlen + (rowlen >> 4) + 2;
-  if (T.nxp & 1) T.nxp += 1;
-  const size_t row_bytes = (size_t)T.nxp * 8;
-  int ty = 8;
-  while (ty > 1 && (4 * (size_t)(ty + 5) * row_bytes > 110 * 1024 ||
-                    (size_t)(ty + 5) * rowlen > (size_t)zs::kIThreads * zs::kMaxPlaneVals))
-    --ty;
-  if (4 * (size_t)(ty + 5) * row_bytes > 200 * 1024 ||
-      (size_t)(ty + 5) * rowlen > (size_t)zs::kIThreads * zs::kMaxPlaneVals)
-    return false;
-  ty = std::min(ty, g.n[1]);
-  T.ty = ty;
-  T.nty = (g.n[1] + ty - 1) / ty;
-  const size_t smem = zsweep_smem_bytes(T, true);
-  const long per_sm = std::max<long>(1, std::min<long>(8, (220L * 1024) / (long)smem));
-  int zc = (int)std::max<long>(4, ((long)g.n[2] * T.nty * 2) / (148L * per_sm * 3));
-  zc = std::min(zc, g.n[2]);
-  T.zc = zc;
-  T.nzc = (g.n[2] + zc - 1) / zc;
-  return true;
 }
 
 SpreadTiling choose_tiling(const DevGrid& g) {
@@ -1112,44 +918,20 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
                      size_t n, PointScratch& s, double* d_out) {
   if (n == 0) return;
   if (interp_tma_path(ctx, g, d_field, d_points, n, s, d_out)) return;
+  // Generic gather (1-D/2-D grids, x extents the TMA rows do not take): one
+  // thread per point in sorted order.
   cudaStream_t st = ctx.stream;
-  zs::Tiling Z;
-  const bool zsweep = zsweep_tiling(g, true, Z);
-  sort_points(ctx, g, d_points, n, s, zsweep, zsweep ? sort::kPayloadInterp : sort::kPayloadNone);
+  sort_points(ctx, g, d_points, n, s, false, sort::kPayloadNone);
   cudaEvent_t ev = nullptr;
-  if (zsweep) {
-    row_table(ctx, g, n, s);
-    static bool attr_set[64] = {};
-    if (!attr_set[ctx.device & 63]) {
-      IBC_CUDA(cudaFuncSetAttribute(zs::interp_zsweep_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-      attr_set[ctx.device & 63] = true;
-    }
-    ctx.prof_begin(kProfInterp, &ev);
-    zs::interp_zsweep_kernel<<<(unsigned)(Z.nty * Z.nzc), zs::kThreads, zsweep_smem_bytes(Z, true), st>>>(
-        g, Z, s.rowstart.p, s.rec.p, d_field, d_out);
-    ++ctx.launches;
-    ctx.prof_end(kProfInterp, ev);
-  } else {
-    ctx.prof_begin(kProfInterp, &ev);
-    interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
-                                                          (uint32_t)n, d_out);
-    ++ctx.launches;
-    ctx.prof_end(kProfInterp, ev);
-  }
+  ctx.prof_begin(kProfInterp, &ev);
+  interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
+                                                        (uint32_t)n, d_out);
+  ++ctx.launches;
+  ctx.prof_end(kProfInterp, ev);
   IBC_CUDA(cudaGetLastError());
   ++ctx.interp_calls;
 }
 
-int debug_zsweep_trace(int block, long long* out) {
-  if (out) {
-    cudaDeviceSynchronize();
-    return (int)cudaMemcpyFromSymbol(out, zs::g_trace, sizeof(long long) * 2 * 64 * 8);
-  }
-  long long zero[2 * 64 * 8] = {};
-  cudaMemcpyToSymbol(zs::g_trace, zero, sizeof(zero));
-  return (int)cudaMemcpyToSymbol(zs::g_trace_block, &block, sizeof(int));
-}
 
 // ws.run_keys and ws.run_count (= q) on the device, computed on demand from
 // the sorted keys (reduce.hpp:36-69); cached until the next sort.

@@ -166,7 +166,6 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
   const bool px = g.periodic[0] != 0, py = g.periodic[1] != 0;
   const bool pz = D == 3 && g.periodic[2] != 0;
   const double q = 0.25 * g.inv_h;
-  const uint32_t lt = (1u << lane) - 1u;
   const int s_lo = D == 3 ? z0 - 1 : 0, s_hi = D == 3 ? z1 + 1 : 0;
 
   // Lane j < 4: sorted range of source row cy = ty + 2 - j (sigma_y = j - 2)
