@@ -154,19 +154,30 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
   }
 }
 
-// K3, interpolation: {x, y, z, index} at row start + rank.
+// K3, interpolation: each point's 64-byte record at row start + rank --
+// {sin/cos(pi u_a / 2) for a = x, y, z; input index, home cx, home cy} -- so
+// the gather does no cell or trig math.
+template <int D>
 __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
-    const double* __restrict__ X, const uint32_t* __restrict__ rows, const uint32_t* __restrict__ rank,
-    uint32_t n, const uint32_t* __restrict__ start, double* __restrict__ rec) {
+    DevGrid g, const double* __restrict__ X, const uint32_t* __restrict__ rows,
+    const uint32_t* __restrict__ rank, uint32_t n, const uint32_t* __restrict__ start,
+    double* __restrict__ rec) {
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const uint32_t slot = __ldg(start + __ldg(rows + i)) + __ldg(rank + i);
-  double4 r;
-  r.x = __ldg(X + (size_t)i * 3);
-  r.y = __ldg(X + (size_t)i * 3 + 1);
-  r.z = __ldg(X + (size_t)i * 3 + 2);
-  r.w = __longlong_as_double((long long)i);
-  reinterpret_cast<double4*>(rec)[slot] = r;
+  double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};
+  int c[3] = {0, 0, 0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double u;
+    c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &u);
+    sincos_half_pi(u, &tr[a][0], &tr[a][1]);
+  }
+  double4* r4 = reinterpret_cast<double4*>(rec) + 2 * (size_t)slot;
+  r4[0] = make_double4(tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
+  uint4 tail = make_uint4(i, (uint32_t)c[0], (uint32_t)c[1], 0u);
+  r4[1] = make_double4(tr[2][0], tr[2][1], __longlong_as_double(((long long)tail.y << 32) | tail.x),
+                       __longlong_as_double((long long)tail.z));
 }
 
 // K3, spread: (key, index) at row start + rank (the rows' stable order comes

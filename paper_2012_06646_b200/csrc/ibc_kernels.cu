@@ -750,7 +750,7 @@ bool interp_tma_tiling(const DevGrid& g, size_t n, sw::InterpTiling& T) {
     const double mean = (double)n * (ty + ghosts) / ((double)(ny + 2) * (nz + 2));
     int cap = (int)std::min(1024.0, std::max(64.0, 2.0 * mean + 32.0));
     cap = (cap + 31) & ~31;
-    const uint32_t stride = (uint32_t)(((size_t)fr * pitch + (size_t)cap * 32 + 1023) & ~size_t(1023));
+    const uint32_t stride = (uint32_t)(((size_t)fr * pitch + (size_t)cap * 64 + 1023) & ~size_t(1023));
     const size_t budget = 226 * 1024 - 16 * sw::kMaxSlots - 12 * (size_t)hmax - 1024;
     const int slots = (int)std::min<size_t>(sw::kMaxSlots, budget / stride);
     if (slots < 5) continue;
@@ -847,8 +847,12 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
       count, s.rowstart.p, nrows, status, ticket, spread ? long_rows : nullptr, nlong);
   ctx.launches += 2;
   if (!spread) {
-    bucket::scatter_interp_kernel<<<blocks, bucket::kThreads, 0, st>>>(
-        d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+    if (g.dim == 3)
+      bucket::scatter_interp_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
+          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+    else
+      bucket::scatter_interp_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
+          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {

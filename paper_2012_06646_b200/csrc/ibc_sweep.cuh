@@ -1,8 +1,9 @@
 // ibc_sweep.cuh -- 3-D interpolation gather fed by TMA (sm_100a).
 //
 // Replaces the per-point loop of ib::interpolate (interpolate.hpp:22-58,
-// Alg. 3).  Points arrive sorted by their home row (cy, cz), each as a 32-byte
-// record {x, y, z, input index} written by the last radix pass.
+// Alg. 3).  Points arrive grouped by their home row (cy, cz) (ibc_bucket.cuh),
+// each as a 64-byte record {sin/cos(pi u_a / 2) per axis, input index, home
+// cx, home cy}: cells and trig are computed once, by the bucketing pass.
 //
 // A CTA (one per SM) owns TY home rows [y0, y0 + TY) of a z-chunk [z0, z1)
 // and sweeps its home planes in order.  The field planes a home plane s needs
@@ -20,9 +21,8 @@
 //
 // Gather layout: four lanes per point, lane k reading x = cx + k - 2 of every
 // (y, z) window row; the quad's partial sums are combined with two
-// xor-shuffles.  Lanes 0..2 of a quad compute the cell and sin/cos of one axis
-// each and share them.  Groups of 8 points are dealt round-robin to the
-// consumer warps across steps, so no warp is systematically the last one.
+// xor-shuffles.  Groups of 8 points are dealt round-robin to the consumer
+// warps across steps, so no warp is systematically the last one.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -45,7 +45,7 @@ struct InterpTiling {
   uint32_t slot_bytes;   // frmax * pitch
   int rec_cap;           // point records staged per step (32 B each)
   int hmax;              // max home planes per CTA (row-range table entries)
-  uint32_t slot_stride;  // slot_bytes + rec_cap * 32, rounded up to 1024
+  uint32_t slot_stride;  // slot_bytes + rec_cap * 64, rounded up to 1024
   int box_ok;            // one TMA per plane allowed (nx % 128 == 0)
 };
 
@@ -131,8 +131,8 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
       const uint32_t dst = base + (uint32_t)slot * T.slot_stride;
       tma::fence_proxy_async();
       if (lane == 0) {
-        tma::mbar_expect_tx(bar, plane_bytes + nrec * 32u);
-        if (nrec) tma::bulk_g2s(dst + T.slot_bytes, rec + 4 * (size_t)ra, nrec * 32u, bar);
+        tma::mbar_expect_tx(bar, plane_bytes + nrec * 64u);
+        if (nrec) tma::bulk_g2s(dst + T.slot_bytes, rec + 8 * (size_t)ra, nrec * 64u, bar);
         if (box) tma::load_4d(dst, &tmap_box, 0, 0, hy0 - 2, t, bar);
       }
       __syncwarp();
@@ -149,10 +149,9 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
 
   // -------------------------------------------------------------- consumers
   // Quad layout: point p = lane / 4 of an 8-point group, kx = lane % 4.
-  const int kx = lane & 3, qbase = lane & ~3;
-  const int ax = kx < 3 ? kx : 0;  // axis this lane evaluates (lane 3 repeats x)
-  const Axis A = axis_of(g, ax);
+  const int kx = lane & 3;
   const bool px = g.periodic[0] != 0;
+  const double q = 0.25 * g.inv_h;
   // Slot of plane j (j % NS) and fill parity of plane j + 3, advanced
   // incrementally (no integer division in the loop).
   int slot_j = 0, slot_3 = 3 % NS;
@@ -169,7 +168,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
       const int sk = slot_j + kz;
       sl[kz] = slots + (size_t)(sk >= NS ? sk - NS : sk) * T.slot_stride;
     }
-    const double2* srec = reinterpret_cast<const double2*>(sl[3] + T.slot_bytes);
+    const double2* srec = reinterpret_cast<const double2*>(sl[3] + T.slot_bytes);  // 4 x double2 per point
     // This warp's groups: k with (gfirst + k) % kIConsumers == warp.
     const uint32_t k0 =
         (uint32_t)(warp - (int)(gfirst % kIConsumers) + kIConsumers) % kIConsumers;
@@ -177,34 +176,26 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
     for (uint32_t g0 = a + 8u * k0; g0 < b; g0 += 8u * kIConsumers) {
       const uint32_t r = g0 + (uint32_t)(lane >> 2);
       const bool valid = r < b;
-      double2 q0 = make_double2(0.0, 0.0), q1 = q0;
+      // Record: {sx, cx', sy, cy', sz, cz', (index, home cx), home cy}.
+      double2 tx = make_double2(0.0, 1.0), ty = tx, tz = tx, id = make_double2(0.0, 0.0);
       if (valid) {
-        if (r - a < (uint32_t)T.rec_cap) {
-          q0 = srec[2 * (r - a)];
-          q1 = srec[2 * (r - a) + 1];
-        } else {
-          q0 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r);
-          q1 = __ldg(reinterpret_cast<const double2*>(rec) + 2 * (size_t)r + 1);
-        }
+        const double2* r2 = r - a < (uint32_t)T.rec_cap
+                                ? srec + 4 * (r - a)
+                                : reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
+        tx = r2[0];
+        ty = r2[1];
+        tz = r2[2];
+        id = r2[3];
       }
-      // This lane's axis: home cell and sin/cos(pi u / 2), u = -t.
-      const double xa = ax == 0 ? q0.x : (ax == 1 ? q0.y : q1.x);
-      double u = 0.0;
-      const int ca = valid ? cell_and_u(A, g.h, g.inv_h, xa, &u) : 0;
-      double sn, cs;
-      sincos_half_pi(u, &sn, &cs);
-      // Gather the three axes from lanes qbase + 0..2.
-      const int cx = __shfl_sync(0xffffffffu, ca, qbase);
-      const int cy = __shfl_sync(0xffffffffu, ca, qbase + 1);
-      const double sx = shfl_d(sn, qbase), cxs = shfl_d(cs, qbase);
-      const double sy = shfl_d(sn, qbase + 1), cys = shfl_d(cs, qbase + 1);
-      const double sz = shfl_d(sn, qbase + 2), czs = shfl_d(cs, qbase + 2);
-      const double q = 0.25 * g.inv_h;
+      const long long pk = __double_as_longlong(id.x);
+      const uint32_t idx = (uint32_t)pk;
+      const int cx = (int)(pk >> 32);
+      const int cy = (int)__double_as_longlong(id.y);
       // phi(sigma - t)/h for sigma = -2..1: (1-c), (1+s), (1+c), (1-s) over 4h.
-      const double wy[4] = {q * (1.0 - cys), q * (1.0 + sy), q * (1.0 + cys), q * (1.0 - sy)};
-      const double wz[4] = {q * (1.0 - czs), q * (1.0 + sz), q * (1.0 + czs), q * (1.0 - sz)};
-      double wxk = kx == 0 ? (1.0 - cxs) : kx == 1 ? (1.0 + sx) : kx == 2 ? (1.0 + cxs) : (1.0 - sx);
-      wxk *= q;
+      const double wy[4] = {fma(-q, ty.y, q), fma(q, ty.x, q), fma(q, ty.y, q), fma(-q, ty.x, q)};
+      const double wz[4] = {fma(-q, tz.y, q), fma(q, tz.x, q), fma(q, tz.y, q), fma(-q, tz.x, q)};
+      const double vx = (kx & 1) ? tx.x : tx.y;
+      double wxk = fma((kx == 0 || kx == 3) ? -q : q, vx, q);
       int x = cx + kx - 2;
       if (px) {
         x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
@@ -228,7 +219,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (valid && kx == 0) out[(uint32_t)__double_as_longlong(q1.y)] = acc * g.hd;
+      if (valid && kx == 0) out[idx] = acc * g.hd;
     }
     // Plane j is not read by any later step.
     __syncwarp();
