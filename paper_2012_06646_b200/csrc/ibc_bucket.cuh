@@ -16,8 +16,9 @@
 // every row into stable (key, index) order -- which makes the result exactly
 // the reference's stable key-value sort -- and writes the weight records the
 // spread sweep streams in that order:
-//   K4 rows of <= 32 points: one warp, rank by 32 shuffled compares;
-//      longer rows (listed by K2): one CTA, bitonic sort in shared memory;
+//   K4 rows of <= 256 points: one warp, rank by shuffled compares against
+//      every 32-point chunk; longer rows (listed by K2): one CTA, bitonic
+//      sort in shared memory;
 //      per sorted position: cell + one sin/cos pair per axis -> 64-byte record.
 #pragma once
 #include <cstdint>
@@ -35,7 +36,7 @@ constexpr int kChunk = kScanThreads * kScanItems;  // rows per scan CTA
 constexpr uint32_t kFlagAggregate = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
-constexpr int kShortRow = 32;       // rows up to this length are sorted by one warp
+constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
 // Cell key of every point (or just its row when full_key == 0), its arrival
@@ -218,8 +219,8 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
   rcx[o] = cx;
 }
 
-// K4, short rows: one warp per row puts (key, index) in stable order and
-// writes each point's weight record at its sorted position.
+// K4, rows up to kShortRow points: one warp per row puts (key, index) in
+// stable order and writes each point's weight record at its sorted position.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     const uint32_t* __restrict__ start, uint32_t nrows, const uint32_t* __restrict__ bkey,
@@ -231,18 +232,34 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
   for (uint32_t r = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
     const uint32_t a = __ldg(start + r), len = __ldg(start + r + 1) - a;
     if (len == 0 || len > (uint32_t)kShortRow) continue;  // empty, or a long row (K4b)
-    const bool valid = (uint32_t)lane < len;
-    const uint32_t k = valid ? __ldg(bkey + a + lane) : 0xffffffffu;
-    const uint32_t ix = valid ? __ldg(bidx + a + lane) : 0xffffffffu;
-    uint32_t rk = 0;
-    for (uint32_t j = 0; j < len; ++j) {
-      const uint32_t kj = __shfl_sync(0xffffffffu, k, j), ij = __shfl_sync(0xffffffffu, ix, j);
-      rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
-    }
-    if (valid) {
-      skey[a + rk] = k;
-      sidx[a + rk] = ix;
-      write_record<D>(g, X, G, ix, a + rk, rec, rcx);
+    // Rank of each element among the row's (key, index) pairs, 32 elements
+    // per pass, by shuffled compares against every 32-element chunk.
+    for (uint32_t e0 = 0; e0 < len; e0 += 32) {
+      const bool valid = e0 + (uint32_t)lane < len;
+      const uint32_t k = valid ? __ldg(bkey + a + e0 + lane) : 0xffffffffu;
+      const uint32_t ix = valid ? __ldg(bidx + a + e0 + lane) : 0xffffffffu;
+      uint32_t rk = 0;
+      if (len <= 32) {  // the common short row: one chunk, already in registers
+        for (uint32_t j = 0; j < len; ++j) {
+          const uint32_t kj = __shfl_sync(0xffffffffu, k, j), ij = __shfl_sync(0xffffffffu, ix, j);
+          rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
+        }
+      } else {
+        for (uint32_t c0 = 0; c0 < len; c0 += 32) {
+          const uint32_t kc = c0 == e0 ? k : (c0 + lane < len ? __ldg(bkey + a + c0 + lane) : 0xffffffffu);
+          const uint32_t ic = c0 == e0 ? ix : (c0 + lane < len ? __ldg(bidx + a + c0 + lane) : 0xffffffffu);
+          const uint32_t m = min(32u, len - c0);
+          for (uint32_t j = 0; j < m; ++j) {
+            const uint32_t kj = __shfl_sync(0xffffffffu, kc, j), ij = __shfl_sync(0xffffffffu, ic, j);
+            rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
+          }
+        }
+      }
+      if (valid) {
+        skey[a + rk] = k;
+        sidx[a + rk] = ix;
+        write_record<D>(g, X, G, ix, a + rk, rec, rcx);
+      }
     }
   }
 }
