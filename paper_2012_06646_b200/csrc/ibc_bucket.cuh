@@ -75,13 +75,14 @@ __device__ __forceinline__ uint32_t ld_flag(const uint32_t* p) {
 
 // Exclusive scan of count[0..nrows) into start[0..nrows] (start[nrows] = total).
 // status: one zeroed word per chunk; ticket: zeroed counter.  Rows longer than
-// kShortRow are appended to long_rows (count in *nlong) when long_rows != null.
+// kShortRow are appended to long_rows (count in *nlong) when long_rows != null;
+// *maxrow (zeroed, may be null) receives the largest row count.
 __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* __restrict__ count,
                                                                 uint32_t* __restrict__ start,
                                                                 uint32_t nrows, uint32_t* status,
                                                                 uint32_t* ticket,
                                                                 uint32_t* __restrict__ long_rows,
-                                                                uint32_t* nlong) {
+                                                                uint32_t* nlong, uint32_t* maxrow) {
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_chunk, s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -89,13 +90,16 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
   __syncthreads();
   const uint32_t chunk = s_chunk;
   const uint32_t r0 = chunk * (uint32_t)kChunk + (uint32_t)tid * kScanItems;
-  uint32_t v[kScanItems], sum = 0;
+  uint32_t v[kScanItems], sum = 0, vmax = 0;
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q) {
     v[q] = r0 + q < nrows ? count[r0 + q] : 0u;
     sum += v[q];
+    vmax = max(vmax, v[q]);
     if (long_rows && v[q] > (uint32_t)kShortRow) long_rows[atomicAdd(nlong, 1u)] = r0 + q;
   }
+  vmax = __reduce_max_sync(0xffffffffu, vmax);
+  if (maxrow && lane == 0) atomicMax(maxrow, vmax);  // densest row (spread batching mode)
   // Block scan of the per-thread sums.
   uint32_t x = sum;
 #pragma unroll

@@ -675,12 +675,17 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   if (!attr_set[ctx.device & 63]) {
     IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
-    for (const void* k : {(const void*)sp::spread_sweep_kernel<2, 0>,
-                          (const void*)sp::spread_sweep_kernel<3, 0>,
-                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64)>,
-                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128)>,
-                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256)>,
-                          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512)>})
+    for (const void* k :
+         {(const void*)sp::spread_sweep_kernel<2, 0, false>, (const void*)sp::spread_sweep_kernel<2, 0, true>,
+          (const void*)sp::spread_sweep_kernel<3, 0, false>, (const void*)sp::spread_sweep_kernel<3, 0, true>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64), false>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64), true>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128), false>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128), true>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256), false>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256), true>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512), false>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512), true>})
       IBC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[ctx.device & 63] = true;
   }
@@ -688,20 +693,30 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     ctx.prof_begin(kProfSpread, &ev);
     const size_t smem = (size_t)W.wpc * (g.dim == 3 ? 4 : 1) * W.rl * sizeof(double);
     const unsigned blocks = (unsigned)(W.nyg * W.nzc);
-    // Compile-time window row length for the common x extents.
-    auto launch = [&](auto kern) {
-      kern<<<blocks, 32 * W.wpc, smem, st>>>(g, W, s.rowstart.p, smap, s.rec.p, s.rec_cx.p, d_out);
+    // Compile-time window row length for the common x extents; both batch
+    // modes are launched when the densest row is only known on the device.
+    const uint32_t* maxrow = (!radix) ? s.maxrow : nullptr;
+    auto launch = [&](auto defer_k, auto pull_k) {
+      defer_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
+                                                s.rec_cx.p, d_out);
+      if (maxrow) {
+        pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
+                                                 s.rec_cx.p, d_out);
+        ++ctx.launches;
+      }
     };
     const int nx = g.n[0];
+#define IBC_SWEEP(D, RL) launch(sp::spread_sweep_kernel<D, RL, false>, sp::spread_sweep_kernel<D, RL, true>)
     if (g.dim == 3) {
-      if (W.rl == sp::row_len(64) && nx == 64) launch(sp::spread_sweep_kernel<3, sp::row_len(64)>);
-      else if (W.rl == sp::row_len(128) && nx == 128) launch(sp::spread_sweep_kernel<3, sp::row_len(128)>);
-      else if (W.rl == sp::row_len(256) && nx == 256) launch(sp::spread_sweep_kernel<3, sp::row_len(256)>);
-      else if (W.rl == sp::row_len(512) && nx == 512) launch(sp::spread_sweep_kernel<3, sp::row_len(512)>);
-      else launch(sp::spread_sweep_kernel<3, 0>);
+      if (W.rl == sp::row_len(64) && nx == 64) IBC_SWEEP(3, sp::row_len(64));
+      else if (W.rl == sp::row_len(128) && nx == 128) IBC_SWEEP(3, sp::row_len(128));
+      else if (W.rl == sp::row_len(256) && nx == 256) IBC_SWEEP(3, sp::row_len(256));
+      else if (W.rl == sp::row_len(512) && nx == 512) IBC_SWEEP(3, sp::row_len(512));
+      else IBC_SWEEP(3, 0);
     } else {
-      launch(sp::spread_sweep_kernel<2, 0>);
+      IBC_SWEEP(2, 0);
     }
+#undef IBC_SWEEP
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   } else {
@@ -822,8 +837,9 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   uint32_t* status = count + nrows;
   uint32_t* ticket = status + nchunks;
   uint32_t* nlong = ticket + 1;
-  uint32_t* long_rows = nlong + 1;
-  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 2) * 4, st));
+  uint32_t* maxrow = nlong + 1;
+  uint32_t* long_rows = maxrow + 1;
+  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 3) * 4, st));
   if (n == 0) {
     IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)nrows + 1) * 4, st));
     return;
@@ -844,7 +860,8 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   ctx.prof_end(kProfKeys, ev);
   ctx.prof_begin(kProfSort, &ev);
   bucket::row_scan_kernel<<<nchunks, bucket::kScanThreads, 0, st>>>(
-      count, s.rowstart.p, nrows, status, ticket, spread ? long_rows : nullptr, nlong);
+      count, s.rowstart.p, nrows, status, ticket, spread ? long_rows : nullptr, nlong, maxrow);
+  s.maxrow = spread ? maxrow : nullptr;
   ctx.launches += 2;
   if (!spread) {
     if (g.dim == 3)

@@ -17,9 +17,11 @@
 // source rows that reach ty (cy = ty+2 .. ty-1, concatenated into full
 // 32-lane batches) and adds their 16 contributions (4 x 4 z) per lane.
 // Lanes that share a home cx -- same cell, or different source rows -- would
-// hit the same address: all but the first (match_any) are deferred to the
-// next batch, so batches stay full, adds never collide, and the summation
-// order is the sequence order -- results are bitwise reproducible.  When plane
+// hit the same addresses.  Sparse points: all but the first (match_any) are
+// deferred to the next batch.  Dense / clustered points: the group's lowest
+// lane gathers the others' contributions by shuffles and adds alone.  Either
+// way adds never collide and the summation order is the sequence order --
+// results are bitwise reproducible.  When plane
 // s is done, target plane s-2 is complete: the warp folds the periodic x pad,
 // stores the row once (coalesced) and clears the slot for plane s+2.  No CTA
 // barrier anywhere: warps are independent, which is what lets 24 of them per
@@ -36,6 +38,7 @@ namespace ibc {
 namespace sp {
 
 constexpr int kPadL = 4;  // padded x index xi = x + kPadL
+constexpr uint32_t kPullRow = 64;  // densest row above which batches pull instead of defer
 constexpr int kPadR = 2;
 
 struct SweepTiling {
@@ -142,14 +145,107 @@ __device__ __forceinline__ void plane_batches(double* __restrict__ W, const int 
   }
 }
 
-template <int D, int RL>
-__global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTiling T,
+template <int D, int RL, int R>
+__device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const int so[4], uint32_t e0,
+                                              uint32_t e1, uint32_t e2, uint32_t total,
+                                              uint32_t rstart, const uint32_t* __restrict__ smap,
+                                              const double* __restrict__ rec,
+                                              const int* __restrict__ rcx, double q) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t base = 0; base < total; base += 32) {
+    const uint32_t p = base + (uint32_t)lane;
+    const bool valid = p < total;
+    const int j = (p >= e0) + (p >= e1) + (p >= e2);
+    const uint32_t rs = __shfl_sync(0xffffffffu, rstart, j & 3) + p;
+    int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
+    double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
+    if (valid) {
+      const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
+      const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
+      g01 = __ldg(r2);
+      g23 = __ldg(r2 + 1);
+      tr = __ldg(r2 + 2);
+      tz2 = __ldg(r2 + 3);
+      cx = __ldg(rcx + r);
+    }
+    // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
+    const double vy = (j & 1) ? tr.x : tr.y;
+    const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
+    double a[4];
+    if (D == 3) {
+      a[0] = fma(-wq, tz2.y, wq);
+      a[1] = fma(wq, tz2.x, wq);
+      a[2] = fma(wq, tz2.y, wq);
+      a[3] = fma(-wq, tz2.x, wq);
+    } else {
+      a[0] = a[1] = a[3] = 0.0;
+      a[2] = wq / q;
+    }
+    double gk[4] = {g01.x, g01.y, g23.x, g23.y};
+    // Lanes with the same home cx (same cell, or another source row) hit the
+    // same 16 targets of this warp's row: the lowest such lane sums the
+    // group's contributions in lane (= sequence) order and adds alone.
+    const uint32_t peers = __match_any_sync(0xffffffffu, cx);  // every lane takes part
+    const int gmax = (int)__reduce_max_sync(0xffffffffu, (uint32_t)__popc(peers));
+    const bool lead = valid && (peers & ((1u << lane) - 1u)) == 0u;
+    double v[4][4];
+#pragma unroll
+    for (int kx = 0; kx < 4; ++kx)
+#pragma unroll
+      for (int kz = 0; kz < 4; ++kz) v[kx][kz] = gk[kx] * a[kz];
+    if (gmax > 1) {
+      uint32_t rest = lead ? peers & (peers - 1u) : 0u;  // members after the leader
+      for (int it = 1; it < gmax; ++it) {
+        const int src = rest ? __ffs(rest) - 1 : lane;
+        double mg[4], ma[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          mg[k] = __shfl_sync(0xffffffffu, gk[k], src);
+          ma[k] = __shfl_sync(0xffffffffu, a[k], src);
+        }
+        if (rest) {
+#pragma unroll
+          for (int kx = 0; kx < 4; ++kx)
+#pragma unroll
+            for (int kz = 0; kz < 4; ++kz) v[kx][kz] = fma(mg[kx], ma[kz], v[kx][kz]);
+          rest &= rest - 1u;
+        }
+      }
+    }
+    const int xb = cx + (kPadL - 2);
+#pragma unroll
+    for (int kx = 0; kx < 4; ++kx) {
+      if (lead) {
+        double* wa = W + skew(xb + kx);
+        if (R >= 0) {
+#pragma unroll
+          for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * RL] += v[kx][kz];
+        } else {
+#pragma unroll
+          for (int kz = 0; kz < 4; ++kz)
+            if (so[kz] >= 0) wa[so[kz]] += v[kx][kz];
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// PULL = false: colliding lanes are deferred to the next batch (few
+// collisions: sparse points).  PULL = true: colliding lanes are summed into
+// their group leader by shuffles (dense or clustered points, where deferral
+// would serialise).  Both are launched; the one that does not match the
+// densest row seen by the row scan (*maxrow) returns at once.
+template <int D, int RL, bool PULL>
+__global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTiling T,
+                                                           const uint32_t* __restrict__ maxrow,
                                                            const uint32_t* __restrict__ rowstart,
                                                            const uint32_t* __restrict__ smap,
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
+  if ((maxrow && *maxrow > kPullRow) != PULL) return;
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -215,13 +311,13 @@ __global__ void __launch_bounds__(256) spread_sweep_kernel(DevGrid g, SweepTilin
       const bool interior = D == 3 && s - 2 >= z0 && s + 1 < z1;
       if (RL > 0 && interior) {
         switch (s & 3) {
-          case 0: plane_batches<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-          case 1: plane_batches<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-          case 2: plane_batches<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-          default: plane_batches<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          case 0: if (PULL) plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          case 1: if (PULL) plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          case 2: if (PULL) plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          default: if (PULL) plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
         }
       } else {
-        plane_batches<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q);
+        if (PULL) plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q);
       }
     }
     // Target plane s - 2 has all its sources: fold, store once, clear.
