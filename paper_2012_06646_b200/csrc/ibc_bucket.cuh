@@ -16,9 +16,9 @@
 // every row into stable (key, index) order -- which makes the result exactly
 // the reference's stable key-value sort -- and writes the weight records the
 // spread sweep streams in that order:
-//   K4 rows of <= 256 points: one warp, rank by shuffled compares against
-//      every 32-point chunk; longer rows (listed by K2): one CTA, bitonic
-//      sort in shared memory;
+//   K4 rows of <= 256 points: one thread per point, rank by compares against
+//      its row's pairs; longer rows (listed by K2): one CTA, bitonic sort in
+//      shared memory;
 //      per sorted position: cell + one sin/cos pair per axis -> 64-byte record.
 #pragma once
 #include <cstdint>
@@ -178,11 +178,10 @@ __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
     c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &u);
     sincos_half_pi(u, &tr[a][0], &tr[a][1]);
   }
-  double4* r4 = reinterpret_cast<double4*>(rec) + 2 * (size_t)slot;
-  r4[0] = make_double4(tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
-  uint4 tail = make_uint4(i, (uint32_t)c[0], (uint32_t)c[1], 0u);
-  r4[1] = make_double4(tr[2][0], tr[2][1], __longlong_as_double(((long long)tail.y << 32) | tail.x),
-                       __longlong_as_double((long long)tail.z));
+  double* r = rec + 8 * (size_t)slot;
+  st_v4(r, tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
+  st_v4(r + 4, tr[2][0], tr[2][1], __longlong_as_double(((long long)c[0] << 32) | i),
+        __longlong_as_double((long long)(uint32_t)c[1]));
 }
 
 // K3, spread: (key, index) at row start + rank (the rows' stable order comes
@@ -203,69 +202,78 @@ __global__ void __launch_bounds__(kThreads) scatter_pairs_kernel(
 //   {G phi_x(k-2-t_x)/h (k = 0..3), sin/cos(pi u_y/2), sin/cos(pi u_z/2)},
 // and its home cell along x (wrapped on periodic x).
 template <int D>
-__device__ __forceinline__ void write_record(const DevGrid& g, const double* __restrict__ X,
-                                             const double* __restrict__ G, uint32_t i, uint32_t o,
-                                             double* __restrict__ rec, int* __restrict__ rcx) {
+__device__ __forceinline__ void write_record_from(const DevGrid& g, const double (&x)[3], double gv,
+                                                  uint32_t o, double* __restrict__ rec,
+                                                  int* __restrict__ rcx) {
   double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};  // u = 0 on padded axes
   int cx = 0;
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     double u;
-    const int c = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &u);
+    const int c = cell_and_u(axis_of(g, a), g.h, g.inv_h, x[a], &u);
     if (a == 0) cx = c;
     sincos_half_pi(u, &tr[a][0], &tr[a][1]);
   }
-  const double gq = __ldg(G + i) * (0.25 * g.inv_h);
-  double4* r4 = reinterpret_cast<double4*>(rec) + 2 * (size_t)o;
-  r4[0] = make_double4(gq * (1.0 - tr[0][1]), gq * (1.0 + tr[0][0]), gq * (1.0 + tr[0][1]),
-                       gq * (1.0 - tr[0][0]));
-  r4[1] = make_double4(tr[1][0], tr[1][1], tr[2][0], tr[2][1]);
+  const double gq = gv * (0.25 * g.inv_h);
+  double* r = rec + 8 * (size_t)o;
+  st_v4(r, gq * (1.0 - tr[0][1]), gq * (1.0 + tr[0][0]), gq * (1.0 + tr[0][1]),
+        gq * (1.0 - tr[0][0]));
+  st_v4(r + 4, tr[1][0], tr[1][1], tr[2][0], tr[2][1]);
   rcx[o] = cx;
 }
 
-// K4, rows up to kShortRow points: one warp per row puts (key, index) in
-// stable order and writes each point's weight record at its sorted position.
+template <int D>
+__device__ __forceinline__ void write_record(const DevGrid& g, const double* __restrict__ X,
+                                             const double* __restrict__ G, uint32_t i, uint32_t o,
+                                             double* __restrict__ rec, int* __restrict__ rcx) {
+  double x[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < D; ++a) x[a] = __ldg(X + (size_t)i * D + a);
+  write_record_from<D>(g, x, __ldg(G + i), o, rec, rcx);
+}
+
+// K4, rows up to kShortRow points: one thread per bucket slot ranks its
+// (key, index) among its row's pairs -- the row is read straight from the
+// bucket (contiguous, and shared by neighbouring lanes, so the loads are
+// L1 broadcasts) -- and writes the pair and its weight record at the row's
+// start + rank: stable (key, index) order.  Full warps whatever the row
+// lengths.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
-    const uint32_t* __restrict__ start, uint32_t nrows, const uint32_t* __restrict__ bkey,
+    const uint32_t* __restrict__ start, uint32_t n, const uint32_t* __restrict__ bkey,
     const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
     double* __restrict__ rec, int* __restrict__ rcx) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warps = gridDim.x * (kThreads / 32);
-  for (uint32_t r = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5); r < nrows; r += warps) {
-    const uint32_t a = __ldg(start + r), len = __ldg(start + r + 1) - a;
-    if (len == 0 || len > (uint32_t)kShortRow) continue;  // empty, or a long row (K4b)
-    // Rank of each element among the row's (key, index) pairs, 32 elements
-    // per pass, by shuffled compares against every 32-element chunk.
-    for (uint32_t e0 = 0; e0 < len; e0 += 32) {
-      const bool valid = e0 + (uint32_t)lane < len;
-      const uint32_t k = valid ? __ldg(bkey + a + e0 + lane) : 0xffffffffu;
-      const uint32_t ix = valid ? __ldg(bidx + a + e0 + lane) : 0xffffffffu;
-      uint32_t rk = 0;
-      if (len <= 32) {  // the common short row: one chunk, already in registers
-        for (uint32_t j = 0; j < len; ++j) {
-          const uint32_t kj = __shfl_sync(0xffffffffu, k, j), ij = __shfl_sync(0xffffffffu, ix, j);
-          rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
-        }
-      } else {
-        for (uint32_t c0 = 0; c0 < len; c0 += 32) {
-          const uint32_t kc = c0 == e0 ? k : (c0 + lane < len ? __ldg(bkey + a + c0 + lane) : 0xffffffffu);
-          const uint32_t ic = c0 == e0 ? ix : (c0 + lane < len ? __ldg(bidx + a + c0 + lane) : 0xffffffffu);
-          const uint32_t m = min(32u, len - c0);
-          for (uint32_t j = 0; j < m; ++j) {
-            const uint32_t kj = __shfl_sync(0xffffffffu, kc, j), ij = __shfl_sync(0xffffffffu, ic, j);
-            rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
-          }
-        }
-      }
-      if (valid) {
-        skey[a + rk] = k;
-        sidx[a + rk] = ix;
-        write_record<D>(g, X, G, ix, a + rk, rec, rcx);
-      }
+  const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
+  if (o >= n) return;
+  const uint32_t k = __ldg(bkey + o), ix = __ldg(bidx + o);
+  const uint32_t row = k / g.rowdiv;
+  const uint32_t a = __ldg(start + row), len = __ldg(start + row + 1) - a;
+  if (len > (uint32_t)kShortRow) return;  // long rows: K4b
+  // The point's position and value are gathered before the rank loop so
+  // their latency hides behind it.
+  double x[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int d = 0; d < D; ++d) x[d] = __ldg(X + (size_t)ix * D + d);
+  const double gv = __ldg(G + ix);
+  uint32_t rk = 0, j = 0;
+  for (; j + 4 <= len; j += 4) {
+    uint32_t kj[4], ij[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      kj[u] = __ldg(bkey + a + j + u);
+      ij[u] = __ldg(bidx + a + j + u);
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) rk += (kj[u] < k || (kj[u] == k && ij[u] < ix)) ? 1u : 0u;
   }
+  for (; j < len; ++j) {
+    const uint32_t kj = __ldg(bkey + a + j), ij = __ldg(bidx + a + j);
+    rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
+  }
+  skey[a + rk] = k;
+  sidx[a + rk] = ix;
+  write_record_from<D>(g, x, gv, a + rk, rec, rcx);
 }
 
 // K4b, long rows: one CTA per listed row, bitonic sort of (key << 32 | index)

@@ -222,4 +222,18 @@ __device__ __forceinline__ void unit_weights(double w[4]) {
   w[0] = 0.0; w[1] = 0.0; w[2] = 1.0; w[3] = 0.0;
 }
 
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): one 32-byte sector
+// per instruction instead of two half-sector 128-bit ones.
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+__device__ __forceinline__ double4 ld_v4_nc(const double* p) {
+  double4 v;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+      : "l"(p));
+  return v;
+}
+
 }  // namespace ibc

@@ -635,6 +635,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
   while (wpc > 1 && wpc * per_warp > 200 * 1024) --wpc;
   T.wpc = wpc;
   T.rl = rl;
+  T.pull_row = getenv("IBC_PULL_ROW") ? (uint32_t)atoi(getenv("IBC_PULL_ROW")) : sp::kPullRow;
   T.nyg = (ny + wpc - 1) / wpc;
   if (g.dim == 3) {
     const long per_sm = std::max<long>(1, std::min<long>(2048 / (32 * wpc), (227L * 1024) / (long)(wpc * per_warp)));
@@ -875,7 +876,6 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   } else {
     bucket::scatter_pairs_kernel<<<blocks, bucket::kThreads, 0, st>>>(
         s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.keys[1].p, s.vals[1].p);
-    const unsigned rblocks = std::min<unsigned>(grid_for(nrows, bucket::kThreads / 32), 148u * 16u);
     static bool attr_set[64] = {};
     const size_t lsm = (size_t)bucket::kLongSortMax * 8;
     if (!attr_set[ctx.device & 63]) {
@@ -886,9 +886,9 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
       attr_set[ctx.device & 63] = true;
     }
     auto sorts = [&](auto short_k, auto long_k) {
-      short_k<<<rblocks, bucket::kThreads, 0, st>>>(s.rowstart.p, nrows, s.keys[1].p, s.vals[1].p,
-                                                    s.keys[0].p, s.vals[0].p, g, d_points,
-                                                    d_values, s.rec.p, s.rec_cx.p);
+      short_k<<<blocks, bucket::kThreads, 0, st>>>(s.rowstart.p, (uint32_t)n, s.keys[1].p,
+                                                   s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
+                                                   d_points, d_values, s.rec.p, s.rec_cx.p);
       long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.keys[1].p,
                                                      s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
                                                      d_points, d_values, s.rec.p, s.rec_cx.p);

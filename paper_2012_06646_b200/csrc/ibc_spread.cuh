@@ -46,6 +46,7 @@ struct SweepTiling {
   int nyg;       // CTAs along y
   int zc, nzc;   // z-chunk length, chunks
   int rl;        // doubles per window row (padded + skewed, even)
+  uint32_t pull_row;  // densest row above which batches pull instead of defer
 };
 
 __device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
@@ -94,11 +95,11 @@ __device__ __forceinline__ void plane_batches(double* __restrict__ W, const int 
     double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
     if (valid) {
       const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
-      const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
-      g01 = __ldg(r2);
-      g23 = __ldg(r2 + 1);
-      tr = __ldg(r2 + 2);
-      tz2 = __ldg(r2 + 3);
+      const double4 ga = ld_v4_nc(rec + 8 * (size_t)r), gb = ld_v4_nc(rec + 8 * (size_t)r + 4);
+      g01 = make_double2(ga.x, ga.y);
+      g23 = make_double2(ga.z, ga.w);
+      tr = make_double2(gb.x, gb.y);
+      tz2 = make_double2(gb.z, gb.w);
       cx = __ldg(rcx + r);
     }
     const uint32_t peers = __match_any_sync(0xffffffffu, cx);  // every lane takes part
@@ -161,11 +162,11 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
     double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
     if (valid) {
       const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
-      const double2* r2 = reinterpret_cast<const double2*>(rec) + 4 * (size_t)r;
-      g01 = __ldg(r2);
-      g23 = __ldg(r2 + 1);
-      tr = __ldg(r2 + 2);
-      tz2 = __ldg(r2 + 3);
+      const double4 ga = ld_v4_nc(rec + 8 * (size_t)r), gb = ld_v4_nc(rec + 8 * (size_t)r + 4);
+      g01 = make_double2(ga.x, ga.y);
+      g23 = make_double2(ga.z, ga.w);
+      tr = make_double2(gb.x, gb.y);
+      tz2 = make_double2(gb.z, gb.w);
       cx = __ldg(rcx + r);
     }
     // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  if ((maxrow && *maxrow > kPullRow) != PULL) return;
+  if ((maxrow && *maxrow > T.pull_row) != PULL) return;
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
