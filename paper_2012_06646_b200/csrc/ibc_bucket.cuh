@@ -36,6 +36,7 @@ constexpr int kChunk = kScanThreads * kScanItems;  // rows per scan CTA
 constexpr uint32_t kFlagAggregate = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
+constexpr int kBanks = 32;         // x banks of the spread sweep's bank mode (x cell mod 32)
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
@@ -235,19 +236,21 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
 // K4, rows up to kShortRow points: one thread per bucket slot ranks its
 // (key, index) among its row's pairs -- the row is read straight from the
 // bucket (contiguous, and shared by neighbouring lanes, so the loads are
-// L1 broadcasts) -- and writes the pair and its weight record at the row's
-// start + rank: stable (key, index) order.  Full warps whatever the row
-// lengths.
+// L1 broadcasts) -- and writes the pair at the row's start + rank: stable
+// (key, index) order.  Its weight record goes to the row's start + its rank
+// in (x bank, key, index) order, and the row's 32-entry bank table is
+// filled.  Full warps whatever the row lengths.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     const uint32_t* __restrict__ start, uint32_t n, const uint32_t* __restrict__ bkey,
     const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
-    double* __restrict__ rec, int* __restrict__ rcx) {
+    double* __restrict__ rec, int* __restrict__ rcx, uint32_t* __restrict__ rowbank,
+    const uint32_t* __restrict__ maxrow, uint32_t bank_rows) {
   const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
   if (o >= n) return;
   const uint32_t k = __ldg(bkey + o), ix = __ldg(bidx + o);
-  const uint32_t row = k / g.rowdiv;
+  const uint32_t row = k / g.rowdiv, base = row * g.rowdiv;
   const uint32_t a = __ldg(start + row), len = __ldg(start + row + 1) - a;
   if (len > (uint32_t)kShortRow) return;  // long rows: K4b
   // The point's position and value are gathered before the rank loop so
@@ -256,24 +259,55 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
 #pragma unroll
   for (int d = 0; d < D; ++d) x[d] = __ldg(X + (size_t)ix * D + d);
   const double gv = __ldg(G + ix);
-  uint32_t rk = 0, j = 0;
-  for (; j + 4 <= len; j += 4) {
-    uint32_t kj[4], ij[4];
+  // rk: rank in (key, index) order -- the sorted pairs.  When the sweep runs
+  // in bank mode (densest row <= bank_rows) the weight records go in (bank,
+  // key, index) order instead, bank = x cell mod 32, so that the sweep's
+  // lanes can take one bank each (ibc_spread.cuh); rb is that rank, lt the
+  // number of the row's points in lower banks, ceq the count in this bank.
+  const bool banked = *maxrow <= bank_rows;
+  const unsigned long long me = ((unsigned long long)k << 32) | ix;
+  uint32_t rk = 0, rbe = 0, lt = 0, ceq = 0;
+  if (!banked) {
+    uint32_t j = 0;
+    for (; j + 4 <= len; j += 4) {
+      unsigned long long c[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      kj[u] = __ldg(bkey + a + j + u);
-      ij[u] = __ldg(bidx + a + j + u);
+      for (int u = 0; u < 4; ++u)
+        c[u] = ((unsigned long long)__ldg(bkey + a + j + u) << 32) | __ldg(bidx + a + j + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) rk += c[u] < me ? 1u : 0u;
     }
+    for (; j < len; ++j)
+      rk += (((unsigned long long)__ldg(bkey + a + j) << 32) | __ldg(bidx + a + j)) < me ? 1u : 0u;
+  } else {
+    const uint32_t bk = (k - base) & 31u;
+    auto visit = [&](uint32_t kj, uint32_t ij) {
+      const uint32_t less = (((unsigned long long)kj << 32) | ij) < me ? 1u : 0u;
+      const uint32_t bj = (kj - base) & 31u;
+      rk += less;
+      lt += bj < bk ? 1u : 0u;
+      ceq += bj == bk ? 1u : 0u;
+      rbe += bj == bk ? less : 0u;
+    };
+    uint32_t j = 0;
+    for (; j + 4 <= len; j += 4) {
+      uint32_t kj[4], ij[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) rk += (kj[u] < k || (kj[u] == k && ij[u] < ix)) ? 1u : 0u;
-  }
-  for (; j < len; ++j) {
-    const uint32_t kj = __ldg(bkey + a + j), ij = __ldg(bidx + a + j);
-    rk += (kj < k || (kj == k && ij < ix)) ? 1u : 0u;
+      for (int u = 0; u < 4; ++u) {
+        kj[u] = __ldg(bkey + a + j + u);
+        ij[u] = __ldg(bidx + a + j + u);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) visit(kj[u], ij[u]);
+    }
+    for (; j < len; ++j) visit(__ldg(bkey + a + j), __ldg(bidx + a + j));
+    // Bank table of the row (zeroed beforehand): entry b = first record of
+    // bank b (relative) << 16 | its record count, written by the bank's first.
+    if (rbe == 0) rowbank[(size_t)row * kBanks + bk] = (lt << 16) | ceq;
   }
   skey[a + rk] = k;
   sidx[a + rk] = ix;
-  write_record_from<D>(g, x, gv, a + rk, rec, rcx);
+  write_record_from<D>(g, x, gv, a + (banked ? lt + rbe : rk), rec, rcx);
 }
 
 // K4b, long rows: one CTA per listed row, bitonic sort of (key << 32 | index)

@@ -50,6 +50,7 @@ struct PointScratch {
   DevBuf<uint32_t> rowstart;
   DevBuf<uint32_t> rowaux;  // bucket sort: row counts | scan status | ticket | long rows
   DevBuf<uint32_t> smap;    // bucket sort: sorted position -> record slot
+  DevBuf<uint32_t> rowbank; // bucket sort: per row, first record of each x bank (16)
   const uint32_t* maxrow = nullptr;  // bucket sort: largest row count (device)
   DevBuf<int> rec_cx;
   DevBuf<double> rec;         // 12 x cap weight records (spread)

@@ -616,6 +616,7 @@ void PointScratch::release_all() {
   hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
   smap.release();
+  rowbank.release();
   cap = 0;
 }
 
@@ -635,7 +636,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
   while (wpc > 1 && wpc * per_warp > 200 * 1024) --wpc;
   T.wpc = wpc;
   T.rl = rl;
-  T.pull_row = getenv("IBC_PULL_ROW") ? (uint32_t)atoi(getenv("IBC_PULL_ROW")) : sp::kPullRow;
+  T.pull_row = sp::pull_row();
   T.nyg = (ny + wpc - 1) / wpc;
   if (g.dim == 3) {
     const long per_sm = std::max<long>(1, std::min<long>(2048 / (32 * wpc), (227L * 1024) / (long)(wpc * per_warp)));
@@ -698,13 +699,13 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     // modes are launched when the densest row is only known on the device.
     const uint32_t* maxrow = (!radix) ? s.maxrow : nullptr;
     auto launch = [&](auto defer_k, auto pull_k) {
-      defer_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
-                                                s.rec_cx.p, d_out);
       if (maxrow) {
-        pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
-                                                 s.rec_cx.p, d_out);
+        defer_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
+                                                  s.rec_cx.p, s.rowbank.p, d_out);
         ++ctx.launches;
       }
+      pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
+                                               s.rec_cx.p, s.rowbank.p, d_out);
     };
     const int nx = g.n[0];
 #define IBC_SWEEP(D, RL) launch(sp::spread_sweep_kernel<D, RL, false>, sp::spread_sweep_kernel<D, RL, true>)
@@ -874,6 +875,8 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
+    s.rowbank.ensure((size_t)nrows * bucket::kBanks);
+    IBC_CUDA(cudaMemsetAsync(s.rowbank.p, 0, (size_t)nrows * bucket::kBanks * 4, st));
     bucket::scatter_pairs_kernel<<<blocks, bucket::kThreads, 0, st>>>(
         s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.keys[1].p, s.vals[1].p);
     static bool attr_set[64] = {};
@@ -888,7 +891,8 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
     auto sorts = [&](auto short_k, auto long_k) {
       short_k<<<blocks, bucket::kThreads, 0, st>>>(s.rowstart.p, (uint32_t)n, s.keys[1].p,
                                                    s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
-                                                   d_points, d_values, s.rec.p, s.rec_cx.p);
+                                                   d_points, d_values, s.rec.p, s.rec_cx.p,
+                                                   s.rowbank.p, maxrow, sp::pull_row());
       long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.keys[1].p,
                                                      s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
                                                      d_points, d_values, s.rec.p, s.rec_cx.p);

@@ -30,6 +30,7 @@
 // FMAs, deferral compaction is a popc binary search.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ibc_device.cuh"
@@ -38,7 +39,11 @@ namespace ibc {
 namespace sp {
 
 constexpr int kPadL = 4;  // padded x index xi = x + kPadL
-constexpr uint32_t kPullRow = 64;  // densest row above which batches pull instead of defer
+constexpr uint32_t kPullRow = 64;  // densest row above which batches pull instead of bank mode
+inline uint32_t pull_row() {  // IBC_PULL_ROW overrides (experiments)
+  static const uint32_t v = getenv("IBC_PULL_ROW") ? (uint32_t)atoi(getenv("IBC_PULL_ROW")) : kPullRow;
+  return v;
+}
 constexpr int kPadR = 2;
 
 struct SweepTiling {
@@ -49,100 +54,95 @@ struct SweepTiling {
   uint32_t pull_row;  // densest row above which batches pull instead of defer
 };
 
-__device__ __forceinline__ int skew(int xi) { return xi + (xi >> 4); }
+__device__ __forceinline__ int skew(int xi) { return xi; }
 
-// Doubles per window row for nx: padded, skewed, even.
+// Doubles per window row for nx: padded, even (16-byte aligned rows).
 __host__ __device__ constexpr int row_len(int nx) {
-  return ((nx + kPadL + kPadR) + ((nx + kPadL + kPadR) >> 4) + 1) +
-         (((nx + kPadL + kPadR) + ((nx + kPadL + kPadR) >> 4) + 1) & 1);
+  return (nx + kPadL + kPadR) + ((nx + kPadL + kPadR) & 1);
 }
 
-// Position of the n-th (0-based) set bit of m (popc(m) > n).
-__device__ __forceinline__ int nth_set(uint32_t m, int n) {
-  int pos = 0;
-#pragma unroll
-  for (int w = 16; w > 0; w >>= 1) {
-    const int c = __popc(m & ((1u << w) - 1u));
-    if (n >= c) {
-      n -= c;
-      m >>= w;
-      pos += w;
-    }
-  }
-  return pos;
-}
-
-// The batches of one source plane (see the file comment).  R >= 0: target
-// plane s + kz - 2 sits in slot (R + kz + 2) & 3 of a compile-time row length
-// RL and is inside the z-chunk; R < 0: runtime slot offsets so[kz] (-1 = skip).
+// Bank mode (sparse rows): one source plane.  Lane b owns x bank b (x cell
+// mod 32, up to a fixed shift) and walks that bank's records of the four
+// source rows in order (records are bank-ordered within a row, with a
+// 32-entry (first, count) bank table per row, ibc_bucket.cuh K4).  The cells of one
+// instruction's adds then differ mod 32: no two lanes share an address (even
+// across kx phases -- cells 16 apart), and within each half-warp the cells
+// differ mod 16, i.e. hit distinct bank pairs: conflict-free, no collision
+// test.  Lane j < 4 holds row j's sorted start rb, length len and row id rid.
 template <int D, int RL, int R>
-__device__ __forceinline__ void plane_batches(double* __restrict__ W, const int so[4], uint32_t e0,
-                                              uint32_t e1, uint32_t e2, uint32_t total,
-                                              uint32_t rstart, const uint32_t* __restrict__ smap,
-                                              const double* __restrict__ rec,
-                                              const int* __restrict__ rcx, double q) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t lt = (1u << lane) - 1u;
-  uint32_t next = 0;   // next unread position in the concatenated rows
-  int ndef = 0;        // deferred lanes carried into this batch
-  uint32_t p_def = 0;  // this lane's deferred position (lanes < ndef)
-  while (next < total || ndef > 0) {
-    const uint32_t p = lane < ndef ? p_def : next + (uint32_t)(lane - ndef);
-    const bool valid = lane < ndef || p < total;
-    const int j = (p >= e0) + (p >= e1) + (p >= e2);
-    const uint32_t rs = __shfl_sync(0xffffffffu, rstart, j & 3) + p;
-    int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
-    double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
-    if (valid) {
-      const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
-      const double4 ga = ld_v4_nc(rec + 8 * (size_t)r), gb = ld_v4_nc(rec + 8 * (size_t)r + 4);
-      g01 = make_double2(ga.x, ga.y);
-      g23 = make_double2(ga.z, ga.w);
-      tr = make_double2(gb.x, gb.y);
-      tz2 = make_double2(gb.z, gb.w);
-      cx = __ldg(rcx + r);
+__device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t rb,
+                                           uint32_t len, uint32_t rid,
+                                           const uint32_t* __restrict__ rowbank,
+                                           const double* __restrict__ rec,
+                                           const int* __restrict__ rcx, double q) {
+  const int bank = threadIdx.x & 31;
+  uint32_t lo[4], c[4], cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t rbj = __shfl_sync(0xffffffffu, rb, j), lenj = __shfl_sync(0xffffffffu, len, j);
+    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, j);
+    const uint32_t e = lenj ? __ldg(rowbank + (size_t)ridj * 32 + bank) : 0u;  // first << 16 | count
+    lo[j] = rbj + (e >> 16) - cnt;  // sorted position of this lane's k-th record = lo[j] + k
+    cnt += e & 0xffffu;
+    c[j] = cnt;
+  }
+  const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
+  auto pos = [&](uint32_t k) {
+    const int j = (k >= c[0]) + (k >= c[1]) + (k >= c[2]);
+    return (j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3]) + k;
+  };
+  // Records are prefetched one iteration ahead (the loop is latency-bound).
+  double4 ga = make_double4(0.0, 0.0, 0.0, 0.0), gb = ga;
+  int cx = 0;
+  if (cnt > 0) {
+    const uint32_t p = pos(0);
+    ga = ld_v4_nc(rec + 8 * (size_t)p);
+    gb = ld_v4_nc(rec + 8 * (size_t)p + 4);
+    cx = __ldg(rcx + p);
+  }
+  for (uint32_t k = 0; k < kmax; ++k) {
+    const bool valid = k < cnt;
+    const int j = (k >= c[0]) + (k >= c[1]) + (k >= c[2]);
+    double4 na = ga, nb = gb;
+    int ncx = cx;
+    if (k + 1 < cnt) {
+      const uint32_t p = pos(k + 1);
+      na = ld_v4_nc(rec + 8 * (size_t)p);
+      nb = ld_v4_nc(rec + 8 * (size_t)p + 4);
+      ncx = __ldg(rcx + p);
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, cx);  // every lane takes part
-    const bool on = valid && (peers & lt) == 0u;
-    // Compact the deferred lanes (same cx as an earlier lane) to the front.
-    const uint32_t defm = __ballot_sync(0xffffffffu, valid && !on);
-    const int newdef = __popc(defm);
-    if (newdef) {
-      const uint32_t pd = __shfl_sync(0xffffffffu, p, lane < newdef ? nth_set(defm, lane) : 0);
-      if (lane < newdef) p_def = pd;
-    }
-    next = min(total, next + (uint32_t)(32 - ndef));
-    ndef = newdef;
     // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
-    const double vy = (j & 1) ? tr.x : tr.y;
+    const double vy = (j & 1) ? gb.x : gb.y;
     const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
     double a[4];
     if (D == 3) {
-      a[0] = fma(-wq, tz2.y, wq);
-      a[1] = fma(wq, tz2.x, wq);
-      a[2] = fma(wq, tz2.y, wq);
-      a[3] = fma(-wq, tz2.x, wq);
+      a[0] = fma(-wq, gb.w, wq);
+      a[1] = fma(wq, gb.z, wq);
+      a[2] = fma(wq, gb.w, wq);
+      a[3] = fma(-wq, gb.z, wq);
     } else {
       a[0] = a[1] = a[3] = 0.0;
       a[2] = wq / q;
     }
-    const double gk[4] = {g01.x, g01.y, g23.x, g23.y};
-    const int xb = cx + (kPadL - 2);
+    const double gk[4] = {ga.x, ga.y, ga.z, ga.w};
+    double* wa = W + (cx + (kPadL - 2));
 #pragma unroll
     for (int kx = 0; kx < 4; ++kx) {
-      if (on) {
-        double* wa = W + skew(xb + kx);
-        if (R >= 0) {
+      if (valid) {
+        if (R >= 0) {  // interior plane: slot offsets are immediates
 #pragma unroll
-          for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * RL] += gk[kx] * a[kz];
+          for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * RL + kx] += gk[kx] * a[kz];
         } else {
 #pragma unroll
           for (int kz = 0; kz < 4; ++kz)
-            if (so[kz] >= 0) wa[so[kz]] += gk[kx] * a[kz];
+            if (so[kz] >= 0) wa[so[kz] + kx] += gk[kx] * a[kz];
         }
       }
       __syncwarp();
     }
+    ga = na;
+    gb = nb;
+    cx = ncx;
   }
 }
 
@@ -244,9 +244,11 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
                                                            const uint32_t* __restrict__ smap,
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
+                                                           const uint32_t* __restrict__ rowbank,
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  if ((maxrow && *maxrow > T.pull_row) != PULL) return;
+  // Bank mode needs the bucket sort's bank-ordered records (maxrow given).
+  if ((!maxrow || *maxrow > T.pull_row) != PULL) return;
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -267,9 +269,10 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
 
   // Lane j < 4: sorted range of source row cy = ty + 2 - j (sigma_y = j - 2)
   // of source plane s; the next plane's ranges are loaded while this one runs.
-  auto ranges = [&](int s, uint32_t& rb, uint32_t& len) {
+  auto ranges = [&](int s, uint32_t& rb, uint32_t& len, uint32_t& rid) {
     rb = 0;
     len = 0;
+    rid = 0;
     const bool zok = D != 3 || pz || (s >= -1 && s <= nz);
     if (lane < 4 && zok && s <= s_hi) {
       const int szw = D == 3 ? (pz ? wrap_cell(s, nz) : s) : 0;
@@ -278,18 +281,18 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
       if (py) cy = wrap_cell(cy, ny);
       else ok = cy >= -1 && cy <= ny;
       if (ok) {
-        const uint32_t rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
+        rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
         rb = __ldg(rowstart + rid);
         len = __ldg(rowstart + rid + 1) - rb;
       }
     }
   };
-  uint32_t rb_n, len_n;
-  ranges(s_lo, rb_n, len_n);
+  uint32_t rb_n, len_n, rid_n;
+  ranges(s_lo, rb_n, len_n, rid_n);
 
   for (int s = s_lo; s <= s_hi; ++s) {
-    const uint32_t rb = rb_n, len = len_n;
-    ranges(s + 1, rb_n, len_n);
+    const uint32_t rb = rb_n, len = len_n, rid = rid_n;
+    ranges(s + 1, rb_n, len_n, rid_n);
     {
       // Window slot offset of target plane s + kz - 2 (-1: outside [z0, z1)).
       int so[4];
@@ -298,27 +301,40 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
         const int tz = s + kz - 2;
         so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * rl : -1) : (kz == 2 ? 0 : -1);
       }
-      uint32_t incl = len;
-#pragma unroll
-      for (int o = 1; o < 4; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-      }
-      const uint32_t e0 = __shfl_sync(0xffffffffu, incl, 0), e1 = __shfl_sync(0xffffffffu, incl, 1);
-      const uint32_t e2 = __shfl_sync(0xffffffffu, incl, 2), total = __shfl_sync(0xffffffffu, incl, 3);
-      const uint32_t rstart = rb - (incl - len);  // sorted index = rstart_j + p
-      // Interior planes with a compile-time row length take the static path:
-      // slot offsets are immediates, no per-add range checks.
       const bool interior = D == 3 && s - 2 >= z0 && s + 1 < z1;
-      if (RL > 0 && interior) {
-        switch (s & 3) {
-          case 0: if (PULL) plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-          case 1: if (PULL) plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-          case 2: if (PULL) plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-          default: if (PULL) plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+      if (!PULL) {
+        if (RL > 0 && interior) {
+          switch (s & 3) {
+            case 0: plane_banks<D, RL, 0>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+            case 1: plane_banks<D, RL, 1>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+            case 2: plane_banks<D, RL, 2>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+            default: plane_banks<D, RL, 3>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+          }
+        } else {
+          plane_banks<D, RL, -1>(W, so, rb, len, rid, rowbank, rec, rcx, q);
         }
       } else {
-        if (PULL) plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); else plane_batches<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q);
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t e0 = __shfl_sync(0xffffffffu, incl, 0), e1 = __shfl_sync(0xffffffffu, incl, 1);
+        const uint32_t e2 = __shfl_sync(0xffffffffu, incl, 2), total = __shfl_sync(0xffffffffu, incl, 3);
+        const uint32_t rstart = rb - (incl - len);  // sorted index = rstart_j + p
+        // Interior planes with a compile-time row length take the static
+        // path: slot offsets are immediates, no per-add range checks.
+        if (RL > 0 && interior) {
+          switch (s & 3) {
+            case 0: plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+            case 1: plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+            case 2: plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+            default: plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+          }
+        } else {
+          plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q);
+        }
       }
     }
     // Target plane s - 2 has all its sources: fold, store once, clear.
