@@ -40,6 +40,10 @@ constexpr int kBanks = 32;         // x banks of the spread sweep's bank mode (x
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
+// Points per thread of the one-pass kernels K1/K3: their loads, atomics and
+// stores are issued for kPer points at once (they are latency-bound chains).
+constexpr int kPer = 1;
+
 // Cell key of every point (or just its row when full_key == 0), its arrival
 // rank in its row, and the per-row counts.
 template <int D>
@@ -48,21 +52,39 @@ __global__ void __launch_bounds__(kThreads) keys_kernel(DevGrid g, const double*
                                                         uint32_t* __restrict__ keys,
                                                         uint32_t* __restrict__ rank,
                                                         uint32_t* __restrict__ count) {
-  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  if (i >= n) return;
-  uint64_t k = 0;
+  const uint32_t i0 = blockIdx.x * (kThreads * kPer) + threadIdx.x;
+  double x[kPer][D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    if (a == 0 && !full_key) continue;
-    double xw;
-    int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
-    if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
-    k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = i0 + u * kThreads;
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
   }
-  const uint32_t key = (uint32_t)k;
-  const uint32_t row = key / g.rowdiv;
-  keys[i] = full_key ? key : row;
-  rank[i] = atomicAdd(count + row, 1u);
+  uint32_t key[kPer], rk[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    uint64_t k = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      if (a == 0 && !full_key) continue;
+      double xw;
+      int c = cell_of(g, a, x[u][a], &xw);
+      if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
+      k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
+    }
+    key[u] = (uint32_t)k;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u)
+    if (i0 + u * kThreads < n) rk[u] = atomicAdd(count + key[u] / g.rowdiv, 1u);
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = i0 + u * kThreads;
+    if (i < n) {
+      keys[i] = full_key ? key[u] : key[u] / g.rowdiv;
+      rank[i] = rk[u];
+    }
+  }
 }
 
 __device__ __forceinline__ void st_flag(uint32_t* p, uint32_t v) {
@@ -168,35 +190,58 @@ __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
     DevGrid g, const double* __restrict__ X, const uint32_t* __restrict__ rows,
     const uint32_t* __restrict__ rank, uint32_t n, const uint32_t* __restrict__ start,
     double* __restrict__ rec) {
-  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t slot = __ldg(start + __ldg(rows + i)) + __ldg(rank + i);
-  double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};
-  int c[3] = {0, 0, 0};
+  const uint32_t i0 = blockIdx.x * (kThreads * kPer) + threadIdx.x;
+  uint32_t slot[kPer];
+  double x[kPer][D];
 #pragma unroll
-  for (int a = 0; a < D; ++a) {
-    double u;
-    c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &u);
-    sincos_half_pi(u, &tr[a][0], &tr[a][1]);
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = i0 + u * kThreads;
+    slot[u] = i < n ? __ldg(start + __ldg(rows + i)) + __ldg(rank + i) : 0u;
+#pragma unroll
+    for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
   }
-  double* r = rec + 8 * (size_t)slot;
-  st_v4(r, tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
-  st_v4(r + 4, tr[2][0], tr[2][1], __longlong_as_double(((long long)c[0] << 32) | i),
-        __longlong_as_double((long long)(uint32_t)c[1]));
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = i0 + u * kThreads;
+    double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};
+    int c[3] = {0, 0, 0};
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+      double w;
+      c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, x[u][a], &w);
+      sincos_half_pi(w, &tr[a][0], &tr[a][1]);
+    }
+    if (i < n) {
+      double* r = rec + 8 * (size_t)slot[u];
+      st_v4(r, tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
+      st_v4(r + 4, tr[2][0], tr[2][1], __longlong_as_double(((long long)c[0] << 32) | i),
+            __longlong_as_double((long long)(uint32_t)c[1]));
+    }
+  }
 }
 
-// K3, spread: (key, index) at row start + rank (the rows' stable order comes
-// from K4; the weight records are then written in that order by K5).
+// K3, spread: the (key << 32 | index) pair at row start + rank (the rows'
+// stable order comes from K4, which also writes the weight records).
 __global__ void __launch_bounds__(kThreads) scatter_pairs_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
-    uint32_t rowdiv, const uint32_t* __restrict__ start, uint32_t* __restrict__ bkey,
-    uint32_t* __restrict__ bidx) {
-  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
-  if (i >= n) return;
-  const uint32_t key = __ldg(keys + i);
-  const uint32_t slot = __ldg(start + key / rowdiv) + __ldg(rank + i);
-  bkey[slot] = key;
-  bidx[slot] = i;
+    uint32_t rowdiv, const uint32_t* __restrict__ start, unsigned long long* __restrict__ bpair) {
+  const uint32_t i0 = blockIdx.x * (kThreads * kPer) + threadIdx.x;
+  uint32_t key[kPer], rk[kPer], slot[kPer];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = i0 + u * kThreads;
+    key[u] = i < n ? __ldg(keys + i) : 0u;
+    rk[u] = i < n ? __ldg(rank + i) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) slot[u] = __ldg(start + key[u] / rowdiv) + rk[u];
+#pragma unroll
+  for (int u = 0; u < kPer; ++u) {
+    const uint32_t i = i0 + u * kThreads;
+    if (i < n) {
+      bpair[slot[u]] = ((unsigned long long)key[u] << 32) | i;  // one sector write per point
+    }
+  }
 }
 
 // The spread's 64-byte weight record of point i at sorted position o:
@@ -242,14 +287,15 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
 // filled.  Full warps whatever the row lengths.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
-    const uint32_t* __restrict__ start, uint32_t n, const uint32_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
+    const uint32_t* __restrict__ start, uint32_t n, const unsigned long long* __restrict__ bpair,
+    uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
     double* __restrict__ rec, int* __restrict__ rcx, uint32_t* __restrict__ rowbank,
     const uint32_t* __restrict__ maxrow, uint32_t bank_rows) {
   const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
   if (o >= n) return;
-  const uint32_t k = __ldg(bkey + o), ix = __ldg(bidx + o);
+  const unsigned long long me = __ldg(bpair + o);
+  const uint32_t k = (uint32_t)(me >> 32), ix = (uint32_t)me;
   const uint32_t row = k / g.rowdiv, base = row * g.rowdiv;
   const uint32_t a = __ldg(start + row), len = __ldg(start + row + 1) - a;
   if (len > (uint32_t)kShortRow) return;  // long rows: K4b
@@ -265,25 +311,23 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
   // lanes can take one bank each (ibc_spread.cuh); rb is that rank, lt the
   // number of the row's points in lower banks, ceq the count in this bank.
   const bool banked = *maxrow <= bank_rows;
-  const unsigned long long me = ((unsigned long long)k << 32) | ix;
   uint32_t rk = 0, rbe = 0, lt = 0, ceq = 0;
   if (!banked) {
     uint32_t j = 0;
     for (; j + 4 <= len; j += 4) {
       unsigned long long c[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        c[u] = ((unsigned long long)__ldg(bkey + a + j + u) << 32) | __ldg(bidx + a + j + u);
+      for (int u = 0; u < 4; ++u) c[u] = __ldg(bpair + a + j + u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) rk += c[u] < me ? 1u : 0u;
     }
     for (; j < len; ++j)
-      rk += (((unsigned long long)__ldg(bkey + a + j) << 32) | __ldg(bidx + a + j)) < me ? 1u : 0u;
+      rk += __ldg(bpair + a + j) < me ? 1u : 0u;
   } else {
     const uint32_t bk = (k - base) & 31u;
-    auto visit = [&](uint32_t kj, uint32_t ij) {
-      const uint32_t less = (((unsigned long long)kj << 32) | ij) < me ? 1u : 0u;
-      const uint32_t bj = (kj - base) & 31u;
+    auto visit = [&](unsigned long long cj) {
+      const uint32_t less = cj < me ? 1u : 0u;
+      const uint32_t bj = ((uint32_t)(cj >> 32) - base) & 31u;
       rk += less;
       lt += bj < bk ? 1u : 0u;
       ceq += bj == bk ? 1u : 0u;
@@ -291,16 +335,13 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     };
     uint32_t j = 0;
     for (; j + 4 <= len; j += 4) {
-      uint32_t kj[4], ij[4];
+      unsigned long long c[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        kj[u] = __ldg(bkey + a + j + u);
-        ij[u] = __ldg(bidx + a + j + u);
-      }
+      for (int u = 0; u < 4; ++u) c[u] = __ldg(bpair + a + j + u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) visit(kj[u], ij[u]);
+      for (int u = 0; u < 4; ++u) visit(c[u]);
     }
-    for (; j < len; ++j) visit(__ldg(bkey + a + j), __ldg(bidx + a + j));
+    for (; j < len; ++j) visit(__ldg(bpair + a + j));
     // Bank table of the row (zeroed beforehand): entry b = first record of
     // bank b (relative) << 16 | its record count, written by the bank's first.
     if (rbe == 0) rowbank[(size_t)row * kBanks + bk] = (lt << 16) | ceq;
@@ -316,8 +357,8 @@ constexpr int kLongThreads = 1024;
 template <int D>
 __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     const uint32_t* __restrict__ start, const uint32_t* __restrict__ long_rows,
-    const uint32_t* __restrict__ nlong, const uint32_t* __restrict__ bkey,
-    const uint32_t* __restrict__ bidx, uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
+    const uint32_t* __restrict__ nlong, const unsigned long long* __restrict__ bpair,
+    uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
     double* __restrict__ rec, int* __restrict__ rcx) {
   extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
@@ -329,7 +370,7 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
       uint32_t m = 1;
       while (m < len) m <<= 1;
       for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
-        sk[e] = e < len ? ((unsigned long long)bkey[a + e] << 32) | bidx[a + e] : ~0ull;
+        sk[e] = e < len ? bpair[a + e] : ~0ull;
       }
       __syncthreads();
       for (uint32_t size = 2; size <= m; size <<= 1) {
@@ -357,10 +398,10 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     } else {
       // Very long row: rank every element by counting (correct, quadratic).
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
-        const unsigned long long ce = ((unsigned long long)bkey[a + e] << 32) | bidx[a + e];
+        const unsigned long long ce = bpair[a + e];
         uint32_t rk = 0;
         for (uint32_t f = 0; f < len; ++f)
-          rk += (((unsigned long long)bkey[a + f] << 32) | bidx[a + f]) < ce ? 1u : 0u;
+          rk += bpair[a + f] < ce ? 1u : 0u;
         skey[a + rk] = (uint32_t)(ce >> 32);
         sidx[a + rk] = (uint32_t)ce;
         write_record<D>(g, X, G, (uint32_t)ce, a + rk, rec, rcx);

@@ -50,7 +50,8 @@ struct PointScratch {
   DevBuf<uint32_t> rowstart;
   DevBuf<uint32_t> rowaux;  // bucket sort: row counts | scan status | ticket | long rows
   DevBuf<uint32_t> smap;    // bucket sort: sorted position -> record slot
-  DevBuf<uint32_t> rowbank; // bucket sort: per row, first record of each x bank (16)
+  DevBuf<uint32_t> rowbank; // bucket sort: per row and x bank, first record << 16 | count
+  DevBuf<unsigned long long> bpair;  // bucket sort: (key << 32 | index) in row buckets
   const uint32_t* maxrow = nullptr;  // bucket sort: largest row count (device)
   DevBuf<int> rec_cx;
   DevBuf<double> rec;         // 12 x cap weight records (spread)

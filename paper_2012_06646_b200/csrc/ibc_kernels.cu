@@ -617,6 +617,7 @@ void PointScratch::release_all() {
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
   smap.release();
   rowbank.release();
+  bpair.release();
   cap = 0;
 }
 
@@ -849,15 +850,16 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
   const unsigned blocks = grid_for(n, bucket::kThreads);
+  const unsigned pblocks = grid_for(n, bucket::kThreads * bucket::kPer);  // K1 / K3
   const int full = spread ? 1 : 0;
   if (g.dim == 3)
-    bucket::keys_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
+    bucket::keys_kernel<3><<<pblocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
                                                                 s.keys[0].p, s.vals[0].p, count);
   else if (g.dim == 2)
-    bucket::keys_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
+    bucket::keys_kernel<2><<<pblocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
                                                                 s.keys[0].p, s.vals[0].p, count);
   else
-    bucket::keys_kernel<1><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
+    bucket::keys_kernel<1><<<pblocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
                                                                 s.keys[0].p, s.vals[0].p, count);
   ctx.prof_end(kProfKeys, ev);
   ctx.prof_begin(kProfSort, &ev);
@@ -867,18 +869,19 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   ctx.launches += 2;
   if (!spread) {
     if (g.dim == 3)
-      bucket::scatter_interp_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
+      bucket::scatter_interp_kernel<3><<<pblocks, bucket::kThreads, 0, st>>>(
           g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     else
-      bucket::scatter_interp_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
+      bucket::scatter_interp_kernel<2><<<pblocks, bucket::kThreads, 0, st>>>(
           g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
     s.rowbank.ensure((size_t)nrows * bucket::kBanks);
+    s.bpair.ensure(n);
     IBC_CUDA(cudaMemsetAsync(s.rowbank.p, 0, (size_t)nrows * bucket::kBanks * 4, st));
-    bucket::scatter_pairs_kernel<<<blocks, bucket::kThreads, 0, st>>>(
-        s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.keys[1].p, s.vals[1].p);
+    bucket::scatter_pairs_kernel<<<pblocks, bucket::kThreads, 0, st>>>(
+        s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.bpair.p);
     static bool attr_set[64] = {};
     const size_t lsm = (size_t)bucket::kLongSortMax * 8;
     if (!attr_set[ctx.device & 63]) {
@@ -889,12 +892,12 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
       attr_set[ctx.device & 63] = true;
     }
     auto sorts = [&](auto short_k, auto long_k) {
-      short_k<<<blocks, bucket::kThreads, 0, st>>>(s.rowstart.p, (uint32_t)n, s.keys[1].p,
-                                                   s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
+      short_k<<<blocks, bucket::kThreads, 0, st>>>(s.rowstart.p, (uint32_t)n, s.bpair.p,
+                                                   s.keys[0].p, s.vals[0].p, g,
                                                    d_points, d_values, s.rec.p, s.rec_cx.p,
                                                    s.rowbank.p, maxrow, sp::pull_row());
-      long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.keys[1].p,
-                                                     s.vals[1].p, s.keys[0].p, s.vals[0].p, g,
+      long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.bpair.p,
+                                                     s.keys[0].p, s.vals[0].p, g,
                                                      d_points, d_values, s.rec.p, s.rec_cx.p);
     };
     if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
