@@ -36,7 +36,7 @@ constexpr int kChunk = kScanThreads * kScanItems;  // rows per scan CTA
 constexpr uint32_t kFlagAggregate = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
-constexpr int kBanks = 32;         // x banks of the spread sweep's bank mode (x cell mod 32)
+constexpr int kBanks = 16;         // x banks of the spread sweep's bank mode (x cell mod 16)
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
@@ -283,7 +283,7 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
 // bucket (contiguous, and shared by neighbouring lanes, so the loads are
 // L1 broadcasts) -- and writes the pair at the row's start + rank: stable
 // (key, index) order.  Its weight record goes to the row's start + its rank
-// in (x bank, key, index) order, and the row's 32-entry bank table is
+// in (x bank, key, index) order, and the row's 16-entry bank table is
 // filled.  Full warps whatever the row lengths.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
@@ -307,7 +307,7 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
   const double gv = __ldg(G + ix);
   // rk: rank in (key, index) order -- the sorted pairs.  When the sweep runs
   // in bank mode (densest row <= bank_rows) the weight records go in (bank,
-  // key, index) order instead, bank = x cell mod 32, so that the sweep's
+  // key, index) order instead, bank = x cell mod 16, so that the sweep's
   // lanes can take one bank each (ibc_spread.cuh); rb is that rank, lt the
   // number of the row's points in lower banks, ceq the count in this bank.
   const bool banked = *maxrow <= bank_rows;
@@ -324,10 +324,10 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     for (; j < len; ++j)
       rk += __ldg(bpair + a + j) < me ? 1u : 0u;
   } else {
-    const uint32_t bk = (k - base) & 31u;
+    const uint32_t bk = (k - base) & (kBanks - 1);
     auto visit = [&](unsigned long long cj) {
       const uint32_t less = cj < me ? 1u : 0u;
-      const uint32_t bj = ((uint32_t)(cj >> 32) - base) & 31u;
+      const uint32_t bj = ((uint32_t)(cj >> 32) - base) & (kBanks - 1);
       rk += less;
       lt += bj < bk ? 1u : 0u;
       ceq += bj == bk ? 1u : 0u;

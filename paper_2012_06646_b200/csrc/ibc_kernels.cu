@@ -626,21 +626,26 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
                    size_t n, PointScratch& s, bool spread);
 
 // Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
-bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
+// rows_per_warp = 1: pull mode (wpc warps per CTA, one target row each);
+// 2: bank mode (one warp per CTA, a target row per half-warp).
+bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
   if (g.dim < 2) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int rl = sp::row_len(nx);
   const int slots = g.dim == 3 ? 4 : 1;
-  const size_t per_warp = (size_t)slots * rl * sizeof(double);
+  const size_t per_warp = (size_t)rows_per_warp * slots * rl * sizeof(double);
   if (per_warp > 200 * 1024) return false;
-  int wpc = 8;
+  int wpc = rows_per_warp == 1 ? 8 : 1;
   while (wpc > 1 && wpc * per_warp > 200 * 1024) --wpc;
   T.wpc = wpc;
   T.rl = rl;
   T.pull_row = sp::pull_row();
-  T.nyg = (ny + wpc - 1) / wpc;
+  const int rows_per_cta = wpc * rows_per_warp;
+  T.nyg = (ny + rows_per_cta - 1) / rows_per_cta;
   if (g.dim == 3) {
-    const long per_sm = std::max<long>(1, std::min<long>(2048 / (32 * wpc), (227L * 1024) / (long)(wpc * per_warp)));
+    const long max_warps = rows_per_warp == 1 ? 2048 / 32 : 16;  // bank mode: __launch_bounds__(32)
+    const long per_sm = std::max<long>(
+        1, std::min<long>(std::min<long>(max_warps / wpc, 32), (227L * 1024) / (long)(wpc * per_warp)));
     const long chunks = std::max<long>(1, (148L * per_sm) / T.nyg);
     T.zc = (int)std::max<long>(1, (nz + chunks - 1) / chunks);
     T.nzc = (nz + T.zc - 1) / T.zc;
@@ -654,8 +659,8 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T) {
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
-  sp::SweepTiling W;
-  const bool sweep = sweep_tiling(g, W);
+  sp::SweepTiling W, WB;  // pull mode, bank mode
+  const bool sweep = sweep_tiling(g, W, 1) && sweep_tiling(g, WB, 2);
   const bool radix = getenv("IBC_SORT") && std::string(getenv("IBC_SORT")) == "radix";
   if (sweep && !radix) {
     bucket_points(ctx, g, d_points, d_values, n, s, true);
@@ -679,42 +684,43 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
     for (const void* k :
-         {(const void*)sp::spread_sweep_kernel<2, 0, false>, (const void*)sp::spread_sweep_kernel<2, 0, true>,
-          (const void*)sp::spread_sweep_kernel<3, 0, false>, (const void*)sp::spread_sweep_kernel<3, 0, true>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64), false>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64), true>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128), false>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128), true>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256), false>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256), true>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512), false>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512), true>})
+         {(const void*)sp::spread_sweep_kernel<2, 0>, (const void*)sp::spread_banks_kernel<2, 0>,
+          (const void*)sp::spread_sweep_kernel<3, 0>, (const void*)sp::spread_banks_kernel<3, 0>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64)>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(64)>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128)>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(128)>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256)>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(256)>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512)>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(512)>})
       IBC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[ctx.device & 63] = true;
   }
   if (sweep) {
     ctx.prof_begin(kProfSpread, &ev);
     const size_t smem = (size_t)W.wpc * (g.dim == 3 ? 4 : 1) * W.rl * sizeof(double);
-    const unsigned blocks = (unsigned)(W.nyg * W.nzc);
-    // Compile-time window row length for the common x extents; both batch
-    // modes are launched when the densest row is only known on the device.
+    const size_t smem_b = (size_t)2 * WB.wpc * (g.dim == 3 ? 4 : 1) * WB.rl * sizeof(double);
+    const unsigned blocks = (unsigned)(W.nyg * W.nzc), blocks_b = (unsigned)(WB.nyg * WB.nzc);
+    // Compile-time window row length for the common x extents; both modes
+    // are launched when the densest row is only known on the device.
     const uint32_t* maxrow = (!radix) ? s.maxrow : nullptr;
-    auto launch = [&](auto defer_k, auto pull_k) {
+    auto launch = [&](auto bank_k, auto pull_k) {
       if (maxrow) {
-        defer_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
-                                                  s.rec_cx.p, s.rowbank.p, d_out);
+        bank_k<<<blocks_b, 32 * WB.wpc, smem_b, st>>>(g, WB, maxrow, s.rowstart.p, s.rec.p,
+                                                      s.rec_cx.p, s.rowbank.p, d_out);
         ++ctx.launches;
       }
       pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
-                                               s.rec_cx.p, s.rowbank.p, d_out);
+                                               s.rec_cx.p, d_out);
     };
     const int nx = g.n[0];
-#define IBC_SWEEP(D, RL) launch(sp::spread_sweep_kernel<D, RL, false>, sp::spread_sweep_kernel<D, RL, true>)
+#define IBC_SWEEP(D, RL) launch(sp::spread_banks_kernel<D, RL>, sp::spread_sweep_kernel<D, RL>)
     if (g.dim == 3) {
-      if (W.rl == sp::row_len(64) && nx == 64) IBC_SWEEP(3, sp::row_len(64));
-      else if (W.rl == sp::row_len(128) && nx == 128) IBC_SWEEP(3, sp::row_len(128));
-      else if (W.rl == sp::row_len(256) && nx == 256) IBC_SWEEP(3, sp::row_len(256));
-      else if (W.rl == sp::row_len(512) && nx == 512) IBC_SWEEP(3, sp::row_len(512));
+      if (nx == 64) IBC_SWEEP(3, sp::row_len(64));
+      else if (nx == 128) IBC_SWEEP(3, sp::row_len(128));
+      else if (nx == 256) IBC_SWEEP(3, sp::row_len(256));
+      else if (nx == 512) IBC_SWEEP(3, sp::row_len(512));
       else IBC_SWEEP(3, 0);
     } else {
       IBC_SWEEP(2, 0);

@@ -61,27 +61,30 @@ __host__ __device__ constexpr int row_len(int nx) {
   return (nx + kPadL + kPadR) + ((nx + kPadL + kPadR) & 1);
 }
 
-// Bank mode (sparse rows): one source plane.  Lane b owns x bank b (x cell
-// mod 32, up to a fixed shift) and walks that bank's records of the four
+// Bank mode (sparse rows): one source plane for the two target rows of a
+// warp, one per half-warp.  In each half, lane b owns x bank b (x cell mod
+// 16, up to a fixed shift) and walks that bank's records of the half's four
 // source rows in order (records are bank-ordered within a row, with a
-// 32-entry (first, count) bank table per row, ibc_bucket.cuh K4).  The cells of one
-// instruction's adds then differ mod 32: no two lanes share an address (even
-// across kx phases -- cells 16 apart), and within each half-warp the cells
-// differ mod 16, i.e. hit distinct bank pairs: conflict-free, no collision
-// test.  Lane j < 4 holds row j's sorted start rb, length len and row id rid.
+// 16-entry (first, count) table per row, ibc_bucket.cuh K4).  The cells of
+// one instruction's adds then differ mod 16 within a half -- distinct bank
+// pairs, and distinct addresses even across kx phases of one point -- and the
+// halves write different windows: conflict-free, no collision test.  Lane
+// 16h + j (j < 4) holds row j's sorted start rb, length len and row id rid
+// for half h.
 template <int D, int RL, int R>
 __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t rb,
                                            uint32_t len, uint32_t rid,
                                            const uint32_t* __restrict__ rowbank,
                                            const double* __restrict__ rec,
                                            const int* __restrict__ rcx, double q) {
-  const int bank = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, bank = lane & 15, hb = lane & 16;
   uint32_t lo[4], c[4], cnt = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t rbj = __shfl_sync(0xffffffffu, rb, j), lenj = __shfl_sync(0xffffffffu, len, j);
-    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, j);
-    const uint32_t e = lenj ? __ldg(rowbank + (size_t)ridj * 32 + bank) : 0u;  // first << 16 | count
+    const uint32_t rbj = __shfl_sync(0xffffffffu, rb, hb + j);
+    const uint32_t lenj = __shfl_sync(0xffffffffu, len, hb + j);
+    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, hb + j);
+    const uint32_t e = lenj ? __ldg(rowbank + (size_t)ridj * 16 + bank) : 0u;  // first << 16 | count
     lo[j] = rbj + (e >> 16) - cnt;  // sorted position of this lane's k-th record = lo[j] + k
     cnt += e & 0xffffu;
     c[j] = cnt;
@@ -232,23 +235,21 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
   }
 }
 
-// PULL = false: colliding lanes are deferred to the next batch (few
-// collisions: sparse points).  PULL = true: colliding lanes are summed into
-// their group leader by shuffles (dense or clustered points, where deferral
-// would serialise).  Both are launched; the one that does not match the
+// Pull mode (dense or clustered rows, or records not bank-ordered): one warp
+// per target row, batches of 32 consecutive records of the four source rows;
+// lanes with the same home cx are summed into their group leader by shuffles.
+// Launched next to the bank-mode kernel; the one that does not match the
 // densest row seen by the row scan (*maxrow) returns at once.
-template <int D, int RL, bool PULL>
+template <int D, int RL>
 __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTiling T,
                                                            const uint32_t* __restrict__ maxrow,
                                                            const uint32_t* __restrict__ rowstart,
                                                            const uint32_t* __restrict__ smap,
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
-                                                           const uint32_t* __restrict__ rowbank,
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  // Bank mode needs the bucket sort's bank-ordered records (maxrow given).
-  if ((!maxrow || *maxrow > T.pull_row) != PULL) return;
+  if (maxrow && *maxrow <= T.pull_row) return;  // bank mode
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -291,7 +292,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
   ranges(s_lo, rb_n, len_n, rid_n);
 
   for (int s = s_lo; s <= s_hi; ++s) {
-    const uint32_t rb = rb_n, len = len_n, rid = rid_n;
+    const uint32_t rb = rb_n, len = len_n;
     ranges(s + 1, rb_n, len_n, rid_n);
     {
       // Window slot offset of target plane s + kz - 2 (-1: outside [z0, z1)).
@@ -302,18 +303,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
         so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * rl : -1) : (kz == 2 ? 0 : -1);
       }
       const bool interior = D == 3 && s - 2 >= z0 && s + 1 < z1;
-      if (!PULL) {
-        if (RL > 0 && interior) {
-          switch (s & 3) {
-            case 0: plane_banks<D, RL, 0>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-            case 1: plane_banks<D, RL, 1>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-            case 2: plane_banks<D, RL, 2>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-            default: plane_banks<D, RL, 3>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-          }
-        } else {
-          plane_banks<D, RL, -1>(W, so, rb, len, rid, rowbank, rec, rcx, q);
-        }
-      } else {
+      {
         uint32_t incl = len;
 #pragma unroll
         for (int o = 1; o < 4; o <<= 1) {
@@ -362,6 +352,113 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
       __syncwarp();
       double2* Z = reinterpret_cast<double2*>(Wr);
       for (int i = lane; i < rl / 2; i += 32) Z[i] = make_double2(0.0, 0.0);
+      __syncwarp();
+    }
+  }
+}
+
+
+// Bank mode (sparse rows, densest row <= T.pull_row): one warp per pair of
+// target rows (one per half-warp), z-sweep as above, plane_banks per source
+// plane.  Window: two rows x four slots per warp.
+template <int D, int RL>
+__global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling T,
+                                                          const uint32_t* __restrict__ maxrow,
+                                                          const uint32_t* __restrict__ rowstart,
+                                                          const double* __restrict__ rec,
+                                                          const int* __restrict__ rcx,
+                                                          const uint32_t* __restrict__ rowbank,
+                                                          double* __restrict__ out) {
+  extern __shared__ __align__(16) double win[];
+  if (*maxrow > T.pull_row) return;  // pull mode
+  constexpr int kSlots = D == 3 ? 4 : 1;
+  const int rl = RL > 0 ? RL : T.rl;
+  const int lane = threadIdx.x & 31, hl = lane & 15, h = lane >> 4;
+  const int nx = g.n[0], ny = g.n[1], nz = D == 3 ? g.n[2] : 1;
+  const int yg = blockIdx.x % T.nyg, zi = blockIdx.x / T.nyg;
+  const int ty = 2 * yg + h;  // this half's target row
+  const bool row_ok = ty < ny;
+  const int z0 = D == 3 ? zi * T.zc : 0;
+  const int z1 = D == 3 ? min(z0 + T.zc, nz) : 1;
+  double* W = win + (size_t)h * kSlots * rl;
+  for (int i = lane; i < 2 * kSlots * rl; i += 32) win[i] = 0.0;
+  __syncwarp();
+
+  const bool px = g.periodic[0] != 0, py = g.periodic[1] != 0;
+  const bool pz = D == 3 && g.periodic[2] != 0;
+  const double q = 0.25 * g.inv_h;
+  const int s_lo = D == 3 ? z0 - 1 : 0, s_hi = D == 3 ? z1 + 1 : 0;
+
+  // Lane 16h + j (j < 4): sorted range of source row cy = ty + 2 - j of
+  // source plane s for half h; the next plane's ranges load while this runs.
+  auto ranges = [&](int s, uint32_t& rb, uint32_t& len, uint32_t& rid) {
+    rb = 0;
+    len = 0;
+    rid = 0;
+    const bool zok = D != 3 || pz || (s >= -1 && s <= nz);
+    if (hl < 4 && row_ok && zok && s <= s_hi) {
+      const int szw = D == 3 ? (pz ? wrap_cell(s, nz) : s) : 0;
+      int cy = ty + 2 - hl;
+      bool ok = true;
+      if (py) cy = wrap_cell(cy, ny);
+      else ok = cy >= -1 && cy <= ny;
+      if (ok) {
+        rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
+        rb = __ldg(rowstart + rid);
+        len = __ldg(rowstart + rid + 1) - rb;
+      }
+    }
+  };
+  uint32_t rb_n, len_n, rid_n;
+  ranges(s_lo, rb_n, len_n, rid_n);
+
+  for (int s = s_lo; s <= s_hi; ++s) {
+    const uint32_t rb = rb_n, len = len_n, rid = rid_n;
+    ranges(s + 1, rb_n, len_n, rid_n);
+    int so[4];
+#pragma unroll
+    for (int kz = 0; kz < 4; ++kz) {
+      const int tz = s + kz - 2;
+      so[kz] = D == 3 ? ((tz >= z0 && tz < z1) ? (tz & 3) * rl : -1) : (kz == 2 ? 0 : -1);
+    }
+    const bool interior = D == 3 && s - 2 >= z0 && s + 1 < z1;
+    if (RL > 0 && interior) {
+      switch (s & 3) {
+        case 0: plane_banks<D, RL, 0>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+        case 1: plane_banks<D, RL, 1>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+        case 2: plane_banks<D, RL, 2>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+        default: plane_banks<D, RL, 3>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+      }
+    } else {
+      plane_banks<D, RL, -1>(W, so, rb, len, rid, rowbank, rec, rcx, q);
+    }
+    // Target plane s - 2 has all its sources: fold, store once, clear.
+    const int t = D == 3 ? s - 2 : 0;
+    if (t >= z0 && t < z1) {
+      double* Wr = W + (D == 3 ? (t & 3) * rl : 0);
+      if (row_ok) {
+        double* orow = out + ((size_t)t * ny + ty) * nx;
+        if (px && nx < 8) {
+          for (int x = hl; x < nx; x += 16) {
+            double v = Wr[x + kPadL];
+            for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[qx + kPadL];
+            for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[qx + kPadL];
+            orow[x] = v;
+          }
+        } else {
+          for (int x = hl; x < nx; x += 16) {
+            double v = Wr[x + kPadL];
+            if (px) {  // pads x' = -4..-1 fold onto nx-4.., x' = nx, nx+1 onto 0, 1
+              if (x >= nx - kPadL) v += Wr[x - nx + kPadL];
+              if (x < kPadR) v += Wr[x + nx + kPadL];
+            }
+            orow[x] = v;
+          }
+        }
+      }
+      __syncwarp();
+      double2* Z = reinterpret_cast<double2*>(Wr);
+      for (int i = hl; i < rl / 2; i += 16) Z[i] = make_double2(0.0, 0.0);
       __syncwarp();
     }
   }
