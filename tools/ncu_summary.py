@@ -41,7 +41,7 @@ for row in r[2:]:
                 pass
     lines.append(f"{name[:70]}\n    " + "  ".join(f"{k}={v}" for k, v in d.items()))
     total = (d.get("dram_read_MB", 0) + d.get("dram_write_MB", 0)) * 1e6
-    for tag, key in (("spread", "spread_sweep"), ("interp", "interp_tma")):
+    for tag, key in (("spread", "spread_banks"), ("interp", "interp_tma")):
         if key in name:
             traffic[tag] = int(total)
 Path(outp).write_text("\n".join(lines) + "\n")
