@@ -770,9 +770,11 @@ bool interp_tma_tiling(const DevGrid& g, size_t n, sw::InterpTiling& T) {
     int zc = (int)std::max<long>(4, (nz + chunks - 1) / chunks);
     zc = std::min(zc, nz);
     const int hmax = zc + 2;
-    // Records staged per step: twice the mean points per step, 64..1024.
+    // Records staged per step: 0.9 x the mean points per step, 64..1024 (a
+    // step's overflow is read from global memory; smaller stages leave room
+    // for taller tiles -- less field re-read -- and a deeper ring).
     const double mean = (double)n * (ty + ghosts) / ((double)(ny + 2) * (nz + 2));
-    int cap = (int)std::min(1024.0, std::max(64.0, 2.0 * mean + 32.0));
+    int cap = (int)std::min(1024.0, std::max(64.0, 0.9 * mean));
     cap = (cap + 31) & ~31;
     const uint32_t stride = (uint32_t)(((size_t)fr * pitch + (size_t)cap * 64 + 1023) & ~size_t(1023));
     const size_t budget = 226 * 1024 - 16 * sw::kMaxSlots - 12 * (size_t)hmax - 1024;
@@ -849,6 +851,7 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   uint32_t* maxrow = nlong + 1;
   uint32_t* long_rows = maxrow + 1;
   IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 3) * 4, st));
+  s.maxrow = spread ? maxrow : nullptr;  // (zeroed above; set by the row scan)
   if (n == 0) {
     IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)nrows + 1) * 4, st));
     return;
@@ -871,7 +874,6 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   ctx.prof_begin(kProfSort, &ev);
   bucket::row_scan_kernel<<<nchunks, bucket::kScanThreads, 0, st>>>(
       count, s.rowstart.p, nrows, status, ticket, spread ? long_rows : nullptr, nlong, maxrow);
-  s.maxrow = spread ? maxrow : nullptr;
   ctx.launches += 2;
   if (!spread) {
     if (g.dim == 3)
