@@ -206,16 +206,18 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
       const uint32_t xo = tma::swz128(x) + (uint32_t)(valid ? cy - hy0 : 0) * T.pitch;
       double acc = 0.0;
       if (valid) {
+        // Pairwise sums (dependency depth 6 instead of 20 fused multiply-adds).
+        double az[4];
 #pragma unroll
         for (int kz = 0; kz < 4; ++kz) {
           const unsigned char* p = sl[kz] + xo;
-          double az = 0.0;
+          double v[4];
 #pragma unroll
           for (int ky = 0; ky < 4; ++ky)
-            az = fma(wy[ky], *reinterpret_cast<const double*>(p + (uint32_t)ky * T.pitch), az);
-          acc = fma(wz[kz], az, acc);
+            v[ky] = *reinterpret_cast<const double*>(p + (uint32_t)ky * T.pitch);
+          az[kz] = fma(wy[1], v[1], wy[0] * v[0]) + fma(wy[3], v[3], wy[2] * v[2]);
         }
-        acc *= wxk;
+        acc = (fma(wz[1], az[1], wz[0] * az[0]) + fma(wz[3], az[3], wz[2] * az[2])) * wxk;
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
