@@ -344,6 +344,42 @@ def test_device_path_matches_host_path():
     assert np.array_equal(ei.cpu().numpy(), ib.interpolate(ib.GridField(g, e), pts, K))
 
 
+def test_cuda_graph_replay_matches_eager():
+    """The device pipeline (sort, records, sweeps) has no host round trip, so
+    a step captured in a CUDA graph replays bit-identically (bench.py)."""
+    import torch
+
+    from paper_2012_06646_b200.device import DeviceOperators
+
+    rng = np.random.default_rng(12)
+    g = ib.StaggeredGrid([64, 48, 40], 0.1, [0.5, 0.5, 0.0], [True] * 3)
+    n = 40000
+    pts = torch.tensor(rand_points(g, n, rng), device="cuda")
+    vals = torch.tensor(rng.uniform(-1, 1, n), device="cuda")
+    e = torch.tensor(rng.uniform(-1, 1, g.point_count()), device="cuda")
+    ops = DeviceOperators(0)
+    ell = torch.empty(g.point_count(), dtype=torch.float64, device="cuda")
+    E = torch.empty(n, dtype=torch.float64, device="cuda")
+
+    def step():
+        ops.spread(pts, vals, g, out=ell)
+        ops.interpolate(e, pts, g, out=E)
+
+    step()
+    torch.cuda.synchronize()
+    ref_ell, ref_E = ell.clone(), E.clone()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    ell.zero_()
+    E.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(ell, ref_ell) and torch.equal(E, ref_E)
+    o = og(g)
+    assert O.max_rel_deviation(ell.cpu().numpy(), O.spread_serial(o, pts.cpu().numpy(), vals.cpu().numpy())) <= TOL
+
+
 def test_clustered_long_runs():
     # many points per cell: rank-serialized shared-memory accumulation
     rng = np.random.default_rng(13)
