@@ -1,0 +1,70 @@
+"""Device-resident MAC step loop (paper_2012_06646_b200/step.py) against the
+reference's bench step (inc/bench/run.hpp:59-128) restated over the oracle."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2012_06646_b200 import step as S
+from paper_2012_06646_b200 import synth
+
+TOL = 1e-12
+
+
+def test_step_config_defaults_match_reference():
+    c = S.StepConfig()
+    assert (c.refinement, c.point_count, c.domain_edge_um) == (64, 1 << 16, 16.0)
+    assert (c.dt_us, c.shear_rate, c.spring_constant, c.seed) == (0.1, 1000.0, 0.01, 1)
+    g = S.mac_grids(16, c.edge_cm)
+    assert [list(x.staggerings) for x in g] == [[0.0, 0.5, 0.5], [0.5, 0.0, 0.5], [0.5, 0.5, 0.0]]
+
+
+def _og(g):
+    return O.make_grid(g.extents, g.spacing(), g.staggerings, g.periodic, g.origin)
+
+
+def _reference_loop(cfg, steps):
+    """run_benchmark's step, numpy + oracle operators (setup.hpp, run.hpp)."""
+    L, dt = cfg.edge_cm, cfg.dt_s
+    grids = [_og(g) for g in S.mac_grids(cfg.refinement, L)]
+    N = cfg.refinement
+    h = L / N
+    y = h * (np.arange(N) + 0.5)
+    u2 = np.broadcast_to((cfg.shear_rate * (y - 0.5 * L))[None, :, None], (N, N, N)).reshape(-1)
+    vel = [np.zeros(N ** 3), np.zeros(N ** 3), np.ascontiguousarray(u2)]
+    X = synth.scatter_points(cfg.point_count, L, cfg.seed).copy()
+    X0 = X.copy()
+    ell = None
+    for _ in range(steps):
+        u = np.stack([O.interpolate(g, vel[a], X) for a, g in enumerate(grids)])
+        Xs = X + dt * u.T
+        d = Xs - X0
+        d -= L * np.round(d / L)
+        F = -cfg.spring_constant * d
+        ell = [O.spread_serial(g, Xs, F[:, a]) for a, g in enumerate(grids)]
+        u2_ = np.stack([O.interpolate(g, vel[a], X) for a, g in enumerate(grids)])
+        X = X + dt * u2_.T
+    return X, ell
+
+
+@pytest.mark.gpu
+def test_mac_step_loop_matches_reference_step():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    # A shear rate large enough that points cross cells within the test.
+    cfg = S.StepConfig(refinement=16, point_count=3000, dt_us=100.0)
+    loop = S.MacStepLoop(cfg)
+    for _ in range(4):
+        loop.step()
+    torch.cuda.synchronize()
+    X_ref, ell_ref = _reference_loop(cfg, 4)
+    X = loop.X.cpu().numpy()
+    assert np.abs(X - X_ref).max() <= TOL * cfg.edge_cm
+    assert np.abs(X - synth.scatter_points(cfg.point_count, cfg.edge_cm, cfg.seed)).max() > 0.1 * cfg.edge_cm / 16
+    for a in range(3):
+        got = loop.spread_result[a].cpu().numpy()
+        if not np.any(ell_ref[a]):  # shear flow along z: no x / y tether forces
+            assert not np.any(got)
+        else:
+            assert O.max_rel_deviation(got, ell_ref[a]) <= TOL
