@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
+    ap.add_argument("--mac-steps", type=int, default=5, help="MAC vector step timing (0: skip)")
     return ap.parse_args()
 
 
@@ -356,6 +357,46 @@ def run_ours(args):
                "h2d_bytes_per_step": int(hx_s.nbytes + hg.nbytes + hx_n.nbytes + hf.nbytes),
                "d2h_bytes_per_step": int(n_omega * 8 + n * 8), "note": note}
 
+    # Secondary figure: the reference's MAC vector step -- 6
+    # interpolations + 3 spreads on the three component grids + tether forces
+    # and position updates -- device-resident (step.py), same n and N,
+    # captured in a CUDA graph like the headline step.
+    mac = None
+    if world == 1 and args.mac_steps > 0:
+        from paper_2012_06646_b200.step import MacStepLoop, StepConfig
+
+        loop = MacStepLoop(StepConfig(refinement=N, point_count=n), device=local, ops=ops,
+                           points=data["x_n"])
+        for _ in range(2):
+            loop.step()
+        torch.cuda.synchronize()
+        mgraph = None
+        if not args.no_graph:
+            mgraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(mgraph):
+                loop.step()
+            mgraph.replay()
+            torch.cuda.synchronize()
+        mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.mac_steps)]
+        for i in range(args.mac_steps):
+            flush.fill_(float(i))
+            mev[i][0].record()
+            if mgraph is not None:
+                mgraph.replay()
+            else:
+                loop.step()
+            mev[i][1].record()
+        torch.cuda.synchronize()
+        mac_ms = sum(a.elapsed_time(b) for a, b in mev) / args.mac_steps
+        mac = {"value": n / (mac_ms * 1e-3), "unit": UNIT, "ms_per_step": mac_ms,
+               "steps": args.mac_steps,
+               "workload": "ib::bench::run_benchmark step on the MAC grids (alpha = (0,.5,.5), "
+                           "(.5,0,.5), (.5,.5,0)) of the same 256^3 periodic cube, fixed shear "
+                           "field, tether forces: 2 x interpolate_vector + 1 x spread_vector + "
+                           "updates per step, same 2^20 points, FP64, CUDA graph"}
+        del loop
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -396,6 +437,7 @@ def run_ours(args):
                               "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
             "breakdown_us": {k: round(v, 2) for k, v in per_launch.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "mac_vector_step": mac,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))
