@@ -38,6 +38,16 @@ constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
 constexpr int kBanks = 16;         // x banks of the spread sweep's bank mode (x cell mod 16)
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
+
+// Spread batching mode, decided on the device from the densest row (row scan):
+// bank mode (lanes own x banks, ibc_spread.cuh) for sparse rows -- and for
+// rows holding more than two points per cell on average, i.e. clustered
+// points, where the pull mode's same-cell shuffle groups serialise -- pull
+// mode otherwise.  Bank tables hold 16-bit offsets, hence the cap.
+__host__ __device__ __forceinline__ bool bank_mode(uint32_t maxrow, uint32_t pull_row,
+                                                   uint32_t rowdiv) {
+  return maxrow <= pull_row || (maxrow > 2u * rowdiv && maxrow <= 0xffffu);
+}
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
 // Points per thread of the one-pass kernels K1/K3: their loads, atomics and
@@ -310,7 +320,7 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
   // key, index) order instead, bank = x cell mod 16, so that the sweep's
   // lanes can take one bank each (ibc_spread.cuh); rb is that rank, lt the
   // number of the row's points in lower banks, ceq the count in this bank.
-  const bool banked = *maxrow <= bank_rows;
+  const bool banked = bank_mode(*maxrow, bank_rows, g.rowdiv);
   uint32_t rk = 0, rbe = 0, lt = 0, ceq = 0;
   if (!banked) {
     uint32_t j = 0;
@@ -360,12 +370,20 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     const uint32_t* __restrict__ nlong, const unsigned long long* __restrict__ bpair,
     uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
-    double* __restrict__ rec, int* __restrict__ rcx) {
-  extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
+    double* __restrict__ rec, int* __restrict__ rcx, uint32_t* __restrict__ rowbank,
+    const uint32_t* __restrict__ maxrow, uint32_t bank_rows) {
+  // [kLongSortMax] (key << 32 | index), then [kLongSortMax] record positions.
+  extern __shared__ unsigned long long sk[];
+  uint32_t* pos = reinterpret_cast<uint32_t*>(sk + kLongSortMax);
+  __shared__ uint32_t hist[kBanks], first[kBanks];
   const uint32_t count = *nlong;
+  const bool banked = bank_mode(*maxrow, bank_rows, g.rowdiv);
+  const int lane = threadIdx.x & 31;
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = long_rows[li];
     const uint32_t a = start[r], len = start[r + 1] - a;
+    const uint32_t base = r * g.rowdiv;
+    auto bank_of = [&](unsigned long long c) { return ((uint32_t)(c >> 32) - base) & (kBanks - 1); };
     if (len <= (uint32_t)kLongSortMax) {
       uint32_t m = 1;
       while (m < len) m <<= 1;
@@ -389,22 +407,61 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
           __syncthreads();
         }
       }
+      if (banked) {
+        // Record positions in (bank, key, index) order: a stable partition
+        // of the sorted row by bank, walked by warp 0 in 32-element chunks.
+        if (threadIdx.x < kBanks) hist[threadIdx.x] = 0;
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) atomicAdd(&hist[bank_of(sk[e])], 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          uint32_t acc = 0;
+          for (int b = 0; b < kBanks; ++b) {
+            first[b] = acc;
+            rowbank[(size_t)r * kBanks + b] = (acc << 16) | hist[b];
+            acc += hist[b];
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {
+          for (uint32_t c0 = 0; c0 < len; c0 += 32) {
+            const uint32_t e = c0 + lane;
+            const uint32_t b = e < len ? bank_of(sk[e]) : 0x100u + lane;
+            const uint32_t peers = __match_any_sync(0xffffffffu, b);
+            if (e < len) {
+              pos[e] = first[b] + __popc(peers & ((1u << lane) - 1u));
+            }
+            __syncwarp();
+            if (e < len && (peers & ((1u << lane) - 1u)) == 0) first[b] += __popc(peers);
+            __syncwarp();
+          }
+        }
+        __syncthreads();
+      }
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
         skey[a + e] = (uint32_t)(sk[e] >> 32);
         sidx[a + e] = (uint32_t)sk[e];
-        write_record<D>(g, X, G, (uint32_t)sk[e], a + e, rec, rcx);
+        write_record<D>(g, X, G, (uint32_t)sk[e], a + (banked ? pos[e] : e), rec, rcx);
       }
       __syncthreads();
     } else {
       // Very long row: rank every element by counting (correct, quadratic).
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
         const unsigned long long ce = bpair[a + e];
-        uint32_t rk = 0;
-        for (uint32_t f = 0; f < len; ++f)
-          rk += bpair[a + f] < ce ? 1u : 0u;
+        const uint32_t be = bank_of(ce);
+        uint32_t rk = 0, rb = 0, lt = 0, ceq = 0;
+        for (uint32_t f = 0; f < len; ++f) {
+          const unsigned long long cf = bpair[a + f];
+          const uint32_t less = cf < ce ? 1u : 0u, bf = bank_of(cf);
+          rk += less;
+          lt += bf < be ? 1u : 0u;
+          ceq += bf == be ? 1u : 0u;
+          rb += bf == be ? less : 0u;
+        }
         skey[a + rk] = (uint32_t)(ce >> 32);
         sidx[a + rk] = (uint32_t)ce;
-        write_record<D>(g, X, G, (uint32_t)ce, a + rk, rec, rcx);
+        write_record<D>(g, X, G, (uint32_t)ce, a + (banked ? lt + rb : rk), rec, rcx);
+        if (banked && rb == 0) rowbank[(size_t)r * kBanks + be] = (lt << 16) | ceq;
       }
     }
   }

@@ -891,7 +891,7 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
     bucket::scatter_pairs_kernel<<<pblocks, bucket::kThreads, 0, st>>>(
         s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.bpair.p);
     static bool attr_set[64] = {};
-    const size_t lsm = (size_t)bucket::kLongSortMax * 8;
+    const size_t lsm = (size_t)bucket::kLongSortMax * 12;  // keys + record positions
     if (!attr_set[ctx.device & 63]) {
       IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<2>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
@@ -905,8 +905,9 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
                                                    d_points, d_values, s.rec.p, s.rec_cx.p,
                                                    s.rowbank.p, maxrow, sp::pull_row());
       long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.bpair.p,
-                                                     s.keys[0].p, s.vals[0].p, g,
-                                                     d_points, d_values, s.rec.p, s.rec_cx.p);
+                                                     s.keys[0].p, s.vals[0].p, g, d_points,
+                                                     d_values, s.rec.p, s.rec_cx.p, s.rowbank.p,
+                                                     maxrow, sp::pull_row());
     };
     if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
     else sorts(bucket::row_sort_kernel<2>, bucket::long_row_sort_kernel<2>);

@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include "ibc_device.cuh"
+#include "ibc_bucket.cuh"  // bank_mode
 
 namespace ibc {
 namespace sp {
@@ -249,7 +250,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  if (maxrow && *maxrow <= T.pull_row) return;  // bank mode
+  if (maxrow && bucket::bank_mode(*maxrow, T.pull_row, g.rowdiv)) return;  // bank mode
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -370,7 +371,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
                                                           const uint32_t* __restrict__ rowbank,
                                                           double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  if (*maxrow > T.pull_row) return;  // pull mode
+  if (!bucket::bank_mode(*maxrow, T.pull_row, g.rowdiv)) return;  // pull mode
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, hl = lane & 15, h = lane >> 4;

@@ -395,6 +395,22 @@ def test_clustered_long_runs():
     assert O.max_rel_deviation(got.values, want) <= TOL
 
 
+def test_clustered_row_longer_than_shared_sort():
+    # one cell-row holding > 8192 points (the quadratic long-row path) next to
+    # ordinary rows: clustered rows put the sweep in bank mode
+    rng = np.random.default_rng(17)
+    g = ib.StaggeredGrid([24, 20, 16], 1.0, [0.5, 0.5, 0.0], [True] * 3)
+    tight = np.array([7.3, 9.6, 4.2]) + rng.normal(0, 0.02, (9000, 3))
+    loose = rand_points(g, 3000, rng)
+    pts = np.concatenate([tight, loose])
+    vals = rng.uniform(-1, 1, len(pts))
+    ws = ib.SpreadWorkspace(len(pts), g)
+    got = ib.spread_fused(pts, vals, g, K, ws, 8)
+    _, keys, perm, _ = O.spread_fused(og(g), pts, vals)
+    assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm)
+    assert O.max_rel_deviation(got.values, O.spread_serial(og(g), pts, vals)) <= TOL
+
+
 @pytest.mark.parametrize("per", [(True, True, True), (False, True, False), (True, False, True),
                                  (False, False, False)])
 def test_zsweep_medium_grids_mixed_periodicity(per):
