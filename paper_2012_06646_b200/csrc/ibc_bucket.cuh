@@ -36,7 +36,12 @@ constexpr int kChunk = kScanThreads * kScanItems;  // rows per scan CTA
 constexpr uint32_t kFlagAggregate = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
-constexpr int kBanks = 16;         // x banks of the spread sweep's bank mode (x cell mod 16)
+// Spread sweep, bank mode: target rows per warp and x banks per row (lanes per
+// row).  A half-warp holds 16 bank pairs: 2 rows per warp -> 16 banks (x
+// mod 16) per row; 4 rows per warp -> two rows interleaved per half, 8 banks
+// (x mod 8) each.
+constexpr int kRowsPerWarp = 2;
+constexpr int kBanks = 32 / kRowsPerWarp;
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 
 // Spread batching mode, decided on the device from the densest row (row scan):
@@ -44,8 +49,11 @@ constexpr int kShortRow = 256;      // rows up to this length are sorted by one 
 // rows holding more than two points per cell on average, i.e. clustered
 // points, where the pull mode's same-cell shuffle groups serialise -- pull
 // mode otherwise.  Bank tables hold 16-bit offsets, hence the cap.
+// pull_row == kNoBankMode: the bank window does not fit (very long x rows).
+constexpr uint32_t kNoBankMode = 0xffffffffu;
 __host__ __device__ __forceinline__ bool bank_mode(uint32_t maxrow, uint32_t pull_row,
                                                    uint32_t rowdiv) {
+  if (pull_row == kNoBankMode) return false;
   return maxrow <= pull_row || (maxrow > 2u * rowdiv && maxrow <= 0xffffu);
 }
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
@@ -293,7 +301,7 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
 // bucket (contiguous, and shared by neighbouring lanes, so the loads are
 // L1 broadcasts) -- and writes the pair at the row's start + rank: stable
 // (key, index) order.  Its weight record goes to the row's start + its rank
-// in (x bank, key, index) order, and the row's 16-entry bank table is
+// in (x bank, key, index) order, and the row's kBanks-entry bank table is
 // filled.  Full warps whatever the row lengths.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(

@@ -53,6 +53,7 @@ struct PointScratch {
   DevBuf<uint32_t> rowbank; // bucket sort: per row and x bank, first record << 16 | count
   DevBuf<unsigned long long> bpair;  // bucket sort: (key << 32 | index) in row buckets
   const uint32_t* maxrow = nullptr;  // bucket sort: largest row count (device)
+  uint32_t bank_rows = 0;            // spread: bank-mode row threshold (bucket::bank_mode)
   DevBuf<int> rec_cx;
   DevBuf<double> rec;         // 12 x cap weight records (spread)
   DevBuf<uint32_t> run_keys;  // lazily filled

@@ -627,7 +627,7 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
 
 // Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
 // rows_per_warp = 1: pull mode (wpc warps per CTA, one target row each);
-// 2: bank mode (one warp per CTA, a target row per half-warp).
+// > 1: bank mode (one warp per CTA, bucket::kRowsPerWarp target rows).
 bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
   if (g.dim < 2) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
@@ -660,7 +660,12 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
   sp::SweepTiling W, WB;  // pull mode, bank mode
-  const bool sweep = sweep_tiling(g, W, 1) && sweep_tiling(g, WB, 2);
+  const bool sweep = sweep_tiling(g, W, 1);
+  if (!sweep_tiling(g, WB, bucket::kRowsPerWarp)) {  // bank window too large: pull mode only
+    WB = W;
+    W.pull_row = WB.pull_row = bucket::kNoBankMode;
+  }
+  s.bank_rows = W.pull_row;
   const bool radix = getenv("IBC_SORT") && std::string(getenv("IBC_SORT")) == "radix";
   if (sweep && !radix) {
     bucket_points(ctx, g, d_points, d_values, n, s, true);
@@ -700,13 +705,14 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   if (sweep) {
     ctx.prof_begin(kProfSpread, &ev);
     const size_t smem = (size_t)W.wpc * (g.dim == 3 ? 4 : 1) * W.rl * sizeof(double);
-    const size_t smem_b = (size_t)2 * WB.wpc * (g.dim == 3 ? 4 : 1) * WB.rl * sizeof(double);
+    const size_t smem_b =
+        (size_t)bucket::kRowsPerWarp * WB.wpc * (g.dim == 3 ? 4 : 1) * WB.rl * sizeof(double);
     const unsigned blocks = (unsigned)(W.nyg * W.nzc), blocks_b = (unsigned)(WB.nyg * WB.nzc);
     // Compile-time window row length for the common x extents; both modes
     // are launched when the densest row is only known on the device.
     const uint32_t* maxrow = (!radix) ? s.maxrow : nullptr;
     auto launch = [&](auto bank_k, auto pull_k) {
-      if (maxrow) {
+      if (maxrow && WB.pull_row != bucket::kNoBankMode) {
         bank_k<<<blocks_b, 32 * WB.wpc, smem_b, st>>>(g, WB, maxrow, s.rowstart.p, s.rec.p,
                                                       s.rec_cx.p, s.rowbank.p, d_out);
         ++ctx.launches;
@@ -903,11 +909,11 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
       short_k<<<blocks, bucket::kThreads, 0, st>>>(s.rowstart.p, (uint32_t)n, s.bpair.p,
                                                    s.keys[0].p, s.vals[0].p, g,
                                                    d_points, d_values, s.rec.p, s.rec_cx.p,
-                                                   s.rowbank.p, maxrow, sp::pull_row());
+                                                   s.rowbank.p, maxrow, s.bank_rows);
       long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.bpair.p,
                                                      s.keys[0].p, s.vals[0].p, g, d_points,
                                                      d_values, s.rec.p, s.rec_cx.p, s.rowbank.p,
-                                                     maxrow, sp::pull_row());
+                                                     maxrow, s.bank_rows);
     };
     if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
     else sorts(bucket::row_sort_kernel<2>, bucket::long_row_sort_kernel<2>);

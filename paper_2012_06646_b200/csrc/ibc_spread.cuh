@@ -62,30 +62,32 @@ __host__ __device__ constexpr int row_len(int nx) {
   return (nx + kPadL + kPadR) + ((nx + kPadL + kPadR) & 1);
 }
 
-// Bank mode (sparse rows): one source plane for the two target rows of a
-// warp, one per half-warp.  In each half, lane b owns x bank b (x cell mod
-// 16, up to a fixed shift) and walks that bank's records of the half's four
-// source rows in order (records are bank-ordered within a row, with a
-// 16-entry (first, count) table per row, ibc_bucket.cuh K4).  The cells of
-// one instruction's adds then differ mod 16 within a half -- distinct bank
-// pairs, and distinct addresses even across kx phases of one point -- and the
-// halves write different windows: conflict-free, no collision test.  Lane
-// 16h + j (j < 4) holds row j's sorted start rb, length len and row id rid
-// for half h.
+// Bank mode: one source plane for the kRowsPerWarp target rows of a warp,
+// GS = kBanks lanes per row.  Lane b of a row's group owns x bank b (x cell
+// mod kBanks, up to a fixed shift) and walks that bank's records of the row's
+// four source rows in order (records are bank-ordered within a row, with a
+// kBanks-entry (first, count) table per row, ibc_bucket.cuh K4).  A half-warp
+// holds 16 / kBanks rows whose windows are interleaved element by element
+// (stride ES = 16 / kBanks), so within a half the cells of one instruction's
+// adds hit distinct bank pairs -- and distinct addresses, even across the kx
+// phases of one point: conflict-free, no collision test.  Lane gb + j (j <
+// 4, gb = the group's first lane) holds source row j's sorted start rb,
+// length len and row id rid for the group's target row.
 template <int D, int RL, int R>
 __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t rb,
                                            uint32_t len, uint32_t rid,
                                            const uint32_t* __restrict__ rowbank,
                                            const double* __restrict__ rec,
                                            const int* __restrict__ rcx, double q) {
-  const int lane = threadIdx.x & 31, bank = lane & 15, hb = lane & 16;
+  constexpr int GS = bucket::kBanks, ES = 16 / GS;
+  const int lane = threadIdx.x & 31, bank = lane & (GS - 1), gb = lane & ~(GS - 1);
   uint32_t lo[4], c[4], cnt = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t rbj = __shfl_sync(0xffffffffu, rb, hb + j);
-    const uint32_t lenj = __shfl_sync(0xffffffffu, len, hb + j);
-    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, hb + j);
-    const uint32_t e = lenj ? __ldg(rowbank + (size_t)ridj * 16 + bank) : 0u;  // first << 16 | count
+    const uint32_t rbj = __shfl_sync(0xffffffffu, rb, gb + j);
+    const uint32_t lenj = __shfl_sync(0xffffffffu, len, gb + j);
+    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, gb + j);
+    const uint32_t e = lenj ? __ldg(rowbank + (size_t)ridj * GS + bank) : 0u;  // first << 16 | count
     lo[j] = rbj + (e >> 16) - cnt;  // sorted position of this lane's k-th record = lo[j] + k
     cnt += e & 0xffffu;
     c[j] = cnt;
@@ -96,18 +98,18 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
     return (j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3]) + k;
   };
   // Records are prefetched one iteration ahead (the loop is latency-bound).
-  double4 ga = make_double4(0.0, 0.0, 0.0, 0.0), gb = ga;
+  double4 ga = make_double4(0.0, 0.0, 0.0, 0.0), gb4 = ga;
   int cx = 0;
   if (cnt > 0) {
     const uint32_t p = pos(0);
     ga = ld_v4_nc(rec + 8 * (size_t)p);
-    gb = ld_v4_nc(rec + 8 * (size_t)p + 4);
+    gb4 = ld_v4_nc(rec + 8 * (size_t)p + 4);
     cx = __ldg(rcx + p);
   }
   for (uint32_t k = 0; k < kmax; ++k) {
     const bool valid = k < cnt;
     const int j = (k >= c[0]) + (k >= c[1]) + (k >= c[2]);
-    double4 na = ga, nb = gb;
+    double4 na = ga, nb = gb4;
     int ncx = cx;
     if (k + 1 < cnt) {
       const uint32_t p = pos(k + 1);
@@ -116,36 +118,36 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
       ncx = __ldg(rcx + p);
     }
     // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
-    const double vy = (j & 1) ? gb.x : gb.y;
+    const double vy = (j & 1) ? gb4.x : gb4.y;
     const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
     double a[4];
     if (D == 3) {
-      a[0] = fma(-wq, gb.w, wq);
-      a[1] = fma(wq, gb.z, wq);
-      a[2] = fma(wq, gb.w, wq);
-      a[3] = fma(-wq, gb.z, wq);
+      a[0] = fma(-wq, gb4.w, wq);
+      a[1] = fma(wq, gb4.z, wq);
+      a[2] = fma(wq, gb4.w, wq);
+      a[3] = fma(-wq, gb4.z, wq);
     } else {
       a[0] = a[1] = a[3] = 0.0;
       a[2] = wq / q;
     }
     const double gk[4] = {ga.x, ga.y, ga.z, ga.w};
-    double* wa = W + (cx + (kPadL - 2));
+    double* wa = W + ES * (cx + (kPadL - 2));
 #pragma unroll
     for (int kx = 0; kx < 4; ++kx) {
       if (valid) {
         if (R >= 0) {  // interior plane: slot offsets are immediates
 #pragma unroll
-          for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * RL + kx] += gk[kx] * a[kz];
+          for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * (ES * RL) + ES * kx] += gk[kx] * a[kz];
         } else {
 #pragma unroll
           for (int kz = 0; kz < 4; ++kz)
-            if (so[kz] >= 0) wa[so[kz] + kx] += gk[kx] * a[kz];
+            if (so[kz] >= 0) wa[ES * (so[kz] + kx)] += gk[kx] * a[kz];
         }
       }
       __syncwarp();
     }
     ga = na;
-    gb = nb;
+    gb4 = nb;
     cx = ncx;
   }
 }
@@ -359,9 +361,9 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
 }
 
 
-// Bank mode (sparse rows, densest row <= T.pull_row): one warp per pair of
-// target rows (one per half-warp), z-sweep as above, plane_banks per source
-// plane.  Window: two rows x four slots per warp.
+// Bank mode (bucket::bank_mode): one warp per kRowsPerWarp target rows of a
+// z-chunk, z-sweep as above, plane_banks per source plane.  Window per
+// half-warp: its 16 / kBanks rows interleaved, four slots.
 template <int D, int RL>
 __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling T,
                                                           const uint32_t* __restrict__ maxrow,
@@ -373,16 +375,20 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
   extern __shared__ __align__(16) double win[];
   if (!bucket::bank_mode(*maxrow, T.pull_row, g.rowdiv)) return;  // pull mode
   constexpr int kSlots = D == 3 ? 4 : 1;
+  constexpr int GS = bucket::kBanks, ES = 16 / GS, RPW = bucket::kRowsPerWarp;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, hl = lane & 15, h = lane >> 4;
+  const int grp = lane / GS, bank = lane & (GS - 1), sub = grp & (ES - 1);
   const int nx = g.n[0], ny = g.n[1], nz = D == 3 ? g.n[2] : 1;
   const int yg = blockIdx.x % T.nyg, zi = blockIdx.x / T.nyg;
-  const int ty = 2 * yg + h;  // this half's target row
+  const int ty = RPW * yg + grp;  // this group's target row
   const bool row_ok = ty < ny;
   const int z0 = D == 3 ? zi * T.zc : 0;
   const int z1 = D == 3 ? min(z0 + T.zc, nz) : 1;
-  double* W = win + (size_t)h * kSlots * rl;
-  for (int i = lane; i < 2 * kSlots * rl; i += 32) win[i] = 0.0;
+  const size_t half_win = (size_t)kSlots * ES * rl;  // doubles per half-warp window
+  double* Wh = win + (size_t)h * half_win;
+  double* W = Wh + sub;  // this group's row, element stride ES
+  for (int i = lane; i < 2 * (int)half_win; i += 32) win[i] = 0.0;
   __syncwarp();
 
   const bool px = g.periodic[0] != 0, py = g.periodic[1] != 0;
@@ -390,16 +396,16 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
   const double q = 0.25 * g.inv_h;
   const int s_lo = D == 3 ? z0 - 1 : 0, s_hi = D == 3 ? z1 + 1 : 0;
 
-  // Lane 16h + j (j < 4): sorted range of source row cy = ty + 2 - j of
-  // source plane s for half h; the next plane's ranges load while this runs.
+  // Lane gb + j (j < 4): sorted range of source row cy = ty + 2 - j of
+  // source plane s for the group's row; the next plane's load while this runs.
   auto ranges = [&](int s, uint32_t& rb, uint32_t& len, uint32_t& rid) {
     rb = 0;
     len = 0;
     rid = 0;
     const bool zok = D != 3 || pz || (s >= -1 && s <= nz);
-    if (hl < 4 && row_ok && zok && s <= s_hi) {
+    if (bank < 4 && row_ok && zok && s <= s_hi) {
       const int szw = D == 3 ? (pz ? wrap_cell(s, nz) : s) : 0;
-      int cy = ty + 2 - hl;
+      int cy = ty + 2 - bank;
       bool ok = true;
       if (py) cy = wrap_cell(cy, ny);
       else ok = cy >= -1 && cy <= ny;
@@ -436,30 +442,31 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
     // Target plane s - 2 has all its sources: fold, store once, clear.
     const int t = D == 3 ? s - 2 : 0;
     if (t >= z0 && t < z1) {
-      double* Wr = W + (D == 3 ? (t & 3) * rl : 0);
+      const size_t slot = D == 3 ? (size_t)(t & 3) * ES * rl : 0;
+      const double* Wr = W + slot;
       if (row_ok) {
         double* orow = out + ((size_t)t * ny + ty) * nx;
         if (px && nx < 8) {
-          for (int x = hl; x < nx; x += 16) {
-            double v = Wr[x + kPadL];
-            for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[qx + kPadL];
-            for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[qx + kPadL];
+          for (int x = bank; x < nx; x += GS) {
+            double v = Wr[ES * (x + kPadL)];
+            for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[ES * (qx + kPadL)];
+            for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[ES * (qx + kPadL)];
             orow[x] = v;
           }
         } else {
-          for (int x = hl; x < nx; x += 16) {
-            double v = Wr[x + kPadL];
+          for (int x = bank; x < nx; x += GS) {
+            double v = Wr[ES * (x + kPadL)];
             if (px) {  // pads x' = -4..-1 fold onto nx-4.., x' = nx, nx+1 onto 0, 1
-              if (x >= nx - kPadL) v += Wr[x - nx + kPadL];
-              if (x < kPadR) v += Wr[x + nx + kPadL];
+              if (x >= nx - kPadL) v += Wr[ES * (x - nx + kPadL)];
+              if (x < kPadR) v += Wr[ES * (x + nx + kPadL)];
             }
             orow[x] = v;
           }
         }
       }
       __syncwarp();
-      double2* Z = reinterpret_cast<double2*>(Wr);
-      for (int i = hl; i < rl / 2; i += 16) Z[i] = make_double2(0.0, 0.0);
+      double2* Z = reinterpret_cast<double2*>(Wh + slot);
+      for (int i = hl; i < ES * rl / 2; i += 16) Z[i] = make_double2(0.0, 0.0);
       __syncwarp();
     }
   }
