@@ -296,6 +296,7 @@ static void copy_sorted(ibc_workspace* ws, uint32_t* host, size_t n, bool perm) 
   if (n != s.last_n) invalid("buffer size differs from the last spread's point count");
   if (!n) return;
   use_device(*ws->w.ctx);
+  ibc::ensure_observables(*ws->w.ctx, s);
   IBC_CUDA(cudaMemcpyAsync(host, perm ? s.sorted_perm : s.sorted_keys, n * 4,
                            cudaMemcpyDeviceToHost, ws->w.ctx->stream));
   IBC_CUDA(cudaStreamSynchronize(ws->w.ctx->stream));

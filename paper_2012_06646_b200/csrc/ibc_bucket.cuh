@@ -31,8 +31,7 @@ namespace bucket {
 
 constexpr int kThreads = 256;
 constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
-constexpr int kChunk = kScanThreads * kScanItems;  // rows per scan CTA
+constexpr int kScanItems = 4;                      // buckets per thread, one per row (interp)
 constexpr uint32_t kFlagAggregate = 1u << 30;
 constexpr uint32_t kFlagPrefix = 2u << 30;
 constexpr uint32_t kValueMask = (1u << 30) - 1u;
@@ -63,46 +62,31 @@ constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sor
 constexpr int kPer = 1;
 
 // Cell key of every point (or just its row when full_key == 0), its arrival
-// rank in its row, and the per-row counts.
+// rank in its bucket, and the per-bucket counts.  Buckets: rows (banks == 1,
+// interpolation) or (row, x bank) pairs, row * kBanks + (x cell mod kBanks)
+// (banks == kBanks, spreading) -- a row's buckets are contiguous, so the
+// bucket order is a row order too.
 template <int D>
 __global__ void __launch_bounds__(kThreads) keys_kernel(DevGrid g, const double* __restrict__ X,
-                                                        uint32_t n, int full_key,
+                                                        uint32_t n, int full_key, int banks,
                                                         uint32_t* __restrict__ keys,
                                                         uint32_t* __restrict__ rank,
                                                         uint32_t* __restrict__ count) {
-  const uint32_t i0 = blockIdx.x * (kThreads * kPer) + threadIdx.x;
-  double x[kPer][D];
+  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  uint64_t k = 0;
 #pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const uint32_t i = i0 + u * kThreads;
-#pragma unroll
-    for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
+  for (int a = 0; a < D; ++a) {
+    if (a == 0 && !full_key) continue;
+    double xw;
+    int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
+    if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
+    k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
   }
-  uint32_t key[kPer], rk[kPer];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    uint64_t k = 0;
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      if (a == 0 && !full_key) continue;
-      double xw;
-      int c = cell_of(g, a, x[u][a], &xw);
-      if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
-      k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
-    }
-    key[u] = (uint32_t)k;
-  }
-#pragma unroll
-  for (int u = 0; u < kPer; ++u)
-    if (i0 + u * kThreads < n) rk[u] = atomicAdd(count + key[u] / g.rowdiv, 1u);
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const uint32_t i = i0 + u * kThreads;
-    if (i < n) {
-      keys[i] = full_key ? key[u] : key[u] / g.rowdiv;
-      rank[i] = rk[u];
-    }
-  }
+  const uint32_t key = (uint32_t)k, row = key / g.rowdiv;
+  const uint32_t bucket = banks > 1 ? row * (uint32_t)banks + ((key - row * g.rowdiv) & (banks - 1)) : row;
+  keys[i] = full_key ? key : row;
+  rank[i] = atomicAdd(count + bucket, 1u);
 }
 
 __device__ __forceinline__ void st_flag(uint32_t* p, uint32_t v) {
@@ -114,14 +98,17 @@ __device__ __forceinline__ uint32_t ld_flag(const uint32_t* p) {
   return v;
 }
 
-// Exclusive scan of count[0..nrows) into start[0..nrows] (start[nrows] = total).
-// status: one zeroed word per chunk; ticket: zeroed counter.  Rows longer than
-// kShortRow are appended to long_rows (count in *nlong) when long_rows != null;
-// *maxrow (zeroed, may be null) receives the largest row count.
+// Exclusive scan of count[0..nrows) into start[0..nrows] (start[nrows] = total);
+// here "rows" are buckets, `group` (1 or kBanks) consecutive buckets per grid
+// row.  status: one zeroed word per chunk; ticket: zeroed
+// counter.  Grid rows longer than kShortRow are appended to long_rows (count
+// in *nlong) when long_rows != null; *maxrow (zeroed, may be null) receives
+// the largest grid-row count.
+template <int ITEMS>  // buckets per thread: kScanItems (group 1) or group (one grid row per thread)
 __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* __restrict__ count,
                                                                 uint32_t* __restrict__ start,
-                                                                uint32_t nrows, uint32_t* status,
-                                                                uint32_t* ticket,
+                                                                uint32_t nrows, int group,
+                                                                uint32_t* status, uint32_t* ticket,
                                                                 uint32_t* __restrict__ long_rows,
                                                                 uint32_t* nlong, uint32_t* maxrow) {
   __shared__ uint32_t s_warp[kScanThreads / 32];
@@ -130,14 +117,33 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
   if (tid == 0) s_chunk = atomicAdd(ticket, 1u);  // chunks start in ticket order
   __syncthreads();
   const uint32_t chunk = s_chunk;
-  const uint32_t r0 = chunk * (uint32_t)kChunk + (uint32_t)tid * kScanItems;
-  uint32_t v[kScanItems], sum = 0, vmax = 0;
+  const uint32_t r0 = chunk * (uint32_t)(kScanThreads * ITEMS) + (uint32_t)tid * ITEMS;
+  uint32_t v[ITEMS], sum = 0, vmax = 0;
+  if (ITEMS % 4 == 0 && r0 + ITEMS <= nrows) {  // whole thread range: 16-byte loads
 #pragma unroll
-  for (int q = 0; q < kScanItems; ++q) {
-    v[q] = r0 + q < nrows ? count[r0 + q] : 0u;
+    for (int q = 0; q < ITEMS; q += 4) {
+      const uint4 w = *reinterpret_cast<const uint4*>(count + r0 + q);
+      v[q] = w.x;
+      v[q + 1] = w.y;
+      v[q + 2] = w.z;
+      v[q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) v[q] = r0 + q < nrows ? count[r0 + q] : 0u;
+  }
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
     sum += v[q];
-    vmax = max(vmax, v[q]);
-    if (long_rows && v[q] > (uint32_t)kShortRow) long_rows[atomicAdd(nlong, 1u)] = r0 + q;
+    if (group == 1) {
+      vmax = max(vmax, v[q]);
+      if (long_rows && v[q] > (uint32_t)kShortRow) long_rows[atomicAdd(nlong, 1u)] = r0 + q;
+    }
+  }
+  if (group > 1) {  // the thread's ITEMS == group buckets are one grid row
+    vmax = sum;
+    if (long_rows && sum > (uint32_t)kShortRow && r0 < nrows)
+      long_rows[atomicAdd(nlong, 1u)] = r0 / (uint32_t)group;
   }
   vmax = __reduce_max_sync(0xffffffffu, vmax);
   if (maxrow && lane == 0) atomicMax(maxrow, vmax);  // densest row (spread batching mode)
@@ -190,8 +196,22 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
   }
   __syncthreads();
   uint32_t run = s_prefix + s_warp[warp] + x - sum;
+  if (ITEMS % 4 == 0 && r0 + ITEMS <= nrows) {  // whole thread range: 16-byte stores
 #pragma unroll
-  for (int q = 0; q < kScanItems; ++q) {
+    for (int q = 0; q < ITEMS; q += 4) {
+      uint4 w;
+      w.x = run;
+      w.y = w.x + v[q];
+      w.z = w.y + v[q + 1];
+      w.w = w.z + v[q + 2];
+      run = w.w + v[q + 3];
+      *reinterpret_cast<uint4*>(start + r0 + q) = w;
+    }
+    if (r0 + ITEMS == nrows) start[nrows] = run;
+    return;
+  }
+#pragma unroll
+  for (int q = 0; q < ITEMS; ++q) {
     if (r0 + q < nrows) {
       start[r0 + q] = run;
       run += v[q];
@@ -238,30 +258,6 @@ __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
   }
 }
 
-// K3, spread: the (key << 32 | index) pair at row start + rank (the rows'
-// stable order comes from K4, which also writes the weight records).
-__global__ void __launch_bounds__(kThreads) scatter_pairs_kernel(
-    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
-    uint32_t rowdiv, const uint32_t* __restrict__ start, unsigned long long* __restrict__ bpair) {
-  const uint32_t i0 = blockIdx.x * (kThreads * kPer) + threadIdx.x;
-  uint32_t key[kPer], rk[kPer], slot[kPer];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const uint32_t i = i0 + u * kThreads;
-    key[u] = i < n ? __ldg(keys + i) : 0u;
-    rk[u] = i < n ? __ldg(rank + i) : 0u;
-  }
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) slot[u] = __ldg(start + key[u] / rowdiv) + rk[u];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const uint32_t i = i0 + u * kThreads;
-    if (i < n) {
-      bpair[slot[u]] = ((unsigned long long)key[u] << 32) | i;  // one sector write per point
-    }
-  }
-}
-
 // The spread's 64-byte weight record of point i at sorted position o:
 //   {G phi_x(k-2-t_x)/h (k = 0..3), sin/cos(pi u_y/2), sin/cos(pi u_z/2)},
 // and its home cell along x (wrapped on periodic x).
@@ -296,77 +292,68 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
   write_record_from<D>(g, x, __ldg(G + i), o, rec, rcx);
 }
 
-// K4, rows up to kShortRow points: one thread per bucket slot ranks its
-// (key, index) among its row's pairs -- the row is read straight from the
-// bucket (contiguous, and shared by neighbouring lanes, so the loads are
-// L1 broadcasts) -- and writes the pair at the row's start + rank: stable
-// (key, index) order.  Its weight record goes to the row's start + its rank
-// in (x bank, key, index) order, and the row's kBanks-entry bank table is
-// filled.  Full warps whatever the row lengths.
+// K3, spread: each point's (key << 32 | index) pair at its (row, x bank)
+// bucket slot, start + arrival rank.
+__global__ void __launch_bounds__(kThreads) scatter_spread_kernel(
+    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
+    uint32_t rowdiv, const uint32_t* __restrict__ start, unsigned long long* __restrict__ bpair) {
+  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t key = __ldg(keys + i), row = key / rowdiv;
+  const uint32_t bucket = row * (uint32_t)kBanks + ((key - row * rowdiv) & (kBanks - 1));
+  bpair[__ldg(start + bucket) + __ldg(rank + i)] = ((unsigned long long)key << 32) | i;
+}
+
+// K4, one thread per bucket slot, ranking its (key, index) pair by counting
+// over a contiguous range of pairs (L1 broadcasts: neighbouring lanes share
+// it); the arrival order inside a bucket is not deterministic, the ranks are.
+//   mode 0, bank mode: range = its (row, x bank) bucket; the weight record
+//     goes to bucket start + rank -- records grouped by row and x bank, in
+//     (key, index) order inside a bank: all the bank-mode sweep needs;
+//   mode 0, pull mode: range = its row (<= kShortRow points, longer rows are
+//     K4b's); the pair goes to row start + rank (ws.keys / ws.perm) and the
+//     record with it;
+//   mode 1 (on request, ensure_observables): the row's sorted pairs only.
 template <int D>
 __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     const uint32_t* __restrict__ start, uint32_t n, const unsigned long long* __restrict__ bpair,
-    uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
-    DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
-    double* __restrict__ rec, int* __restrict__ rcx, uint32_t* __restrict__ rowbank,
-    const uint32_t* __restrict__ maxrow, uint32_t bank_rows) {
+    uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx, DevGrid g,
+    const double* __restrict__ X, const double* __restrict__ G, double* __restrict__ rec,
+    int* __restrict__ rcx, const uint32_t* __restrict__ maxrow, uint32_t bank_rows, int mode) {
   const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
   if (o >= n) return;
+  const bool banked = mode == 0 && bank_mode(*maxrow, bank_rows, g.rowdiv);
   const unsigned long long me = __ldg(bpair + o);
   const uint32_t k = (uint32_t)(me >> 32), ix = (uint32_t)me;
-  const uint32_t row = k / g.rowdiv, base = row * g.rowdiv;
-  const uint32_t a = __ldg(start + row), len = __ldg(start + row + 1) - a;
-  if (len > (uint32_t)kShortRow) return;  // long rows: K4b
+  const uint32_t row = k / g.rowdiv;
+  const uint32_t b0 = banked ? row * (uint32_t)kBanks + ((k - row * g.rowdiv) & (kBanks - 1))
+                             : row * (uint32_t)kBanks;
+  const uint32_t a = __ldg(start + b0);
+  const uint32_t len = __ldg(start + b0 + (banked ? 1 : kBanks)) - a;
+  if (!banked && len > (uint32_t)kShortRow) return;  // long rows: K4b
   // The point's position and value are gathered before the rank loop so
   // their latency hides behind it.
   double x[3] = {0.0, 0.0, 0.0};
+  double gv = 0.0;
+  if (mode == 0) {
 #pragma unroll
-  for (int d = 0; d < D; ++d) x[d] = __ldg(X + (size_t)ix * D + d);
-  const double gv = __ldg(G + ix);
-  // rk: rank in (key, index) order -- the sorted pairs.  When the sweep runs
-  // in bank mode (densest row <= bank_rows) the weight records go in (bank,
-  // key, index) order instead, bank = x cell mod 16, so that the sweep's
-  // lanes can take one bank each (ibc_spread.cuh); rb is that rank, lt the
-  // number of the row's points in lower banks, ceq the count in this bank.
-  const bool banked = bank_mode(*maxrow, bank_rows, g.rowdiv);
-  uint32_t rk = 0, rbe = 0, lt = 0, ceq = 0;
-  if (!banked) {
-    uint32_t j = 0;
-    for (; j + 4 <= len; j += 4) {
-      unsigned long long c[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = __ldg(bpair + a + j + u);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) rk += c[u] < me ? 1u : 0u;
-    }
-    for (; j < len; ++j)
-      rk += __ldg(bpair + a + j) < me ? 1u : 0u;
-  } else {
-    const uint32_t bk = (k - base) & (kBanks - 1);
-    auto visit = [&](unsigned long long cj) {
-      const uint32_t less = cj < me ? 1u : 0u;
-      const uint32_t bj = ((uint32_t)(cj >> 32) - base) & (kBanks - 1);
-      rk += less;
-      lt += bj < bk ? 1u : 0u;
-      ceq += bj == bk ? 1u : 0u;
-      rbe += bj == bk ? less : 0u;
-    };
-    uint32_t j = 0;
-    for (; j + 4 <= len; j += 4) {
-      unsigned long long c[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) c[u] = __ldg(bpair + a + j + u);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) visit(c[u]);
-    }
-    for (; j < len; ++j) visit(__ldg(bpair + a + j));
-    // Bank table of the row (zeroed beforehand): entry b = first record of
-    // bank b (relative) << 16 | its record count, written by the bank's first.
-    if (rbe == 0) rowbank[(size_t)row * kBanks + bk] = (lt << 16) | ceq;
+    for (int d = 0; d < D; ++d) x[d] = __ldg(X + (size_t)ix * D + d);
+    gv = __ldg(G + ix);
   }
-  skey[a + rk] = k;
-  sidx[a + rk] = ix;
-  write_record_from<D>(g, x, gv, a + (banked ? lt + rbe : rk), rec, rcx);
+  uint32_t rk = 0, j = 0;
+  for (; j + 4 <= len; j += 4) {
+    unsigned long long c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = __ldg(bpair + a + j + u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) rk += c[u] < me ? 1u : 0u;
+  }
+  for (; j < len; ++j) rk += __ldg(bpair + a + j) < me ? 1u : 0u;
+  if (!banked) {
+    skey[a + rk] = k;
+    sidx[a + rk] = ix;
+  }
+  if (mode == 0) write_record_from<D>(g, x, gv, a + rk, rec, rcx);
 }
 
 // K4b, long rows: one CTA per listed row, bitonic sort of (key << 32 | index)
@@ -378,20 +365,14 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     const uint32_t* __restrict__ nlong, const unsigned long long* __restrict__ bpair,
     uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
-    double* __restrict__ rec, int* __restrict__ rcx, uint32_t* __restrict__ rowbank,
-    const uint32_t* __restrict__ maxrow, uint32_t bank_rows) {
-  // [kLongSortMax] (key << 32 | index), then [kLongSortMax] record positions.
-  extern __shared__ unsigned long long sk[];
-  uint32_t* pos = reinterpret_cast<uint32_t*>(sk + kLongSortMax);
-  __shared__ uint32_t hist[kBanks], first[kBanks];
+    double* __restrict__ rec, int* __restrict__ rcx, const uint32_t* __restrict__ maxrow,
+    uint32_t bank_rows, int mode) {
+  extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
+  if (mode == 0 && bank_mode(*maxrow, bank_rows, g.rowdiv)) return;
   const uint32_t count = *nlong;
-  const bool banked = bank_mode(*maxrow, bank_rows, g.rowdiv);
-  const int lane = threadIdx.x & 31;
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = long_rows[li];
-    const uint32_t a = start[r], len = start[r + 1] - a;
-    const uint32_t base = r * g.rowdiv;
-    auto bank_of = [&](unsigned long long c) { return ((uint32_t)(c >> 32) - base) & (kBanks - 1); };
+    const uint32_t a = start[(size_t)r * kBanks], len = start[(size_t)r * kBanks + kBanks] - a;
     if (len <= (uint32_t)kLongSortMax) {
       uint32_t m = 1;
       while (m < len) m <<= 1;
@@ -415,61 +396,21 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
           __syncthreads();
         }
       }
-      if (banked) {
-        // Record positions in (bank, key, index) order: a stable partition
-        // of the sorted row by bank, walked by warp 0 in 32-element chunks.
-        if (threadIdx.x < kBanks) hist[threadIdx.x] = 0;
-        __syncthreads();
-        for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) atomicAdd(&hist[bank_of(sk[e])], 1u);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          uint32_t acc = 0;
-          for (int b = 0; b < kBanks; ++b) {
-            first[b] = acc;
-            rowbank[(size_t)r * kBanks + b] = (acc << 16) | hist[b];
-            acc += hist[b];
-          }
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-          for (uint32_t c0 = 0; c0 < len; c0 += 32) {
-            const uint32_t e = c0 + lane;
-            const uint32_t b = e < len ? bank_of(sk[e]) : 0x100u + lane;
-            const uint32_t peers = __match_any_sync(0xffffffffu, b);
-            if (e < len) {
-              pos[e] = first[b] + __popc(peers & ((1u << lane) - 1u));
-            }
-            __syncwarp();
-            if (e < len && (peers & ((1u << lane) - 1u)) == 0) first[b] += __popc(peers);
-            __syncwarp();
-          }
-        }
-        __syncthreads();
-      }
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
         skey[a + e] = (uint32_t)(sk[e] >> 32);
         sidx[a + e] = (uint32_t)sk[e];
-        write_record<D>(g, X, G, (uint32_t)sk[e], a + (banked ? pos[e] : e), rec, rcx);
+        if (mode == 0) write_record<D>(g, X, G, (uint32_t)sk[e], a + e, rec, rcx);
       }
       __syncthreads();
     } else {
       // Very long row: rank every element by counting (correct, quadratic).
       for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
         const unsigned long long ce = bpair[a + e];
-        const uint32_t be = bank_of(ce);
-        uint32_t rk = 0, rb = 0, lt = 0, ceq = 0;
-        for (uint32_t f = 0; f < len; ++f) {
-          const unsigned long long cf = bpair[a + f];
-          const uint32_t less = cf < ce ? 1u : 0u, bf = bank_of(cf);
-          rk += less;
-          lt += bf < be ? 1u : 0u;
-          ceq += bf == be ? 1u : 0u;
-          rb += bf == be ? less : 0u;
-        }
+        uint32_t rk = 0;
+        for (uint32_t f = 0; f < len; ++f) rk += bpair[a + f] < ce ? 1u : 0u;
         skey[a + rk] = (uint32_t)(ce >> 32);
         sidx[a + rk] = (uint32_t)ce;
-        write_record<D>(g, X, G, (uint32_t)ce, a + (banked ? lt + rb : rk), rec, rcx);
-        if (banked && rb == 0) rowbank[(size_t)r * kBanks + be] = (lt << 16) | ceq;
+        if (mode == 0) write_record<D>(g, X, G, (uint32_t)ce, a + rk, rec, rcx);
       }
     }
   }

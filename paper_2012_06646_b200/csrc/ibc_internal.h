@@ -50,10 +50,11 @@ struct PointScratch {
   DevBuf<uint32_t> rowstart;
   DevBuf<uint32_t> rowaux;  // bucket sort: row counts | scan status | ticket | long rows
   DevBuf<uint32_t> smap;    // bucket sort: sorted position -> record slot
-  DevBuf<uint32_t> rowbank; // bucket sort: per row and x bank, first record << 16 | count
   DevBuf<unsigned long long> bpair;  // bucket sort: (key << 32 | index) in row buckets
   const uint32_t* maxrow = nullptr;  // bucket sort: largest row count (device)
   uint32_t bank_rows = 0;            // spread: bank-mode row threshold (bucket::bank_mode)
+  bool obs_pending = false;          // spread: ws.keys / ws.perm not materialised yet
+  DevGrid obs_grid{};                // spread: the grid of the last spread (for them)
   DevBuf<int> rec_cx;
   DevBuf<double> rec;         // 12 x cap weight records (spread)
   DevBuf<uint32_t> run_keys;  // lazily filled
@@ -105,6 +106,8 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field,
                      const double* d_points, size_t n, PointScratch& s, double* d_out);
 // ws.run_keys on the device; returns q (synchronizes).
 size_t compute_run_keys(Context& ctx, PointScratch& s);
+// The stable (key, index) order of the last spread (ws.keys / ws.perm), on request.
+void ensure_observables(Context& ctx, PointScratch& s);
 size_t read_run_count(Context& ctx, PointScratch& s);
 
 }  // namespace ibc

@@ -616,7 +616,6 @@ void PointScratch::release_all() {
   hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
   smap.release();
-  rowbank.release();
   bpair.release();
   cap = 0;
 }
@@ -640,6 +639,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
   T.wpc = wpc;
   T.rl = rl;
   T.pull_row = sp::pull_row();
+  T.group = bucket::kBanks;
   const int rows_per_cta = wpc * rows_per_warp;
   T.nyg = (ny + rows_per_cta - 1) / rows_per_cta;
   if (g.dim == 3) {
@@ -681,6 +681,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
       s.keys_are_rows = false;
     }
     row_table(ctx, g, n, s);
+    W.group = WB.group = 1;  // one row-start entry per row
   }
   const uint32_t* smap = nullptr;  // records are in sorted order on both sort paths
   cudaEvent_t ev = nullptr;
@@ -714,7 +715,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     auto launch = [&](auto bank_k, auto pull_k) {
       if (maxrow && WB.pull_row != bucket::kNoBankMode) {
         bank_k<<<blocks_b, 32 * WB.wpc, smem_b, st>>>(g, WB, maxrow, s.rowstart.p, s.rec.p,
-                                                      s.rec_cx.p, s.rowbank.p, d_out);
+                                                      s.rec_cx.p, d_out);
         ++ctx.launches;
       }
       pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
@@ -840,87 +841,121 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
 }  // namespace tma
 
 namespace {
-// Row bucket sort (ibc_bucket.cuh).  Interpolation: records {x, y, z, index}
-// in s.rec grouped by row.  Spread: the weight records (s.rec, s.rec_cx) in
-// bucket slots, plus the stable key order -- s.sorted_keys / s.sorted_perm
-// (the reference's ws.keys / ws.perm) and s.smap (sorted position -> slot).
+// K3 over the spread buckets.
+void launch_scatter_spread(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
+  bucket::scatter_spread_kernel<<<grid_for(n, bucket::kThreads), bucket::kThreads, 0, ctx.stream>>>(
+      s.keys[1].p, s.vals[1].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.bpair.p);
+  ++ctx.launches;
+}
+
+// K4 / K4b over the spread buckets: mode 0 inside the spread (pull mode:
+// sorted pairs + records), mode 1 on request (sorted pairs only).
+void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
+                      const double* d_values, size_t n, PointScratch& s, int mode) {
+  cudaStream_t st = ctx.stream;
+  const uint32_t* maxrow = s.maxrow;
+  uint32_t* nlong = const_cast<uint32_t*>(maxrow) - 1;
+  const uint32_t* long_rows = maxrow + 1;
+  static bool attr_set[64] = {};
+  const size_t lsm = (size_t)bucket::kLongSortMax * 8;
+  if (!attr_set[ctx.device & 63]) {
+    IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<2>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<3>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
+    attr_set[ctx.device & 63] = true;
+  }
+  auto sorts = [&](auto short_k, auto long_k) {
+    short_k<<<grid_for(n, bucket::kThreads), bucket::kThreads, 0, st>>>(
+        s.rowstart.p, (uint32_t)n, s.bpair.p, s.keys[0].p, s.vals[0].p, g, d_points, d_values,
+        s.rec.p, s.rec_cx.p, maxrow, s.bank_rows, mode);
+    long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.bpair.p,
+                                                   s.keys[0].p, s.vals[0].p, g, d_points,
+                                                   d_values, s.rec.p, s.rec_cx.p, maxrow,
+                                                   s.bank_rows, mode);
+  };
+  if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
+  else sorts(bucket::row_sort_kernel<2>, bucket::long_row_sort_kernel<2>);
+  ctx.launches += 2;
+}
+
+// Bucket sort (ibc_bucket.cuh).  Interpolation: records grouped by row.
+// Spread: points bucketed by (row, x bank); in bank mode the weight records
+// are written straight into the buckets, in pull mode K4 puts them in the
+// rows' key order.  The stable (key, index) order the reference exposes as
+// ws.keys / ws.perm is materialised on request (ensure_observables).
 void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
                    size_t n, PointScratch& s, bool spread) {
   cudaStream_t st = ctx.stream;
   const uint32_t nrows = g.nrows;
-  const uint32_t nchunks = (nrows + bucket::kChunk - 1) / bucket::kChunk;
-  s.rowaux.ensure(2 * (size_t)nrows + nchunks + 8);
+  const int group = spread ? bucket::kBanks : 1;     // buckets per grid row
+  const uint32_t nb = nrows * (uint32_t)group;       // buckets
+  const uint32_t chunk = bucket::kScanThreads * (spread ? bucket::kBanks : bucket::kScanItems);
+  const uint32_t nchunks = (nb + chunk - 1) / chunk;
+  s.rowaux.ensure((size_t)nb + nchunks + 8 + nrows);
+  s.rowstart.ensure((size_t)nb + 1);
   uint32_t* count = s.rowaux.p;
-  uint32_t* status = count + nrows;
+  uint32_t* status = count + nb;
   uint32_t* ticket = status + nchunks;
   uint32_t* nlong = ticket + 1;
   uint32_t* maxrow = nlong + 1;
   uint32_t* long_rows = maxrow + 1;
-  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nrows + nchunks + 3) * 4, st));
+  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nb + nchunks + 3) * 4, st));
   s.maxrow = spread ? maxrow : nullptr;  // (zeroed above; set by the row scan)
   if (n == 0) {
-    IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)nrows + 1) * 4, st));
+    IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)nb + 1) * 4, st));
+    if (spread) {
+      s.last_n = 0;
+      s.obs_pending = false;
+    }
     return;
   }
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfKeys, &ev);
   const unsigned blocks = grid_for(n, bucket::kThreads);
-  const unsigned pblocks = grid_for(n, bucket::kThreads * bucket::kPer);  // K1 / K3
   const int full = spread ? 1 : 0;
+  // Input-order keys and ranks: buffers 1 for the spread (buffers 0 receive
+  // the sorted keys / permutation), 0 for interpolation.
+  uint32_t* ikeys = s.keys[spread ? 1 : 0].p;
+  uint32_t* irank = s.vals[spread ? 1 : 0].p;
   if (g.dim == 3)
-    bucket::keys_kernel<3><<<pblocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
-                                                                s.keys[0].p, s.vals[0].p, count);
+    bucket::keys_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full, group,
+                                                               ikeys, irank, count);
   else if (g.dim == 2)
-    bucket::keys_kernel<2><<<pblocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
-                                                                s.keys[0].p, s.vals[0].p, count);
+    bucket::keys_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full, group,
+                                                               ikeys, irank, count);
   else
-    bucket::keys_kernel<1><<<pblocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full,
-                                                                s.keys[0].p, s.vals[0].p, count);
+    bucket::keys_kernel<1><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full, group,
+                                                               ikeys, irank, count);
   ctx.prof_end(kProfKeys, ev);
   ctx.prof_begin(kProfSort, &ev);
-  bucket::row_scan_kernel<<<nchunks, bucket::kScanThreads, 0, st>>>(
-      count, s.rowstart.p, nrows, status, ticket, spread ? long_rows : nullptr, nlong, maxrow);
+  if (spread)
+    bucket::row_scan_kernel<bucket::kBanks><<<nchunks, bucket::kScanThreads, 0, st>>>(
+        count, s.rowstart.p, nb, group, status, ticket, long_rows, nlong, maxrow);
+  else
+    bucket::row_scan_kernel<bucket::kScanItems><<<nchunks, bucket::kScanThreads, 0, st>>>(
+        count, s.rowstart.p, nb, group, status, ticket, nullptr, nlong, maxrow);
   ctx.launches += 2;
   if (!spread) {
     if (g.dim == 3)
-      bucket::scatter_interp_kernel<3><<<pblocks, bucket::kThreads, 0, st>>>(
+      bucket::scatter_interp_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
           g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     else
-      bucket::scatter_interp_kernel<2><<<pblocks, bucket::kThreads, 0, st>>>(
+      bucket::scatter_interp_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
           g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
-    s.rowbank.ensure((size_t)nrows * bucket::kBanks);
     s.bpair.ensure(n);
-    IBC_CUDA(cudaMemsetAsync(s.rowbank.p, 0, (size_t)nrows * bucket::kBanks * 4, st));
-    bucket::scatter_pairs_kernel<<<pblocks, bucket::kThreads, 0, st>>>(
-        s.keys[0].p, s.vals[0].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.bpair.p);
-    static bool attr_set[64] = {};
-    const size_t lsm = (size_t)bucket::kLongSortMax * 12;  // keys + record positions
-    if (!attr_set[ctx.device & 63]) {
-      IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<2>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-      IBC_CUDA(cudaFuncSetAttribute(bucket::long_row_sort_kernel<3>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lsm));
-      attr_set[ctx.device & 63] = true;
-    }
-    auto sorts = [&](auto short_k, auto long_k) {
-      short_k<<<blocks, bucket::kThreads, 0, st>>>(s.rowstart.p, (uint32_t)n, s.bpair.p,
-                                                   s.keys[0].p, s.vals[0].p, g,
-                                                   d_points, d_values, s.rec.p, s.rec_cx.p,
-                                                   s.rowbank.p, maxrow, s.bank_rows);
-      long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.bpair.p,
-                                                     s.keys[0].p, s.vals[0].p, g, d_points,
-                                                     d_values, s.rec.p, s.rec_cx.p, s.rowbank.p,
-                                                     maxrow, s.bank_rows);
-    };
-    if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
-    else sorts(bucket::row_sort_kernel<2>, bucket::long_row_sort_kernel<2>);
-    ctx.launches += 3;
+    launch_scatter_spread(ctx, g, n, s);
+    // Records: in (row, x bank) buckets (bank mode) or the rows' key order
+    // (pull mode, K4b for the long rows; it exits at once in bank mode).
+    launch_row_sorts(ctx, g, d_points, d_values, n, s, 0);
     s.sorted_keys = s.keys[0].p;
     s.sorted_perm = s.vals[0].p;
     s.last_n = n;
+    s.obs_pending = true;
+    s.obs_grid = g;
     s.run_keys_valid = false;
     s.keys_are_rows = false;
   }
@@ -978,9 +1013,18 @@ void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, cons
 
 // ws.run_keys and ws.run_count (= q) on the device, computed on demand from
 // the sorted keys (reduce.hpp:36-69); cached until the next sort.
+void ensure_observables(Context& ctx, PointScratch& s) {
+  if (!s.obs_pending || !s.last_n) return;
+  launch_row_sorts(ctx, s.obs_grid, nullptr, nullptr, s.last_n, s, 1);
+  IBC_CUDA(cudaGetLastError());
+  s.obs_pending = false;
+  s.run_keys_valid = false;
+}
+
 size_t compute_run_keys(Context& ctx, PointScratch& s) {
   const size_t n = s.last_n;
   if (n == 0) return 0;
+  ensure_observables(ctx, s);
   cudaStream_t st = ctx.stream;
   if (!s.run_keys_valid) {
     const unsigned nb = grid_for(n, kBlock);

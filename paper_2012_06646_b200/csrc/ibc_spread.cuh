@@ -51,7 +51,8 @@ struct SweepTiling {
   int wpc;       // warps (target rows) per CTA
   int nyg;       // CTAs along y
   int zc, nzc;   // z-chunk length, chunks
-  int rl;        // doubles per window row (padded + skewed, even)
+  int rl;        // doubles per window row (padded, even)
+  int group;     // row start table entries per grid row (kBanks: bucket sort; 1: radix path)
   uint32_t pull_row;  // densest row above which batches pull instead of defer
 };
 
@@ -65,18 +66,17 @@ __host__ __device__ constexpr int row_len(int nx) {
 // Bank mode: one source plane for the kRowsPerWarp target rows of a warp,
 // GS = kBanks lanes per row.  Lane b of a row's group owns x bank b (x cell
 // mod kBanks, up to a fixed shift) and walks that bank's records of the row's
-// four source rows in order (records are bank-ordered within a row, with a
-// kBanks-entry (first, count) table per row, ibc_bucket.cuh K4).  A half-warp
+// four source rows in order (records sit in (row, x bank) buckets,
+// ibc_bucket.cuh K1-K3; bstart is the bucket start table).  A half-warp
 // holds 16 / kBanks rows whose windows are interleaved element by element
 // (stride ES = 16 / kBanks), so within a half the cells of one instruction's
 // adds hit distinct bank pairs -- and distinct addresses, even across the kx
 // phases of one point: conflict-free, no collision test.  Lane gb + j (j <
-// 4, gb = the group's first lane) holds source row j's sorted start rb,
-// length len and row id rid for the group's target row.
+// 4, gb = the group's first lane) holds source row j's length len and row id
+// rid for the group's target row.
 template <int D, int RL, int R>
-__device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t rb,
-                                           uint32_t len, uint32_t rid,
-                                           const uint32_t* __restrict__ rowbank,
+__device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t len,
+                                           uint32_t rid, const uint32_t* __restrict__ bstart,
                                            const double* __restrict__ rec,
                                            const int* __restrict__ rcx, double q) {
   constexpr int GS = bucket::kBanks, ES = 16 / GS;
@@ -84,12 +84,16 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
   uint32_t lo[4], c[4], cnt = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t rbj = __shfl_sync(0xffffffffu, rb, gb + j);
     const uint32_t lenj = __shfl_sync(0xffffffffu, len, gb + j);
     const uint32_t ridj = __shfl_sync(0xffffffffu, rid, gb + j);
-    const uint32_t e = lenj ? __ldg(rowbank + (size_t)ridj * GS + bank) : 0u;  // first << 16 | count
-    lo[j] = rbj + (e >> 16) - cnt;  // sorted position of this lane's k-th record = lo[j] + k
-    cnt += e & 0xffffu;
+    uint32_t b0 = 0, b1 = 0;  // this lane's (row, bank) bucket of source row j
+    if (lenj) {
+      const uint32_t* t = bstart + (size_t)ridj * GS + bank;
+      b0 = __ldg(t);
+      b1 = __ldg(t + 1);
+    }
+    lo[j] = b0 - cnt;  // record slot of this lane's k-th record = lo[j] + k
+    cnt += b1 - b0;
     c[j] = cnt;
   }
   const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
@@ -286,8 +290,8 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
       else ok = cy >= -1 && cy <= ny;
       if (ok) {
         rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
-        rb = __ldg(rowstart + rid);
-        len = __ldg(rowstart + rid + 1) - rb;
+        rb = __ldg(rowstart + (size_t)rid * T.group);  // row = T.group buckets
+        len = __ldg(rowstart + (size_t)rid * T.group + T.group) - rb;
       }
     }
   };
@@ -367,10 +371,9 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
 template <int D, int RL>
 __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling T,
                                                           const uint32_t* __restrict__ maxrow,
-                                                          const uint32_t* __restrict__ rowstart,
+                                                          const uint32_t* __restrict__ bstart,
                                                           const double* __restrict__ rec,
                                                           const int* __restrict__ rcx,
-                                                          const uint32_t* __restrict__ rowbank,
                                                           double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
   if (!bucket::bank_mode(*maxrow, T.pull_row, g.rowdiv)) return;  // pull mode
@@ -411,8 +414,8 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
       else ok = cy >= -1 && cy <= ny;
       if (ok) {
         rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
-        rb = __ldg(rowstart + rid);
-        len = __ldg(rowstart + rid + 1) - rb;
+        rb = __ldg(bstart + (size_t)rid * GS);  // a row's kBanks buckets
+        len = __ldg(bstart + (size_t)rid * GS + GS) - rb;
       }
     }
   };
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
   ranges(s_lo, rb_n, len_n, rid_n);
 
   for (int s = s_lo; s <= s_hi; ++s) {
-    const uint32_t rb = rb_n, len = len_n, rid = rid_n;
+    const uint32_t len = len_n, rid = rid_n;  // (rb_n: unused, the buckets give the slots)
     ranges(s + 1, rb_n, len_n, rid_n);
     int so[4];
 #pragma unroll
@@ -431,13 +434,13 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
     const bool interior = D == 3 && s - 2 >= z0 && s + 1 < z1;
     if (RL > 0 && interior) {
       switch (s & 3) {
-        case 0: plane_banks<D, RL, 0>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-        case 1: plane_banks<D, RL, 1>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-        case 2: plane_banks<D, RL, 2>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
-        default: plane_banks<D, RL, 3>(W, so, rb, len, rid, rowbank, rec, rcx, q); break;
+        case 0: plane_banks<D, RL, 0>(W, so, len, rid, bstart, rec, rcx, q); break;
+        case 1: plane_banks<D, RL, 1>(W, so, len, rid, bstart, rec, rcx, q); break;
+        case 2: plane_banks<D, RL, 2>(W, so, len, rid, bstart, rec, rcx, q); break;
+        default: plane_banks<D, RL, 3>(W, so, len, rid, bstart, rec, rcx, q); break;
       }
     } else {
-      plane_banks<D, RL, -1>(W, so, rb, len, rid, rowbank, rec, rcx, q);
+      plane_banks<D, RL, -1>(W, so, len, rid, bstart, rec, rcx, q);
     }
     // Target plane s - 2 has all its sources: fold, store once, clear.
     const int t = D == 3 ? s - 2 : 0;
