@@ -49,7 +49,6 @@ struct PointScratch {
   DevBuf<uint32_t> hist, base, counters;  // per-tile digit histograms, digit totals
   DevBuf<uint32_t> rowstart;
   DevBuf<uint32_t> rowaux;  // bucket sort: row counts | scan status | ticket | long rows
-  DevBuf<uint32_t> smap;    // bucket sort: sorted position -> record slot
   DevBuf<unsigned long long> bpair;  // bucket sort: (key << 32 | index) in row buckets
   const uint32_t* maxrow = nullptr;  // bucket sort: largest row count (device)
   uint32_t bank_rows = 0;            // spread: bank-mode row threshold (bucket::bank_mode)

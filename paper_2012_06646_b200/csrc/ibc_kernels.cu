@@ -615,7 +615,6 @@ void PointScratch::release_all() {
   }
   hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
-  smap.release();
   bpair.release();
   cap = 0;
 }
@@ -683,7 +682,6 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     row_table(ctx, g, n, s);
     W.group = WB.group = 1;  // one row-start entry per row
   }
-  const uint32_t* smap = nullptr;  // records are in sorted order on both sort paths
   cudaEvent_t ev = nullptr;
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
@@ -718,7 +716,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                                                       s.rec_cx.p, d_out);
         ++ctx.launches;
       }
-      pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, smap, s.rec.p,
+      pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, s.rec.p,
                                                s.rec_cx.p, d_out);
     };
     const int nx = g.n[0];

@@ -1,33 +1,34 @@
-// ibc_spread.cuh -- write-once spreading sweep (sm_100a), 2-D and 3-D grids.
+// ibc_spread.cuh -- write-once spreading sweeps (sm_100a), 2-D and 3-D grids.
 //
 // Replaces ib::spread_fused (spread.hpp:165-216, Alg. 4): the same operator
 // l_m = sum_sigma sum_{p in cell(m - sigma)} w_sigma(t_p) G_p, with every grid
 // value written to HBM exactly once and no global atomics.
 //
-// Inputs: the points in stable cell-key order (ibc_bucket.cuh / ibc_sort.cuh),
-// each with a 64-byte weight record -- G * phi_x(k-2-t_x)/h for k = 0..3 and
-// sin/cos(pi u / 2) of the y and z displacements -- and its home cell along x;
-// and the row start table (rows of the sorted keys are contiguous).
+// Inputs: each point's 64-byte weight record -- G * phi_x(k-2-t_x)/h for
+// k = 0..3 and sin/cos(pi u / 2) of the y and z displacements -- and its
+// home cell along x, grouped by home row (ibc_bucket.cuh / ibc_sort.cuh), and
+// the start table of those groups.
 //
-// Each warp owns ONE target row (ty) of a z-chunk [z0, z1) and sweeps the
-// source planes z0-1 .. z1+1.  Its private shared-memory window holds the row
-// in the four target planes a source plane reaches (s-2 .. s+1), padded and
-// skewed (x index xi lives at xi + xi/16, so points ~16 cells apart hit
-// distinct banks).  For source plane s the warp pulls the points of the four
-// source rows that reach ty (cy = ty+2 .. ty-1, concatenated into full
-// 32-lane batches) and adds their 16 contributions (4 x 4 z) per lane.
-// Lanes that share a home cx -- same cell, or different source rows -- would
-// hit the same addresses.  Sparse points: all but the first (match_any) are
-// deferred to the next batch.  Dense / clustered points: the group's lowest
-// lane gathers the others' contributions by shuffles and adds alone.  Either
-// way adds never collide and the summation order is the sequence order --
-// results are bitwise reproducible.  When plane
-// s is done, target plane s-2 is complete: the warp folds the periodic x pad,
+// Warps own target rows of a z-chunk [z0, z1) and sweep the source planes
+// z0-1 .. z1+1.  A warp's private shared-memory window holds its rows in the
+// four target planes a source plane reaches (s-2 .. s+1), padded by 4 cells
+// left and 2 right for the periodic fold.  For source plane s the warp takes
+// the points of the four source rows that reach each target row (cy = ty+2 ..
+// ty-1) and adds their 16 contributions (4 x x 4 z) per lane.  When plane s is
+// done, target plane s-2 is complete: the warp folds the periodic x pad,
 // stores the row once (coalesced) and clears the slot for plane s+2.  No CTA
-// barrier anywhere: warps are independent, which is what lets 24 of them per
-// SM hide the record loads.  The inner loop is kept lean (the kernel is
-// issue-bound): per-plane slot offsets are hoisted, weights are a handful of
-// FMAs, deferral compaction is a popc binary search.
+// barrier anywhere: warps are independent.
+//
+// Two ways to keep a lane's read-modify-writes from colliding, picked on the
+// device from the densest row (bucket::bank_mode):
+//  * bank mode (spread_banks_kernel): a target row per half-warp; lane b owns
+//    x cells = b mod 16 and walks that bank's records (records sit in
+//    (row, x bank) buckets), so one instruction's adds hit 16 distinct bank
+//    pairs -- conflict-free and collision-free by construction;
+//  * pull mode (spread_sweep_kernel): a target row per warp, 32 consecutive
+//    records per batch; lanes with the same home cx are summed into their
+//    group's lowest lane by shuffles, which adds alone.
+// Either way the summation order is fixed by the data: bitwise reproducible.
 #pragma once
 #include <cstdint>
 #include <cstdlib>
@@ -53,10 +54,8 @@ struct SweepTiling {
   int zc, nzc;   // z-chunk length, chunks
   int rl;        // doubles per window row (padded, even)
   int group;     // row start table entries per grid row (kBanks: bucket sort; 1: radix path)
-  uint32_t pull_row;  // densest row above which batches pull instead of defer
+  uint32_t pull_row;  // bucket::bank_mode threshold (kNoBankMode: pull mode only)
 };
-
-__device__ __forceinline__ int skew(int xi) { return xi; }
 
 // Doubles per window row for nx: padded, even (16-byte aligned rows).
 __host__ __device__ constexpr int row_len(int nx) {
@@ -159,7 +158,7 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
 template <int D, int RL, int R>
 __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const int so[4], uint32_t e0,
                                               uint32_t e1, uint32_t e2, uint32_t total,
-                                              uint32_t rstart, const uint32_t* __restrict__ smap,
+                                              uint32_t rstart,
                                               const double* __restrict__ rec,
                                               const int* __restrict__ rcx, double q) {
   const int lane = threadIdx.x & 31;
@@ -171,7 +170,7 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
     int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
     double2 g01 = make_double2(0.0, 0.0), g23 = g01, tr = g01, tz2 = g01;
     if (valid) {
-      const uint32_t r = smap ? __ldg(smap + rs) : rs;  // record slot of sorted position rs
+      const uint32_t r = rs;  // record slot = sorted position
       const double4 ga = ld_v4_nc(rec + 8 * (size_t)r), gb = ld_v4_nc(rec + 8 * (size_t)r + 4);
       g01 = make_double2(ga.x, ga.y);
       g23 = make_double2(ga.z, ga.w);
@@ -227,7 +226,7 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
 #pragma unroll
     for (int kx = 0; kx < 4; ++kx) {
       if (lead) {
-        double* wa = W + skew(xb + kx);
+        double* wa = W + (xb + kx);
         if (R >= 0) {
 #pragma unroll
           for (int kz = 0; kz < 4; ++kz) wa[((R + kz + 2) & 3) * RL] += v[kx][kz];
@@ -251,7 +250,6 @@ template <int D, int RL>
 __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTiling T,
                                                            const uint32_t* __restrict__ maxrow,
                                                            const uint32_t* __restrict__ rowstart,
-                                                           const uint32_t* __restrict__ smap,
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
@@ -324,13 +322,13 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
         // path: slot offsets are immediates, no per-add range checks.
         if (RL > 0 && interior) {
           switch (s & 3) {
-            case 0: plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-            case 1: plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-            case 2: plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
-            default: plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q); break;
+            case 0: plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
+            case 1: plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
+            case 2: plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
+            default: plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
           }
         } else {
-          plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, smap, rec, rcx, q);
+          plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, rec, rcx, q);
         }
       }
     }
@@ -341,17 +339,17 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
       double* orow = out + ((size_t)t * ny + ty) * nx;
       if (px && nx < 8) {
         for (int x = lane; x < nx; x += 32) {
-          double v = Wr[skew(x + kPadL)];
-          for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[skew(qx + kPadL)];
-          for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[skew(qx + kPadL)];
+          double v = Wr[(x + kPadL)];
+          for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[(qx + kPadL)];
+          for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[(qx + kPadL)];
           orow[x] = v;
         }
       } else {
         for (int x = lane; x < nx; x += 32) {
-          double v = Wr[skew(x + kPadL)];
+          double v = Wr[(x + kPadL)];
           if (px) {  // pads x' = -4..-1 fold onto nx-4.., x' = nx, nx+1 onto 0, 1
-            if (x >= nx - kPadL) v += Wr[skew(x - nx + kPadL)];
-            if (x < kPadR) v += Wr[skew(x + nx + kPadL)];
+            if (x >= nx - kPadL) v += Wr[(x - nx + kPadL)];
+            if (x < kPadR) v += Wr[(x + nx + kPadL)];
           }
           orow[x] = v;
         }
