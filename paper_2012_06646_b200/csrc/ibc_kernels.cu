@@ -806,7 +806,7 @@ bool interp_tma_tiling(const DevGrid& g, size_t n, sw::InterpTiling& T) {
   if (!found) return false;
   T.pitch = pitch;
   T.slot_bytes = (uint32_t)T.frmax * pitch;
-  T.box_ok = nx % 128 == 0 ? 1 : 0;  // box rows keep the 128B-swizzle phase
+  T.box_ok = nx % 128 == 0 ? 1 : 0;  // box rows land at the slot pitch (1024-byte multiple)
   return true;
 }
 
@@ -833,7 +833,7 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
   const cuuint32_t box[4] = {16, (cuuint32_t)(nx / 16), (cuuint32_t)box_rows, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
   return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(field), dims, strides, box,
-            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace tma

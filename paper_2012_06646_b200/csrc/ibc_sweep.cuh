@@ -9,7 +9,7 @@
 // and sweeps its home planes in order.  The field planes a home plane s needs
 // (s-2 .. s+1, rows y0-2 .. y0+TY) live in a ring of `slots` shared-memory
 // slots.  A dedicated producer warp fills slot i % slots with field plane i --
-// one TMA tensor load per plane (128-byte swizzle; per field row where the
+// one TMA tensor load per plane (unswizzled rows; per field row where the
 // rows wrap around a periodic y boundary), plus one bulk copy of the point
 // records of the step that plane completes -- and signals a `full` mbarrier.
 // Periodic rows/planes are wrapped by the producer; non-periodic ones fall
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
         wxk = 0.0;  // off the closed grid: the reference skips the term
         x = 0;
       }
-      const uint32_t xo = tma::swz128(x) + (uint32_t)(valid ? cy - hy0 : 0) * T.pitch;
+      const uint32_t xo = (uint32_t)x * 8u + (uint32_t)(valid ? cy - hy0 : 0) * T.pitch;
       double acc = 0.0;
       if (valid) {
         // Pairwise sums (dependency depth 6 instead of 20 fused multiply-adds).

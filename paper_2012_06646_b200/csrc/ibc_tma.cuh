@@ -88,18 +88,10 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
       : "memory");
 }
 
-// Byte offset of double x inside a 1024-byte-aligned row written by a TMA box
-// with CU_TENSOR_MAP_SWIZZLE_128B: 16-byte chunk c of 128-byte line L lands at
-// chunk c ^ (L & 7).  Rows are placed at multiples of 1024 bytes, so L & 7
-// depends on x alone.
-__device__ __forceinline__ uint32_t swz128(int x) {
-  const uint32_t line = (uint32_t)x >> 4, chunk = ((uint32_t)x >> 1) & 7u;
-  return (line << 7) | ((chunk ^ (line & 7u)) << 4) | (((uint32_t)x & 1u) << 3);
-}
-
 // Host: field rows of an (nx, ny, nz) colex FP64 grid as a 4-D tensor
-// (16, nx/16, ny, nz) with a one-row box (16, nx/16, 1, 1), 128-byte swizzle,
-// zero fill out of bounds.  Requires nx % 16 == 0, nx <= 4096.
+// (16, nx/16, ny, nz) with a box of box_rows rows (16, nx/16, box_rows, 1), no
+// swizzle (the gather's bank pattern depends on x only either way; measured
+// a little faster unswizzled), zero fill out of bounds.  Requires nx % 16 == 0, nx <= 4096.
 bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz, int box_rows = 1);
 
 }  // namespace tma
