@@ -223,32 +223,47 @@ def run_ours(args):
     E = torch.empty(n, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
-    def step():
-        if dec is None:
-            ops.spread(xs, gv, grid, out=ell)
-            ops.interpolate(fe, xn, grid, out=E)
-        else:
-            dec.spread(xs, gv)
-            dec.interpolate(fe, xn)
+    if dec is not None:
+        local_out = torch.empty(dec.local.point_count(), dtype=torch.float64, device=dev)
+        field_local = torch.empty(dec.local.point_count(), dtype=torch.float64, device=dev)
+    # The device-side pieces of a step: both operators on one GPU; for slabs
+    # the local spread and the local gather, with the NCCL ghost-plane sum and
+    # halo fill between them (eager: they go through torch.distributed).
+    local_ops = [(lambda: (ops.spread(xs, gv, grid, out=ell), ops.interpolate(fe, xn, grid, out=E)))] \
+        if dec is None else [lambda: dec._device_spread(xs, gv, out=local_out),
+                             lambda: dec._device_interpolate(field_local, xn, out=E)]
+    graphs = [None] * len(local_ops)
+
+    def step(eager=False):
+        def run(k):
+            if graphs[k] is not None and not eager:
+                graphs[k].replay()
+            else:
+                local_ops[k]()
+
+        run(0)
+        if dec is not None:
+            dec.ghost_sum(local_out)
+            dec.halo_fill(fe, out=field_local)
+            run(1)
 
     for i in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    # Single GPU: the step (both operators, every sort/record/sweep kernel
-    # and memset) is captured once in a CUDA graph and replayed -- no host
-    # round trip inside the pipeline, so it captures as is.  Slabs (N > 1)
-    # run eagerly (the exchange goes through torch.distributed).
-    graph = None
     l0 = ops.launches
     step()
     torch.cuda.synchronize()
     launches_per_step = ops.launches - l0
-    if world == 1 and not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step()
-        graph.replay()
+    # Every kernel and memset of the operators is captured once in a CUDA
+    # graph and replayed (the pipeline has no host round trip).
+    if not args.no_graph:
+        for k, f in enumerate(local_ops):
+            graphs[k] = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graphs[k]):
+                f()
+        step()
         torch.cuda.synchronize()
+    graph = graphs[0]
 
     K = args.steps
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
@@ -259,10 +274,7 @@ def run_ours(args):
         for i in range(K):
             flush.fill_(float(i))  # evict L2 (256 MiB > 126 MB) outside the events
             ev[i][0].record()
-            if graph is not None:
-                graph.replay()
-            else:
-                step()
+            step()
             ev[i][1].record()
         torch.cuda.synchronize()
     launches = launches_per_step * K  # our kernels per step (graph replays launch them all)
@@ -281,7 +293,7 @@ def run_ours(args):
     ops.context.reset_profile()
     for i in range(P):
         flush.fill_(float(i))
-        step()
+        step(eager=True)  # per-kernel-class events are recorded by the eager launches
     prof = ops.context.profile()
     ops.context.set_profiling(False)
     per_launch = {k[:-3]: prof[k] / P * 1e3 for k in prof if k.endswith("_ms")}  # us per step

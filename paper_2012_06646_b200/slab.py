@@ -187,14 +187,21 @@ class SlabDecomposition:
         return self.ghost_sum(self._spread(points, values))
 
     # -------------------------------------------------------- interpolate
-    def halo_fill(self, owned):
+    def halo_fill(self, owned, out=None):
         """Owned planes (nloc x plane) -> local field with halos (local_planes x plane)."""
         import torch
 
         lay, P = self.lay, self.lay.plane
         O = owned.view(lay.nloc, P)
         from_up, from_down = self._exchange(O[0:1], O[lay.nloc - 2:lay.nloc], (1, P), (2, P))
-        L = torch.zeros((lay.local_planes, P), dtype=owned.dtype, device=owned.device)
+        if out is None:
+            L = torch.zeros((lay.local_planes, P), dtype=owned.dtype, device=owned.device)
+        else:
+            L = out.view(lay.local_planes, P)
+            if from_down is None:
+                L[0:2].zero_()
+            if from_up is None:
+                L[lay.nloc + 2].zero_()
         L[2:lay.nloc + 2] = O
         if from_down is not None:  # planes z0-2, z0-1
             L[0:2] = from_down
@@ -215,7 +222,7 @@ class SlabDecomposition:
             self._ops = DeviceOperators(torch.cuda.current_device())
         return self._ops
 
-    def _device_spread(self, points, values):
+    def _device_spread(self, points, values, out=None):
         import torch
 
         from .device import _ptr, _require
@@ -224,7 +231,8 @@ class SlabDecomposition:
         n = points.shape[0]
         _require(points, "points", n * self.grid.dim)
         _require(values, "values", n)
-        out = torch.empty(self.local.point_count(), dtype=torch.float64, device=points.device)
+        if out is None:
+            out = torch.empty(self.local.point_count(), dtype=torch.float64, device=points.device)
         ws = ops.workspace(n, self.local)
         ops._sync_stream()
         slab = c_slab(self.lay)
@@ -233,7 +241,7 @@ class SlabDecomposition:
                                             _ptr(points), _ptr(values), n, ws.handle, _ptr(out)))
         return out
 
-    def _device_interpolate(self, field_local, points):
+    def _device_interpolate(self, field_local, points, out=None):
         import torch
 
         from .device import _ptr, _require
@@ -242,7 +250,8 @@ class SlabDecomposition:
         n = points.shape[0]
         _require(field_local, "field", self.local.point_count())
         _require(points, "points", n * self.grid.dim)
-        out = torch.empty(n, dtype=torch.float64, device=points.device)
+        if out is None:
+            out = torch.empty(n, dtype=torch.float64, device=points.device)
         ops._sync_stream()
         slab = c_slab(self.lay)
         check(load().ibc_interpolate_slab_device(ops.context.handle, C.byref(self.local.c_grid),
