@@ -633,8 +633,23 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
   const int slots = g.dim == 3 ? 4 : 1;
   const size_t per_warp = (size_t)rows_per_warp * slots * rl * sizeof(double);
   if (per_warp > 200 * 1024) return false;
-  int wpc = rows_per_warp == 1 ? 8 : 1;
-  while (wpc > 1 && wpc * per_warp > 200 * 1024) --wpc;
+  // Warps per CTA: bank mode one (its kernel is __launch_bounds__(32)); pull
+  // mode the CTA size (<= 8 warps) that keeps the most warps resident per SM
+  // under the window (shared memory) and register (__launch_bounds__(256, 3):
+  // 24 warps) limits -- long x rows need small CTAs to fill an SM.
+  int wpc = 1;
+  if (rows_per_warp == 1) {
+    long best = 0;
+    for (int w = 8; w >= 1; --w) {
+      if ((size_t)w * per_warp > 200 * 1024) continue;
+      const long ctas = std::min<long>(32, (227L * 1024) / (long)(w * per_warp));
+      const long warps = std::min<long>(24, (long)w * ctas);
+      if (warps > best) {
+        best = warps;
+        wpc = w;
+      }
+    }
+  }
   T.wpc = wpc;
   T.rl = rl;
   T.pull_row = sp::pull_row();
@@ -642,7 +657,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
   const int rows_per_cta = wpc * rows_per_warp;
   T.nyg = (ny + rows_per_cta - 1) / rows_per_cta;
   if (g.dim == 3) {
-    const long max_warps = rows_per_warp == 1 ? 2048 / 32 : 16;  // bank mode: __launch_bounds__(32)
+    const long max_warps = rows_per_warp == 1 ? 24 : 16;  // registers / __launch_bounds__
     const long per_sm = std::max<long>(
         1, std::min<long>(std::min<long>(max_warps / wpc, 32), (227L * 1024) / (long)(wpc * per_warp)));
     const long chunks = std::max<long>(1, (148L * per_sm) / T.nyg);
