@@ -43,17 +43,19 @@ constexpr int kRowsPerWarp = 2;
 constexpr int kBanks = 32 / kRowsPerWarp;
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 
-// Spread batching mode, decided on the device from the densest row (row scan):
-// bank mode (lanes own x banks, ibc_spread.cuh) for sparse rows -- and for
-// rows holding more than two points per cell on average, i.e. clustered
-// points, where the pull mode's same-cell shuffle groups serialise -- pull
-// mode otherwise.  Bank tables hold 16-bit offsets, hence the cap.
+// Spread batching mode, decided on the device from the row scan's statistics
+// stats[0] = densest row, stats[1] = fullest (row, x bank) bucket: bank mode
+// (lanes own x banks, ibc_spread.cuh) for sparse rows, and for clustered
+// points -- a bucket of >= kClusterBucket points, where the pull mode's
+// same-cell shuffle groups serialise (measured: clustered 2.1 ms bank vs
+// 2.7 ms pull, severe 14 ms vs 33 ms; uniform 1 point/cell and RBC surfaces,
+// fullest buckets 17-24, are 4-30% faster in pull mode).
+constexpr uint32_t kClusterBucket = 28;
 // pull_row == kNoBankMode: the bank window does not fit (very long x rows).
 constexpr uint32_t kNoBankMode = 0xffffffffu;
-__host__ __device__ __forceinline__ bool bank_mode(uint32_t maxrow, uint32_t pull_row,
-                                                   uint32_t rowdiv) {
+__host__ __device__ __forceinline__ bool bank_mode(const uint32_t* stats, uint32_t pull_row) {
   if (pull_row == kNoBankMode) return false;
-  return maxrow <= pull_row || (maxrow > 2u * rowdiv && maxrow <= 0xffffu);
+  return stats[0] <= pull_row || stats[1] >= kClusterBucket;
 }
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 
@@ -102,8 +104,8 @@ __device__ __forceinline__ uint32_t ld_flag(const uint32_t* p) {
 // here "rows" are buckets, `group` (1 or kBanks) consecutive buckets per grid
 // row.  status: one zeroed word per chunk; ticket: zeroed
 // counter.  Grid rows longer than kShortRow are appended to long_rows (count
-// in *nlong) when long_rows != null; *maxrow (zeroed, may be null) receives
-// the largest grid-row count.
+// in *nlong) when long_rows != null; maxrow[0] (zeroed, may be null) receives
+// the largest grid-row count, maxrow[1] the largest bucket count.
 template <int ITEMS>  // buckets per thread: kScanItems (group 1) or group (one grid row per thread)
 __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* __restrict__ count,
                                                                 uint32_t* __restrict__ start,
@@ -140,13 +142,20 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
       if (long_rows && v[q] > (uint32_t)kShortRow) long_rows[atomicAdd(nlong, 1u)] = r0 + q;
     }
   }
+  uint32_t bmax = 0;
   if (group > 1) {  // the thread's ITEMS == group buckets are one grid row
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) bmax = max(bmax, v[q]);
     vmax = sum;
     if (long_rows && sum > (uint32_t)kShortRow && r0 < nrows)
       long_rows[atomicAdd(nlong, 1u)] = r0 / (uint32_t)group;
   }
   vmax = __reduce_max_sync(0xffffffffu, vmax);
-  if (maxrow && lane == 0) atomicMax(maxrow, vmax);  // densest row (spread batching mode)
+  bmax = __reduce_max_sync(0xffffffffu, bmax);
+  if (maxrow && lane == 0) {  // densest row, fullest bucket (spread batching mode)
+    atomicMax(maxrow, vmax);
+    if (group > 1) atomicMax(maxrow + 1, bmax);
+  }
   // Block scan of the per-thread sums.
   uint32_t x = sum;
 #pragma unroll
@@ -322,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     int* __restrict__ rcx, const uint32_t* __restrict__ maxrow, uint32_t bank_rows, int mode) {
   const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
   if (o >= n) return;
-  const bool banked = mode == 0 && bank_mode(*maxrow, bank_rows, g.rowdiv);
+  const bool banked = mode == 0 && bank_mode(maxrow, bank_rows);
   const unsigned long long me = __ldg(bpair + o);
   const uint32_t k = (uint32_t)(me >> 32), ix = (uint32_t)me;
   const uint32_t row = k / g.rowdiv;
@@ -368,7 +377,7 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     double* __restrict__ rec, int* __restrict__ rcx, const uint32_t* __restrict__ maxrow,
     uint32_t bank_rows, int mode) {
   extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
-  if (mode == 0 && bank_mode(*maxrow, bank_rows, g.rowdiv)) return;
+  if (mode == 0 && bank_mode(maxrow, bank_rows)) return;
   const uint32_t count = *nlong;
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = long_rows[li];

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  if (maxrow && bucket::bank_mode(*maxrow, T.pull_row, g.rowdiv)) return;  // bank mode
+  if (maxrow && bucket::bank_mode(maxrow, T.pull_row)) return;  // bank mode
   constexpr int kSlots = D == 3 ? 4 : 1;
   const int rl = RL > 0 ? RL : T.rl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -374,7 +374,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
                                                           const int* __restrict__ rcx,
                                                           double* __restrict__ out) {
   extern __shared__ __align__(16) double win[];
-  if (!bucket::bank_mode(*maxrow, T.pull_row, g.rowdiv)) return;  // pull mode
+  if (!bucket::bank_mode(maxrow, T.pull_row)) return;  // pull mode
   constexpr int kSlots = D == 3 ? 4 : 1;
   constexpr int GS = bucket::kBanks, ES = 16 / GS, RPW = bucket::kRowsPerWarp;
   const int rl = RL > 0 ? RL : T.rl;
