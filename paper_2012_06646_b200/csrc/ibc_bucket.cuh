@@ -1,25 +1,27 @@
-// ibc_bucket.cuh -- row bucket sort of the Lagrangian points (sm_100a).
+// ibc_bucket.cuh -- bucket sort of the Lagrangian points (sm_100a).
 //
 // Both operators consume the points grouped by home row (cy, cz) -- the
 // contiguous ranges of the reference's sorted cell keys that share a row
-// (spread.hpp:88-122).  A one-pass counting sort by row does the grouping:
-//   K1 cell key (bit-exact, grid.hpp:121-170) of every point, its row, and
-//      its arrival rank in the row (the row-count atomic's return value);
-//   K2 single-pass scan of the row counts (decoupled look-back over 4096-row
-//      chunks) -> the row start table;
-//   K3 atomic-free scatter to row start + rank (interpolation: the record
-//      {x, y, z, index}; spread: the (key, index) pair).
+// (spread.hpp:88-122).  A one-pass counting sort does the grouping:
+//   K1 cell key (bit-exact, grid.hpp:121-170) of every point, its bucket --
+//      its row (interpolation) or its (row, x cell mod 16) pair (spread; a
+//      row's 16 buckets are contiguous, so rows stay contiguous) -- and its
+//      arrival rank in the bucket (the bucket-count atomic's return value);
+//   K2 single-pass scan of the bucket counts (decoupled look-back) -> the
+//      start table, the long-row list, the densest row and fullest bucket;
+//   K3 atomic-free scatter to bucket start + rank (interpolation: the 64-byte
+//      gather record; spread: the (key << 32 | index) pair).
 // Interpolation results do not depend on the order inside a row (each point
 // is summed alone, into its own slot), so K1-K3 are all it needs.  The spread
-// sums many points into each grid value, and the reference exposes the stable
-// key order (ws.keys / ws.perm, spread.hpp:33-34), so a fourth kernel puts
-// every row into stable (key, index) order -- which makes the result exactly
-// the reference's stable key-value sort -- and writes the weight records the
-// spread sweep streams in that order:
-//   K4 rows of <= 256 points: one thread per point, rank by compares against
-//      its row's pairs; longer rows (listed by K2): one CTA, bitonic sort in
-//      shared memory;
-//      per sorted position: cell + one sin/cos pair per axis -> 64-byte record.
+// sums many points into each grid value, so its summation order must not
+// depend on the atomics' arrival order:
+//   K4 one thread per point ranks its pair by counting over its (row, x bank)
+//      bucket (bank mode) or its row (pull mode, rows <= 256 points; longer
+//      rows: K4b, one CTA, bitonic sort in shared memory) and writes the
+//      64-byte weight record (cell + one sin/cos pair per axis) at start +
+//      rank.  Pull mode also writes the sorted pairs -- the reference's
+//      stable key-value sort, ws.keys / ws.perm (spread.hpp:33-34); in bank
+//      mode they are materialised on request (K4/K4b over the rows, mode 1).
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

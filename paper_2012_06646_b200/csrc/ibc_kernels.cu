@@ -1,8 +1,9 @@
 // ibc_kernels.cu -- pipelines of the spread / interpolate hot path (sm_100a).
 //
 // Per operator call:
-//   spread, 2-D/3-D grids:  row bucket sort + in-row stable sort + weight
-//     records (ibc_bucket.cuh) -> write-once sweep (ibc_spread.cuh)
+//   spread, 2-D/3-D grids:  (row, x bank) bucket sort + in-bucket (bank mode)
+//     or in-row (pull mode) ranking + weight records (ibc_bucket.cuh) ->
+//     write-once sweep (ibc_spread.cuh)
 //   interpolation, 3-D grids with nx % 16 == 0: row bucketing
 //     (ibc_bucket.cuh) -> TMA-fed gather (ibc_sweep.cuh)
 //   general path (1-D grids, rows too long for a shared-memory window, other
