@@ -60,10 +60,7 @@ __host__ __device__ __forceinline__ bool bank_mode(const uint32_t* stats, uint32
   return stats[0] <= pull_row || stats[1] >= kClusterBucket;
 }
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
-
-// Points per thread of the one-pass kernels K1/K3: their loads, atomics and
-// stores are issued for kPer points at once (they are latency-bound chains).
-constexpr int kPer = 1;
+constexpr uint32_t kOutside = 0x80000000u;  // rank flag: home cell outside the grid (K1)
 
 // Cell key of every point (or just its row when full_key == 0), its arrival
 // rank in its bucket, and the per-bucket counts.  Buckets: rows (banks == 1,
@@ -79,18 +76,25 @@ __global__ void __launch_bounds__(kThreads) keys_kernel(DevGrid g, const double*
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   uint64_t k = 0;
+  bool inside = true;  // home cell within the extended range [-1, n] on closed axes
 #pragma unroll
   for (int a = 0; a < D; ++a) {
     if (a == 0 && !full_key) continue;
     double xw;
     int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
     if (g.periodic[a]) c = wrap_cell(c, g.n[a]);
+    else inside = inside && c >= -1 && c <= g.n[a];
     k += (uint64_t)(int64_t)(c + 1) * g.kstride[a];  // cell_key, grid.hpp:158-170
   }
   const uint32_t key = (uint32_t)k, row = key / g.rowdiv;
-  const uint32_t bucket = banks > 1 ? row * (uint32_t)banks + ((key - row * g.rowdiv) & (banks - 1)) : row;
+  // Points homed outside the extended cells of a closed axis (their keys
+  // alias other rows, grid.hpp:158-170) go to an extra last row, flagged in
+  // the rank's top bit; the operators skip them.
+  const uint32_t bucket = !inside ? g.nrows * (uint32_t)banks
+                          : banks > 1 ? row * (uint32_t)banks + ((key - row * g.rowdiv) & (banks - 1))
+                                      : row;
   keys[i] = full_key ? key : row;
-  rank[i] = atomicAdd(count + bucket, 1u);
+  rank[i] = atomicAdd(count + bucket, 1u) | (inside ? 0u : kOutside);
 }
 
 __device__ __forceinline__ void st_flag(uint32_t* p, uint32_t v) {
@@ -238,35 +242,27 @@ template <int D>
 __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
     DevGrid g, const double* __restrict__ X, const uint32_t* __restrict__ rows,
     const uint32_t* __restrict__ rank, uint32_t n, const uint32_t* __restrict__ start,
-    double* __restrict__ rec) {
-  const uint32_t i0 = blockIdx.x * (kThreads * kPer) + threadIdx.x;
-  uint32_t slot[kPer];
-  double x[kPer][D];
-#pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const uint32_t i = i0 + u * kThreads;
-    slot[u] = i < n ? __ldg(start + __ldg(rows + i)) + __ldg(rank + i) : 0u;
-#pragma unroll
-    for (int a = 0; a < D; ++a) x[u][a] = i < n ? __ldg(X + (size_t)i * D + a) : 0.0;
+    double* __restrict__ rec, double* __restrict__ out) {
+  const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t rk = __ldg(rank + i);
+  if (rk & kOutside) {  // homed outside the grid: no gather reaches it
+    out[i] = 0.0;
+    return;
   }
+  const uint32_t slot = __ldg(start + __ldg(rows + i)) + rk;
+  double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};
+  int c[3] = {0, 0, 0};
 #pragma unroll
-  for (int u = 0; u < kPer; ++u) {
-    const uint32_t i = i0 + u * kThreads;
-    double tr[3][2] = {{0.0, 1.0}, {0.0, 1.0}, {0.0, 1.0}};
-    int c[3] = {0, 0, 0};
-#pragma unroll
-    for (int a = 0; a < D; ++a) {
-      double w;
-      c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, x[u][a], &w);
-      sincos_half_pi(w, &tr[a][0], &tr[a][1]);
-    }
-    if (i < n) {
-      double* r = rec + 8 * (size_t)slot[u];
-      st_v4(r, tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
-      st_v4(r + 4, tr[2][0], tr[2][1], __longlong_as_double(((long long)c[0] << 32) | i),
-            __longlong_as_double((long long)(uint32_t)c[1]));
-    }
+  for (int a = 0; a < D; ++a) {
+    double w;
+    c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &w);
+    sincos_half_pi(w, &tr[a][0], &tr[a][1]);
   }
+  double* r = rec + 8 * (size_t)slot;
+  st_v4(r, tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
+  st_v4(r + 4, tr[2][0], tr[2][1], __longlong_as_double(((long long)c[0] << 32) | i),
+        __longlong_as_double((long long)(uint32_t)c[1]));
 }
 
 // The spread's 64-byte weight record of point i at sorted position o:
@@ -307,12 +303,14 @@ __device__ __forceinline__ void write_record(const DevGrid& g, const double* __r
 // bucket slot, start + arrival rank.
 __global__ void __launch_bounds__(kThreads) scatter_spread_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
-    uint32_t rowdiv, const uint32_t* __restrict__ start, unsigned long long* __restrict__ bpair) {
+    uint32_t rowdiv, uint32_t nrows, const uint32_t* __restrict__ start,
+    unsigned long long* __restrict__ bpair) {
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
-  const uint32_t key = __ldg(keys + i), row = key / rowdiv;
-  const uint32_t bucket = row * (uint32_t)kBanks + ((key - row * rowdiv) & (kBanks - 1));
-  bpair[__ldg(start + bucket) + __ldg(rank + i)] = ((unsigned long long)key << 32) | i;
+  const uint32_t key = __ldg(keys + i), row = key / rowdiv, rk = __ldg(rank + i);
+  const uint32_t bucket = (rk & kOutside) ? nrows * (uint32_t)kBanks
+                                          : row * (uint32_t)kBanks + ((key - row * rowdiv) & (kBanks - 1));
+  bpair[__ldg(start + bucket) + (rk & ~kOutside)] = ((unsigned long long)key << 32) | i;
 }
 
 // K4, one thread per bucket slot, ranking its (key, index) pair by counting
@@ -336,9 +334,12 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
   const bool banked = mode == 0 && bank_mode(maxrow, bank_rows);
   const unsigned long long me = __ldg(bpair + o);
   const uint32_t k = (uint32_t)(me >> 32), ix = (uint32_t)me;
-  const uint32_t row = k / g.rowdiv;
-  const uint32_t b0 = banked ? row * (uint32_t)kBanks + ((k - row * g.rowdiv) & (kBanks - 1))
-                             : row * (uint32_t)kBanks;
+  // Slots past the grid rows hold the points homed outside (one bucket).
+  const bool outside = o >= __ldg(start + (size_t)g.nrows * kBanks);
+  const uint32_t row = outside ? g.nrows : k / g.rowdiv;
+  const uint32_t b0 = banked && !outside
+                          ? row * (uint32_t)kBanks + ((k - row * g.rowdiv) & (kBanks - 1))
+                          : row * (uint32_t)kBanks;
   const uint32_t a = __ldg(start + b0);
   const uint32_t len = __ldg(start + b0 + (banked ? 1 : kBanks)) - a;
   if (!banked && len > (uint32_t)kShortRow) return;  // long rows: K4b

@@ -622,7 +622,7 @@ void PointScratch::release_all() {
 
 namespace {
 void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
-                   size_t n, PointScratch& s, bool spread);
+                   size_t n, PointScratch& s, bool spread, double* d_out = nullptr);
 
 // Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
 // rows_per_warp = 1: pull mode (wpc warps per CTA, one target row each);
@@ -858,7 +858,7 @@ namespace {
 // K3 over the spread buckets.
 void launch_scatter_spread(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
   bucket::scatter_spread_kernel<<<grid_for(n, bucket::kThreads), bucket::kThreads, 0, ctx.stream>>>(
-      s.keys[1].p, s.vals[1].p, (uint32_t)n, g.rowdiv, s.rowstart.p, s.bpair.p);
+      s.keys[1].p, s.vals[1].p, (uint32_t)n, g.rowdiv, g.nrows, s.rowstart.p, s.bpair.p);
   ++ctx.launches;
 }
 
@@ -899,9 +899,9 @@ void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
 // rows' key order.  The stable (key, index) order the reference exposes as
 // ws.keys / ws.perm is materialised on request (ensure_observables).
 void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
-                   size_t n, PointScratch& s, bool spread) {
+                   size_t n, PointScratch& s, bool spread, double* d_out) {
   cudaStream_t st = ctx.stream;
-  const uint32_t nrows = g.nrows;
+  const uint32_t nrows = g.nrows + 1;  // + the row of points homed outside (K1)
   const int group = spread ? bucket::kBanks : 1;     // buckets per grid row
   const uint32_t nb = nrows * (uint32_t)group;       // buckets
   const uint32_t chunk = bucket::kScanThreads * (spread ? bucket::kBanks : bucket::kScanItems);
@@ -953,10 +953,10 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   if (!spread) {
     if (g.dim == 3)
       bucket::scatter_interp_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
-          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p, d_out);
     else
       bucket::scatter_interp_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
-          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
+          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p, d_out);
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
@@ -986,7 +986,7 @@ bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, cons
   CUtensorMap map_box;
   if (!tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax)) return false;
   cudaStream_t st = ctx.stream;
-  bucket_points(ctx, g, d_points, nullptr, n, s, false);
+  bucket_points(ctx, g, d_points, nullptr, n, s, false, d_out);
   const size_t smem = interp_tma_smem(T);
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
