@@ -129,8 +129,10 @@ __global__ void __launch_bounds__(kBlock) rowstart_kernel(const uint32_t* __rest
                                                           uint32_t* __restrict__ rowstart) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
-    const uint32_t row = sk[i] / rowdiv;
-    const uint32_t prow = i == 0 ? 0u : sk[i - 1] / rowdiv;
+    // (min: keys of points homed outside a closed axis can alias past the
+    // last row -- keep the writes inside the table.)
+    const uint32_t row = min(sk[i] / rowdiv, nrows);
+    const uint32_t prow = i == 0 ? 0u : min(sk[i - 1] / rowdiv, nrows);
     for (uint32_t r = i == 0 ? 0u : prow + 1; r <= row; ++r) rowstart[r] = i;
     if (i == n - 1)
       for (uint32_t r = row + 1; r <= nrows; ++r) rowstart[r] = n;
