@@ -160,11 +160,11 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
                                               uint32_t e1, uint32_t e2, uint32_t total,
                                               uint32_t rstart,
                                               const double* __restrict__ rec,
-                                              const int* __restrict__ rcx, double q) {
+                                              const int* __restrict__ rcx, double q, int nx) {
   const int lane = threadIdx.x & 31;
   for (uint32_t base = 0; base < total; base += 32) {
     const uint32_t p = base + (uint32_t)lane;
-    const bool valid = p < total;
+    bool valid = p < total;
     const int j = (p >= e0) + (p >= e1) + (p >= e2);
     const uint32_t rs = __shfl_sync(0xffffffffu, rstart, j & 3) + p;
     int cx = -0x40000000 - lane;  // distinct per idle lane: never matched
@@ -177,6 +177,10 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
       tr = make_double2(gb.x, gb.y);
       tz2 = make_double2(gb.z, gb.w);
       cx = __ldg(rcx + r);
+      if (cx < -1 || cx > nx) {  // homed outside a closed x axis (radix path): no target
+        valid = false;
+        cx = -0x40000000 - lane;
+      }
     }
     // phi(sigma_y - t_y)/h: j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h.
     const double vy = (j & 1) ? tr.x : tr.y;
@@ -322,13 +326,13 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
         // path: slot offsets are immediates, no per-add range checks.
         if (RL > 0 && interior) {
           switch (s & 3) {
-            case 0: plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
-            case 1: plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
-            case 2: plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
-            default: plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, rec, rcx, q); break;
+            case 0: plane_batches_pull<D, RL, 0>(W, so, e0, e1, e2, total, rstart, rec, rcx, q, nx); break;
+            case 1: plane_batches_pull<D, RL, 1>(W, so, e0, e1, e2, total, rstart, rec, rcx, q, nx); break;
+            case 2: plane_batches_pull<D, RL, 2>(W, so, e0, e1, e2, total, rstart, rec, rcx, q, nx); break;
+            default: plane_batches_pull<D, RL, 3>(W, so, e0, e1, e2, total, rstart, rec, rcx, q, nx); break;
           }
         } else {
-          plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, rec, rcx, q);
+          plane_batches_pull<D, RL, -1>(W, so, e0, e1, e2, total, rstart, rec, rcx, q, nx);
         }
       }
     }
