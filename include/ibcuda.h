@@ -113,7 +113,10 @@ ibc_status ibc_workspace_destroy(ibc_workspace* ws);
 ibc_status ibc_workspace_info(const ibc_workspace* ws, size_t* point_count,
                               size_t* grid_points, int* sweep_width);
 /* Observable results of the most recent spread through `ws` (synchronize):
- * ws.run_count, ws.keys (sorted), ws.perm, ws.run_keys[0..q) (spread.hpp:33-41). */
+ * ws.run_count, ws.keys (sorted), ws.perm, ws.run_keys[0..q) (spread.hpp:33-41).
+ * The spread itself only buckets the points; the stable (key, index) order
+ * is computed on the first of these calls after it (bit-exact with the
+ * reference's key_value_sort, sort.hpp:17-71). */
 ibc_status ibc_workspace_run_count(ibc_workspace* ws, size_t* q);
 ibc_status ibc_workspace_get_keys(ibc_workspace* ws, uint32_t* host_keys, size_t n);
 ibc_status ibc_workspace_get_perm(ibc_workspace* ws, uint32_t* host_perm, size_t n);
