@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
     ap.add_argument("--mac-steps", type=int, default=5, help="MAC vector step timing (0: skip)")
+    ap.add_argument("--no-serial", action="store_true", help="reference arm: skip the spread_serial timing")
     return ap.parse_args()
 
 
@@ -169,6 +170,16 @@ def run_reference(args):
     t = cpu_reference_steps(data, steps, warm, threads)
     per = float(statistics.median(t))
     value = data["n"] / per
+    # also ib::spread_serial (Alg. 2) at one worker, one call.
+    serial_ms = None
+    if not args.no_serial:
+        import oracle as O
+
+        N = data["N"]
+        g = O.make_grid([N] * 3, data["h"], [0.5, 0.5, 0.0], [1, 1, 1])
+        t0 = time.perf_counter()
+        O.ref_spread(g, data["x_star"], data["values"], algo="serial", workers=1)
+        serial_ms = (time.perf_counter() - t0) * 1e3
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(t), "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
@@ -178,6 +189,7 @@ def run_reference(args):
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{len(t)} full config-2 steps (2^20 points, 256^3), median"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "spread_serial_1_thread_ms": serial_ms,
     }
     print(json.dumps(line))
 
