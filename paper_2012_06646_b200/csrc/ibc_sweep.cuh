@@ -123,16 +123,19 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
       if (g.periodic[2]) t = wrap_cell(t, nz);
       const uint32_t bar = full0 + 8u * slot;
       const int jr = i - 3;  // step whose records ride with this plane
-      uint32_t nrec = 0, ra = 0;
+      uint32_t nrec = 0, ra = 0, over = 0;
       if (jr >= 0 && jr < H) {
         ra = rs[jr];
-        nrec = min(rs[T.hmax + jr] - ra, (uint32_t)T.rec_cap);
+        const uint32_t all = rs[T.hmax + jr] - ra;
+        nrec = min(all, (uint32_t)T.rec_cap);
+        over = all - nrec;  // read from global by the consumers: pull them into L2 now
       }
       const uint32_t dst = base + (uint32_t)slot * T.slot_stride;
       tma::fence_proxy_async();
       if (lane == 0) {
         tma::mbar_expect_tx(bar, plane_bytes + nrec * 64u);
         if (nrec) tma::bulk_g2s(dst + T.slot_bytes, rec + 8 * (size_t)ra, nrec * 64u, bar);
+        if (over) tma::prefetch_bytes(rec + 8 * (size_t)(ra + nrec), over * 64u);
         if (box) tma::load_4d(dst, &tmap_box, 0, 0, hy0 - 2, t, bar);
       }
       __syncwarp();
