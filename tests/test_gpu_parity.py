@@ -442,3 +442,36 @@ def test_dense_one_point_per_cell():
     assert O.max_rel_deviation(got.values, want) <= TOL
     e = rng.uniform(-1, 1, g.point_count())
     assert O.max_rel_deviation(ib.interpolate(ib.GridField(g, e), pts, K), O.interpolate(og(g), e, pts)) <= TOL
+
+
+def _full_size_parity(N, pts, seed):
+    edge = 16e-4
+    g = ib.StaggeredGrid([N] * 3, edge / N, [0.5, 0.5, 0.0], [True] * 3)
+    rng = np.random.default_rng(seed)
+    vals = rng.uniform(-1, 1, len(pts))
+    ws = ib.SpreadWorkspace(len(pts), g)
+    got = ib.spread_fused(pts, vals, g, K, ws, 8)
+    keys, perm, run_keys = O.prepare_keys(og(g), pts)
+    assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm)
+    assert ws.run_count == run_keys.size
+    assert O.max_rel_deviation(got.values, O.spread_serial(og(g), pts, vals)) <= TOL
+    e = rng.uniform(-1, 1, g.point_count())
+    E = ib.interpolate(ib.GridField(g, e), pts, K, 8)
+    assert O.max_rel_deviation(E, O.interpolate(og(g), e, pts)) <= TOL
+
+
+@pytest.mark.slow
+def test_config_rbc_full_array_parity():
+    # ~0.9 M points on RBC surfaces, 256^3 (pull mode)
+    from paper_2012_06646_b200 import synth
+
+    _full_size_parity(256, synth.rbc_points(16e-4, 16e-4 / 256, 7), 31)
+
+
+@pytest.mark.slow
+def test_config_clustered_full_array_parity():
+    # 2^22 points in 64 Gaussian clusters, 512^3 (bank
+    # mode, clustered rows, CTA-sorted long rows)
+    from paper_2012_06646_b200 import synth
+
+    _full_size_parity(512, synth.clustered_points(1 << 22, 16e-4, 64, 8 * 16e-4 / 512, 5), 32)
