@@ -68,3 +68,31 @@ def test_mac_step_loop_matches_reference_step():
             assert not np.any(got)
         else:
             assert O.max_rel_deviation(got, ell_ref[a]) <= TOL
+
+
+@pytest.mark.gpu
+def test_mac_step_loop_graph_replay_matches_eager():
+    """bench.py times the MAC step replayed from a CUDA graph: same state as
+    the eager loop, bit for bit."""
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    cfg = S.StepConfig(refinement=16, point_count=2000, dt_us=100.0)
+    eager = S.MacStepLoop(cfg)
+    for _ in range(3):
+        eager.step()
+    torch.cuda.synchronize()
+    loop = S.MacStepLoop(cfg)
+    loop.step()  # warm-up (allocations, kernel attributes) ...
+    torch.cuda.synchronize()
+    loop.X.copy_(loop.anchors)  # ... then back to the initial state
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        loop.step()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(loop.X, eager.X)
+    for a in range(3):
+        assert torch.equal(loop.spread_result[a], eager.spread_result[a])
