@@ -13,9 +13,11 @@ data resident in HBM: per step
 on the MAC component grids of `mac_grids` (`setup.hpp:16-23`, staggering 0
 along the component's own axis, 1/2 along the others) with the fixed shear
 field of `shear_field` (`setup.hpp:27-40`).  The six interpolations and three
-spreads run through libibcuda's device operators; the per-point updates (b),
-(c), (f) are a few elementwise torch ops on (n, 3) tensors (plumbing around
-the operators, as the reference's loops are around its calls).
+spreads run through libibcuda's device operators -- the three components of
+a vector operation concurrently, each on its own stream and context -- and
+the per-point updates (b), (c), (f) are a few elementwise torch ops on (n, 3)
+tensors (plumbing around the operators, as the reference's loops are around
+its calls).
 
 This is SURVEY.md 8(f) item 2 and the "MAC vector step" secondary figure of
 8(d); the headline metric stays the scalar spread + interpolation pair.
@@ -88,7 +90,8 @@ def hookean_force(predicted, anchors, k: float, edge_cm: float, out=None):
 class MacStepLoop:
     """The reference bench step with every array on one GPU."""
 
-    def __init__(self, cfg: StepConfig, device: int = 0, ops=None, points=None):
+    def __init__(self, cfg: StepConfig, device: int = 0, ops=None, points=None,
+                 concurrent: bool = True):
         import numpy as np
         import torch
 
@@ -98,6 +101,16 @@ class MacStepLoop:
         self.cfg = cfg
         self.dev = torch.device("cuda", device)
         self.ops = ops or DeviceOperators(device)
+        # The three components are independent: with `concurrent`, each runs
+        # on its own stream and context (its own scratch), forked from and
+        # joined back to the caller's stream -- graph-capturable.
+        self.concurrent = concurrent
+        if concurrent:
+            self.comp_ops = [self.ops] + [DeviceOperators(device) for _ in range(2)]
+            self.streams = [torch.cuda.Stream(self.dev) for _ in range(3)]
+        else:
+            self.comp_ops = [self.ops] * 3
+            self.streams = None
         L = cfg.edge_cm
         self.grids = mac_grids(cfg.refinement, L)
         self.velocity = shear_field(self.grids, cfg.shear_rate, L, self.dev)
@@ -111,9 +124,25 @@ class MacStepLoop:
         self.F = torch.empty((3, n), **f64)          # tether forces
         self.ell = [torch.empty(g.point_count(), **f64) for g in self.grids]
 
+    def _components(self, fn):
+        """fn(a) for the three components, concurrently when configured."""
+        import torch
+
+        if not self.concurrent:
+            for a in range(3):
+                fn(a)
+            return
+        main = torch.cuda.current_stream(self.dev)
+        for a in range(3):
+            self.streams[a].wait_stream(main)
+            with torch.cuda.stream(self.streams[a]):
+                fn(a)
+        for a in range(3):
+            main.wait_stream(self.streams[a])
+
     def _interpolate_vector(self):
-        for a, g in enumerate(self.grids):
-            self.ops.interpolate(self.velocity[a], self.X, g, out=self.U[a])
+        self._components(lambda a: self.comp_ops[a].interpolate(
+            self.velocity[a], self.X, self.grids[a], out=self.U[a]))
 
     def step(self):
         c = self.cfg
@@ -121,8 +150,8 @@ class MacStepLoop:
         torch = __import__("torch")
         torch.add(self.X, self.U.t(), alpha=c.dt_s, out=self.Xs)          # (b)
         hookean_force(self.Xs, self.anchors, c.spring_constant, c.edge_cm, out=self.F)  # (c)
-        for a, g in enumerate(self.grids):                                # (d)
-            self.ops.spread(self.Xs, self.F[a], g, out=self.ell[a])
+        self._components(lambda a: self.comp_ops[a].spread(               # (d)
+            self.Xs, self.F[a], self.grids[a], out=self.ell[a]))
         self._interpolate_vector()                                        # (e)
         self.X.add_(self.U.t(), alpha=c.dt_s)                             # (f)
 
