@@ -211,19 +211,18 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
       uint32_t rest = lead ? peers & (peers - 1u) : 0u;  // members after the leader
       for (int it = 1; it < gmax; ++it) {
         const int src = rest ? __ffs(rest) - 1 : lane;
-        double mg[4], ma[4];
+        double ma[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          mg[k] = __shfl_sync(0xffffffffu, gk[k], src);
-          ma[k] = __shfl_sync(0xffffffffu, a[k], src);
+        for (int k = 0; k < 4; ++k) ma[k] = __shfl_sync(0xffffffffu, a[k], src);
+#pragma unroll
+        for (int kx = 0; kx < 4; ++kx) {  // one member weight at a time (register pressure)
+          const double mg = __shfl_sync(0xffffffffu, gk[kx], src);
+          if (rest) {
+#pragma unroll
+            for (int kz = 0; kz < 4; ++kz) v[kx][kz] = fma(mg, ma[kz], v[kx][kz]);
+          }
         }
-        if (rest) {
-#pragma unroll
-          for (int kx = 0; kx < 4; ++kx)
-#pragma unroll
-            for (int kz = 0; kz < 4; ++kz) v[kx][kz] = fma(mg[kx], ma[kz], v[kx][kz]);
-          rest &= rest - 1u;
-        }
+        if (rest) rest &= rest - 1u;
       }
     }
     const int xb = cx + (kPadL - 2);
