@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
       if (ok) {
         rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
         rb = __ldg(rowstart + (size_t)rid * T.group);  // row = T.group buckets
-        len = __ldg(rowstart + (size_t)rid * T.group + T.group) - rb;
+        len = __ldg(rowstart + (size_t)rid * T.group + T.group);  // the end: len = end - rb at use
       }
     }
   };
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
   ranges(s_lo, rb_n, len_n, rid_n);
 
   for (int s = s_lo; s <= s_hi; ++s) {
-    const uint32_t rb = rb_n, len = len_n;
+    const uint32_t rb = rb_n, len = len_n - rb_n;  // (loaded during the previous plane)
     ranges(s + 1, rb_n, len_n, rid_n);
     {
       // Window slot offset of target plane s + kz - 2 (-1: outside [z0, z1)).
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
       if (ok) {
         rid = (uint32_t)(cy + 1) + (D == 3 ? (uint32_t)(szw + 1) * (uint32_t)(ny + 2) : 0u);
         rb = __ldg(bstart + (size_t)rid * GS);  // a row's kBanks buckets
-        len = __ldg(bstart + (size_t)rid * GS + GS) - rb;
+        len = __ldg(bstart + (size_t)rid * GS + GS);  // the end: len = end - rb at use
       }
     }
   };
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
   ranges(s_lo, rb_n, len_n, rid_n);
 
   for (int s = s_lo; s <= s_hi; ++s) {
-    const uint32_t len = len_n, rid = rid_n;  // (rb_n: unused, the buckets give the slots)
+    const uint32_t len = len_n - rb_n, rid = rid_n;  // (loaded during the previous plane)
     ranges(s + 1, rb_n, len_n, rid_n);
     int so[4];
 #pragma unroll
