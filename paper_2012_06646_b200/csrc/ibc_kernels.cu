@@ -647,7 +647,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
       if ((size_t)w * per_warp > 200 * 1024) continue;
       const long ctas = std::min<long>(32, (227L * 1024) / (long)(w * per_warp));
       const long warps = std::min<long>(24, (long)w * ctas);
-      if (warps > best) {
+      if (warps >= best) {  // ties: smaller CTAs (finer load balance across SMs)
         best = warps;
         wpc = w;
       }
