@@ -47,12 +47,13 @@ constexpr int kShortRow = 256;      // rows up to this length are sorted by one 
 
 // Spread batching mode, decided on the device from the row scan's statistics
 // stats[0] = densest row, stats[1] = fullest (row, x bank) bucket: bank mode
-// (lanes own x banks, ibc_spread.cuh) for sparse rows, and for clustered
-// points -- a bucket of >= kClusterBucket points, where the pull mode's
-// same-cell shuffle groups serialise (measured: clustered 2.1 ms bank vs
-// 2.7 ms pull, severe 14 ms vs 33 ms; uniform 1 point/cell and RBC surfaces,
-// fullest buckets 17-24, are 4-30% faster in pull mode).
-constexpr uint32_t kClusterBucket = 28;
+// (lanes own x banks, ibc_spread.cuh) for sparse rows, and for crowded
+// buckets (>= kClusterBucket points), where the pull mode's same-cell shuffle
+// groups serialise.  Measured spreads, bank vs pull: W 256^3 (fullest bucket
+// 40) 3.75 vs 5.49 ms, severe clustering (293) 13.8 vs 33 ms; clustered
+// (32) 2.08 vs 2.04 ms, W 128^3 (24) 0.52 vs 0.49 ms, RBC (17) 0.45 vs
+// 0.29 ms.
+constexpr uint32_t kClusterBucket = 36;
 // pull_row == kNoBankMode: the bank window does not fit (very long x rows).
 constexpr uint32_t kNoBankMode = 0xffffffffu;
 __host__ __device__ __forceinline__ bool bank_mode(const uint32_t* stats, uint32_t pull_row) {
