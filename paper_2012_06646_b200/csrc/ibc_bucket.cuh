@@ -50,7 +50,7 @@ constexpr int kShortRow = 256;      // rows up to this length are sorted by one 
 // (lanes own x banks, ibc_spread.cuh) for sparse rows, and for crowded
 // buckets (>= kClusterBucket points), where the pull mode's same-cell shuffle
 // groups serialise.  Measured spreads, bank vs pull: W 256^3 (fullest bucket
-// 40) 3.75 vs 5.49 ms, severe clustering (293) 13.8 vs 33 ms; clustered
+// 40) 3.75 vs 5.49 ms, severe clustering (293) 13.9 vs 26.9 ms; clustered
 // (32) 2.08 vs 2.04 ms, W 128^3 (24) 0.52 vs 0.49 ms, RBC (17) 0.45 vs
 // 0.29 ms.
 constexpr uint32_t kClusterBucket = 36;
