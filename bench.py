@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
     ap.add_argument("--mac-steps", type=int, default=5, help="MAC vector step timing (0: skip)")
     ap.add_argument("--no-serial", action="store_true", help="reference arm: skip the spread_serial timing")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c1", "w128", "w256", "rbc", "clustered"],
+                    help="one-GPU workload (default: BASELINE config 2, the headline)")
     return ap.parse_args()
 
 
@@ -161,7 +163,7 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libibref.so not built (reference headers absent at build)"}))
         return
-    data = synth.config2()
+    data = synth.survey_config(args.workload)
     threads = host_threads()
     # One step of the full workload takes ~1-2 s on 8 cores: bound the run to a
     # few minutes by capping the number of measured steps.
@@ -184,10 +186,14 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(t), "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_points": data["n"], "grid": [data["N"]] * 3,
+        "config": {"workload": WORKLOAD if args.workload == "c2" else
+                   f"SURVEY 8(d) workload {args.workload}: {data['n']} points on a {data['N']}^3 "
+                   "periodic grid, one scalar spread + one scalar interpolation per step, FP64",
+                   "n_points": data["n"], "grid": [data["N"]] * 3,
                    "parallelism": f"OpenMP {threads} threads (rank 0 only)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                         "sample": f"{len(t)} full config-2 steps (2^20 points, 256^3), median"},
+                         "sample": f"{len(t)} full {args.workload} steps ({data['n']} points, "
+                                   f"{data['N']}^3), median"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "spread_serial_1_thread_ms": serial_ms,
     }
@@ -216,7 +222,7 @@ def run_ours(args):
     # z-slabs of a 256 x 256 x 256N periodic grid (weak scaling), with the
     # ghost-plane sum and halo fill over NCCL between ring neighbours.
     if world == 1:
-        data = synth.config2(seed_offset=0)
+        data = synth.survey_config(args.workload)
         n, N, h = data["n"], data["N"], data["h"]
         grid = ib.StaggeredGrid([N] * 3, h, [0.5, 0.5, 0.0], [True] * 3)
         ops = DeviceOperators(local)
@@ -431,14 +437,17 @@ def run_ours(args):
                 t = cpu_reference_steps(data, 2, 1, threads)
                 cpu = {"value": n / float(statistics.median(t)), "unit": UNIT, "cores": threads,
                        "kind": "reference",
-                       "sample": "2 full config-2 steps (ib::spread_fused + ib::interpolate, "
+                       "sample": f"2 full {args.workload} steps (ib::spread_fused + ib::interpolate, "
                                  "oracle/_ref, OpenMP) after 1 warm-up, median"}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                    "sample": f"failed: {exc}"}
 
     if rank == 0:
-        workload = WORKLOAD if world == 1 else (
+        workload = (WORKLOAD if args.workload == "c2" else
+                    f"SURVEY 8(d) workload {args.workload}: {n} points on a {N}^3 periodic grid, "
+                    f"one scalar spread (at X*) + one scalar interpolation (at X^n) per step, FP64") \
+            if world == 1 else (
             f"config 2 per GPU, weak scaling: {world} z-slabs of a 256 x 256 x {256 * world} "
             f"periodic grid, 2^20 points homed in each slab; per step one scalar spread (local + "
             f"NCCL ghost-plane sum) and one scalar interpolation (NCCL halo fill + local gather), FP64")

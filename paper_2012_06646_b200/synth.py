@@ -140,6 +140,32 @@ def config2(seed_offset: int = 0):
     return dict(n=n, N=N, edge=edge, h=h, x_n=xn, x_star=xs, values=g, field=e)
 
 
+def survey_config(name: str, seed_offset: int = 0):
+    """The other SURVEY 8(d) workloads in config2()'s format: c1 (2^16 points,
+    64^3), w128 / w256 (one point per cell), rbc (RBC surfaces, 256^3),
+    clustered (2^22 points in 64 Gaussian clusters, 512^3)."""
+    edge = 16e-4
+    if name == "c2":
+        return config2(seed_offset)
+    if name == "c1":
+        N, xn = 64, scatter_points(1 << 16, edge, 1 + seed_offset)
+    elif name in ("w128", "w256"):
+        N = int(name[1:])
+        xn = scatter_points(N ** 3, edge, 1 + seed_offset)
+    elif name == "rbc":
+        N = 256
+        xn = rbc_points(edge, edge / N, 7 + seed_offset)
+    elif name == "clustered":
+        N = 512
+        xn = clustered_points(1 << 22, edge, 64, 8 * edge / N, 5 + seed_offset)
+    else:
+        raise ValueError(f"unknown workload {name!r}")
+    n, h = len(xn), edge / N
+    xs = perturb(xn, 0.1 * h, 3 + seed_offset)
+    return dict(n=n, N=N, edge=edge, h=h, x_n=xn, x_star=xs, values=uniform_pm1(n, 2 + seed_offset),
+                field=uniform_pm1(N ** 3, 4 + seed_offset))
+
+
 def slab_config(rank: int, world: int):
     """Weak-scaling multi-GPU workload (BASELINE config 2 per GPU): a global
     256 x 256 x 256*world periodic grid split in z-slabs of 256 planes; rank r
