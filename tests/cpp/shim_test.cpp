@@ -85,6 +85,52 @@ static void coupling_case(std::mt19937_64& rng, std::array<int, D> ext, std::arr
   EXPECT(max_rel_dev(e, ew) <= 1e-12);
 }
 
+// run.hpp's MAC vector calls: spread_vector under every algorithm switch
+// and interpolate_vector on the three component grids (setup.hpp:16-23).
+static void mac_vector_case(std::mt19937_64& rng) {
+  std::uniform_real_distribution<double> u(0.0, 1.0);
+  const std::array<int, 3> ext = {16, 12, 10};
+  const std::array<bool, 3> per = {true, true, true};
+  std::array<ib::StaggeredGrid<3>, 3> grids = {
+      ib::StaggeredGrid<3>(ext, 0.5, {0.0, 0.5, 0.5}, per),
+      ib::StaggeredGrid<3>(ext, 0.5, {0.5, 0.0, 0.5}, per),
+      ib::StaggeredGrid<3>(ext, 0.5, {0.5, 0.5, 0.0}, per)};
+  const std::size_t n = 900;
+  ib::PointSet<3> pts(n);
+  std::array<ib::LagrangianValues, 3> force;
+  for (auto& f : force) f.resize(n);
+  for (std::size_t i = 0; i < n; ++i)
+    for (std::size_t a = 0; a < 3; ++a) {
+      pts[i][a] = u(rng) * grids[0].axis_length(a);
+      force[a][i] = 2 * u(rng) - 1;
+    }
+  ib::CosineKernel kern;
+  ib::SpreadWorkspace<3> ws(n, grids[0], 2);
+  std::array<std::vector<double>, 3> want;
+  for (int c = 0; c < 3; ++c) {
+    const or_grid og = to_or(grids[c]);
+    want[c].resize(grids[c].point_count());
+    or_spread_serial(&og, pts.front().data(), force[c].data(), n, want[c].data());
+  }
+  for (auto algo : {ib::SpreadAlgorithm::serial, ib::SpreadAlgorithm::fused,
+                    ib::SpreadAlgorithm::buffered, ib::SpreadAlgorithm::otf}) {
+    auto got = ib::spread_vector<3>(pts, force, std::span<const ib::StaggeredGrid<3>>(grids), kern,
+                                    algo, 2, &ws, 8);
+    for (int c = 0; c < 3; ++c) EXPECT(max_rel_dev(got[c].values, want[c]) <= 1e-12);
+  }
+  std::array<ib::GridField<3>, 3> u3 = {ib::GridField<3>(grids[0]), ib::GridField<3>(grids[1]),
+                                        ib::GridField<3>(grids[2])};
+  for (auto& f : u3)
+    for (auto& v : f.values) v = 2 * u(rng) - 1;
+  auto e = ib::interpolate_vector<3>(std::span<const ib::GridField<3>>(u3), pts, kern, 8);
+  for (int c = 0; c < 3; ++c) {
+    const or_grid og = to_or(grids[c]);
+    std::vector<double> ew(n);
+    or_interpolate(&og, u3[c].values.data(), pts.front().data(), n, ew.data());
+    EXPECT(max_rel_dev(e[c], ew) <= 1e-12);
+  }
+}
+
 int main() {
   try {
     (void)ib::b200::context();
@@ -98,6 +144,7 @@ int main() {
   coupling_case<2>(rng, {13, 7}, {true, false}, 300);
   coupling_case<1>(rng, {17}, {true}, 100);
   coupling_case<3>(rng, {32, 32, 32}, {true, true, true}, 20000);
+  mac_vector_case(rng);
 
   // Reference exceptions (spread.hpp:60-77, grid.hpp:37-60).
   ib::StaggeredGrid<2> g({4, 4}, 1.0, {0.0, 0.0}, {false, false});
