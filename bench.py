@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
     ap.add_argument("--mac-steps", type=int, default=5, help="MAC vector step timing (0: skip)")
     ap.add_argument("--no-serial", action="store_true", help="reference arm: skip the spread_serial timing")
+    ap.add_argument("--strong", action="store_true",
+                    help="N > 1: strong scaling -- config 2 (2^20 points, one 256^3 grid) split into N z-slabs")
     ap.add_argument("--workload", default="c2", choices=["c2", "c1", "w128", "w256", "rbc", "clustered"],
                     help="one-GPU workload (default: BASELINE config 2, the headline)")
     return ap.parse_args()
@@ -227,12 +229,38 @@ def run_ours(args):
         grid = ib.StaggeredGrid([N] * 3, h, [0.5, 0.5, 0.0], [True] * 3)
         ops = DeviceOperators(local)
         dec = None
+    elif args.strong:
+        # the one config-2 workload, each rank taking
+        # the spread points (X*) and interpolation points (X^n) homed in its
+        # z-slab of the 256^3 grid and its owned planes of the field.
+        from paper_2012_06646_b200.slab import home_planes, owner_of_planes, slab_bounds
+
+        data = dict(synth.survey_config("c2"))
+        n_total, N, h = data["n"], data["N"], data["h"]
+        grid = ib.StaggeredGrid([N] * 3, h, [0.5, 0.5, 0.0], [True] * 3)
+        ops = DeviceOperators(local)
+        dec = SlabDecomposition(grid, rank, world, ops=ops)
+
+        def mine(a):
+            t = torch.tensor(np.ascontiguousarray(a), device=dev)
+            return (owner_of_planes(home_planes(grid, t, ops), N, world) == rank).cpu().numpy()
+
+        ms, mn = mine(data["x_star"]), mine(data["x_n"])
+        zb = slab_bounds(N, world)
+        data.update(x_star=np.ascontiguousarray(data["x_star"][ms]),
+                    values=np.ascontiguousarray(data["values"][ms]),
+                    x_n=np.ascontiguousarray(data["x_n"][mn]),
+                    field=np.ascontiguousarray(
+                        np.asarray(data["field"]).reshape(N, N * N)[zb[rank]:zb[rank + 1]].reshape(-1)))
+        n = len(data["x_n"])
     else:
         data = synth.slab_config(rank, world)
         n, N, h = data["n"], data["N"], data["h"]
         grid = ib.StaggeredGrid([N, N, data["nz_global"]], h, [0.5, 0.5, 0.0], [True] * 3)
         ops = DeviceOperators(local)
         dec = SlabDecomposition(grid, rank, world, ops=ops)
+    strong = world > 1 and args.strong
+    total_points = n_total if strong else world * n
     xs = torch.tensor(data["x_star"], device=dev)
     xn = torch.tensor(data["x_n"], device=dev)
     gv = torch.tensor(data["values"], device=dev)
@@ -303,7 +331,7 @@ def run_ours(args):
         total_ms = float(t.item())
         dist.barrier()
     ms_per_step = total_ms / K
-    value = world * n * K / (total_ms * 1e-3)
+    value = total_points * K / (total_ms * 1e-3)
 
     # Per-kernel-class device times (CUDA events on the operators' stream), separate pass.
     P = max(3, min(K, 10))
@@ -315,7 +343,7 @@ def run_ours(args):
     prof = ops.context.profile()
     ops.context.set_profiling(False)
     per_launch = {k[:-3]: prof[k] / P * 1e3 for k in prof if k.endswith("_ms")}  # us per step
-    n_omega = N ** 3  # grid points each rank owns
+    n_omega = dec.lay.nloc * N * N if dec is not None else N ** 3  # grid points this rank owns
     alg = {"spread": 32 * n + 8 * n_omega, "interp": 32 * n + 8 * n_omega}
     dom = max(("spread", "interp"), key=lambda k: per_launch.get(k, 0.0))
     peak, peak_src = peaks()
@@ -383,7 +411,7 @@ def run_ours(args):
             t = torch.tensor([e2e_s], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        e2e = {"value": world * n / e2e_s, "unit": UNIT,
+        e2e = {"value": total_points / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(hx_s.nbytes + hg.nbytes + hx_n.nbytes + hf.nbytes),
                "d2h_bytes_per_step": int(n_omega * 8 + n * 8), "note": note}
 
@@ -448,15 +476,20 @@ def run_ours(args):
                     f"SURVEY 8(d) workload {args.workload}: {n} points on a {N}^3 periodic grid, "
                     f"one scalar spread (at X*) + one scalar interpolation (at X^n) per step, FP64") \
             if world == 1 else (
+            f"config 2, strong scaling: 2^20 points on one 256^3 periodic grid split into {world} "
+            f"z-slabs, each rank the points homed in its slab; per step one scalar spread (local + "
+            f"NCCL ghost-plane sum) and one scalar interpolation (NCCL halo fill + local gather), FP64"
+            ) if strong else (
             f"config 2 per GPU, weak scaling: {world} z-slabs of a 256 x 256 x {256 * world} "
             f"periodic grid, 2^20 points homed in each slab; per step one scalar spread (local + "
             f"NCCL ghost-plane sum) and one scalar interpolation (NCCL halo fill + local gather), FP64")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": workload, "n_points_per_gpu": n,
-                       "grid": [N, N, N * world],
+                       "grid": [N, N, N if strong else N * world],
                        "parallelism": f"z-slab x{world} (NCCL ghost/halo exchange)" if world > 1
                        else "single GPU",
                        "l2": "flushed between steps (256 MiB write outside the events)",
