@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kThreads) keys_kernel(DevGrid g, const double*
                                                         uint32_t* __restrict__ keys,
                                                         uint32_t* __restrict__ rank,
                                                         uint32_t* __restrict__ count) {
+  pdl_wait();
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   uint64_t k = 0;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
                                                                 uint32_t* status, uint32_t* ticket,
                                                                 uint32_t* __restrict__ long_rows,
                                                                 uint32_t* nlong, uint32_t* maxrow) {
+  pdl_wait();
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_chunk, s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
     DevGrid g, const double* __restrict__ X, const uint32_t* __restrict__ rows,
     const uint32_t* __restrict__ rank, uint32_t n, const uint32_t* __restrict__ start,
     double* __restrict__ rec, double* __restrict__ out) {
+  pdl_wait();
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const uint32_t rk = __ldg(rank + i);
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(kThreads) scatter_spread_kernel(
     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ rank, uint32_t n,
     uint32_t rowdiv, uint32_t nrows, const uint32_t* __restrict__ start,
     unsigned long long* __restrict__ bpair) {
+  pdl_wait();
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const uint32_t key = __ldg(keys + i), row = key / rowdiv, rk = __ldg(rank + i);
@@ -330,6 +334,7 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
     uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx, DevGrid g,
     const double* __restrict__ X, const double* __restrict__ G, double* __restrict__ rec,
     int* __restrict__ rcx, const uint32_t* __restrict__ maxrow, uint32_t bank_rows, int mode) {
+  pdl_wait();
   const uint32_t o = blockIdx.x * kThreads + threadIdx.x;
   if (o >= n) return;
   const bool banked = mode == 0 && bank_mode(maxrow, bank_rows);
@@ -380,6 +385,7 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
     double* __restrict__ rec, int* __restrict__ rcx, const uint32_t* __restrict__ maxrow,
     uint32_t bank_rows, int mode) {
+  pdl_wait();
   extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
   if (mode == 0 && bank_mode(maxrow, bank_rows)) return;
   const uint32_t count = *nlong;

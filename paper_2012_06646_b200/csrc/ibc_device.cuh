@@ -222,6 +222,13 @@ __device__ __forceinline__ void unit_weights(double w[4]) {
   w[0] = 0.0; w[1] = 0.0; w[2] = 1.0; w[3] = 0.0;
 }
 
+// Programmatic dependent launch: the pipeline's kernels are launched with
+// programmatic stream serialization (their launch and block scheduling
+// overlap the predecessor's tail) and wait here, before touching memory,
+// until the predecessor grid has completed and flushed.  A no-op for a
+// normal launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): one 32-byte sector
 // per instruction instead of two half-sector 128-bit ones.
 __device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {

@@ -24,6 +24,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "ibc_internal.h"
 #include "ibc_sort.cuh"
@@ -33,6 +34,25 @@
 #include "ibc_tma.cuh"
 
 namespace ibc {
+
+// Launch with programmatic stream serialization (PDL): the kernel's launch
+// overlaps its predecessor's tail; it waits in pdl_wait() (ibc_device.cuh)
+// before touching memory.  Works inside CUDA graph capture.
+template <typename... KArgs, typename... Args>
+static void pdl_launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  IBC_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 namespace {
 
@@ -730,11 +750,11 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     const uint32_t* maxrow = (!radix) ? s.maxrow : nullptr;
     auto launch = [&](auto bank_k, auto pull_k) {
       if (maxrow && WB.pull_row != bucket::kNoBankMode) {
-        bank_k<<<blocks_b, 32 * WB.wpc, smem_b, st>>>(g, WB, maxrow, s.rowstart.p, s.rec.p,
+        pdl_launch(bank_k, blocks_b, 32 * WB.wpc, smem_b, st, g, WB, maxrow, s.rowstart.p, s.rec.p,
                                                       s.rec_cx.p, d_out);
         ++ctx.launches;
       }
-      pull_k<<<blocks, 32 * W.wpc, smem, st>>>(g, W, maxrow, s.rowstart.p, s.rec.p,
+      pdl_launch(pull_k, blocks, 32 * W.wpc, smem, st, g, W, maxrow, s.rowstart.p, s.rec.p,
                                                s.rec_cx.p, d_out);
     };
     const int nx = g.n[0];
@@ -859,7 +879,7 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
 namespace {
 // K3 over the spread buckets.
 void launch_scatter_spread(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
-  bucket::scatter_spread_kernel<<<grid_for(n, bucket::kThreads), bucket::kThreads, 0, ctx.stream>>>(
+  pdl_launch(bucket::scatter_spread_kernel, grid_for(n, bucket::kThreads), bucket::kThreads, 0, ctx.stream, 
       s.keys[1].p, s.vals[1].p, (uint32_t)n, g.rowdiv, g.nrows, s.rowstart.p, s.bpair.p);
   ++ctx.launches;
 }
@@ -882,10 +902,10 @@ void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
     attr_set[ctx.device & 63] = true;
   }
   auto sorts = [&](auto short_k, auto long_k) {
-    short_k<<<grid_for(n, bucket::kThreads), bucket::kThreads, 0, st>>>(
+    pdl_launch(short_k, grid_for(n, bucket::kThreads), bucket::kThreads, 0, st, 
         s.rowstart.p, (uint32_t)n, s.bpair.p, s.keys[0].p, s.vals[0].p, g, d_points, d_values,
         s.rec.p, s.rec_cx.p, maxrow, s.bank_rows, mode);
-    long_k<<<148, bucket::kLongThreads, lsm, st>>>(s.rowstart.p, long_rows, nlong, s.bpair.p,
+    pdl_launch(long_k, 148, bucket::kLongThreads, lsm, st, s.rowstart.p, long_rows, nlong, s.bpair.p,
                                                    s.keys[0].p, s.vals[0].p, g, d_points,
                                                    d_values, s.rec.p, s.rec_cx.p, maxrow,
                                                    s.bank_rows, mode);
@@ -935,29 +955,29 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   uint32_t* ikeys = s.keys[spread ? 1 : 0].p;
   uint32_t* irank = s.vals[spread ? 1 : 0].p;
   if (g.dim == 3)
-    bucket::keys_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full, group,
+    pdl_launch(bucket::keys_kernel<3>, blocks, bucket::kThreads, 0, st, g, d_points, (uint32_t)n, full, group,
                                                                ikeys, irank, count);
   else if (g.dim == 2)
-    bucket::keys_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full, group,
+    pdl_launch(bucket::keys_kernel<2>, blocks, bucket::kThreads, 0, st, g, d_points, (uint32_t)n, full, group,
                                                                ikeys, irank, count);
   else
-    bucket::keys_kernel<1><<<blocks, bucket::kThreads, 0, st>>>(g, d_points, (uint32_t)n, full, group,
+    pdl_launch(bucket::keys_kernel<1>, blocks, bucket::kThreads, 0, st, g, d_points, (uint32_t)n, full, group,
                                                                ikeys, irank, count);
   ctx.prof_end(kProfKeys, ev);
   ctx.prof_begin(kProfSort, &ev);
   if (spread)
-    bucket::row_scan_kernel<bucket::kBanks><<<nchunks, bucket::kScanThreads, 0, st>>>(
+    pdl_launch(bucket::row_scan_kernel<bucket::kBanks>, nchunks, bucket::kScanThreads, 0, st, 
         count, s.rowstart.p, nb, group, status, ticket, long_rows, nlong, maxrow);
   else
-    bucket::row_scan_kernel<bucket::kScanItems><<<nchunks, bucket::kScanThreads, 0, st>>>(
+    pdl_launch(bucket::row_scan_kernel<bucket::kScanItems>, nchunks, bucket::kScanThreads, 0, st, 
         count, s.rowstart.p, nb, group, status, ticket, nullptr, nlong, maxrow);
   ctx.launches += 2;
   if (!spread) {
     if (g.dim == 3)
-      bucket::scatter_interp_kernel<3><<<blocks, bucket::kThreads, 0, st>>>(
+      pdl_launch(bucket::scatter_interp_kernel<3>, blocks, bucket::kThreads, 0, st, 
           g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p, d_out);
     else
-      bucket::scatter_interp_kernel<2><<<blocks, bucket::kThreads, 0, st>>>(
+      pdl_launch(bucket::scatter_interp_kernel<2>, blocks, bucket::kThreads, 0, st, 
           g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p, d_out);
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
@@ -998,7 +1018,7 @@ bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, cons
   }
   cudaEvent_t ev = nullptr;
   ctx.prof_begin(kProfInterp, &ev);
-  sw::interp_tma_kernel<<<(unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st>>>(
+  pdl_launch(sw::interp_tma_kernel, (unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st, 
       g, T, map, map_box, s.rowstart.p, s.rec.p, d_out);
   ++ctx.launches;
   ctx.prof_end(kProfInterp, ev);

@@ -256,6 +256,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
                                                            double* __restrict__ out) {
+  pdl_wait();
   extern __shared__ __align__(16) double win[];
   if (maxrow && bucket::bank_mode(maxrow, T.pull_row)) return;  // bank mode
   constexpr int kSlots = D == 3 ? 4 : 1;
@@ -376,6 +377,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
                                                           const double* __restrict__ rec,
                                                           const int* __restrict__ rcx,
                                                           double* __restrict__ out) {
+  pdl_wait();
   extern __shared__ __align__(16) double win[];
   if (!bucket::bank_mode(maxrow, T.pull_row)) return;  // pull mode
   constexpr int kSlots = D == 3 ? 4 : 1;

@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
     DevGrid g, InterpTiling T, const __grid_constant__ CUtensorMap tmap_row,
     const __grid_constant__ CUtensorMap tmap_box, const uint32_t* __restrict__ rowstart,
     const double* __restrict__ rec, double* __restrict__ out) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // Layout: full[kMaxSlots] | empty[kMaxSlots] | step table [3][hmax] |
   // ring of 1024-aligned slots (field rows of one plane + records of one step).
