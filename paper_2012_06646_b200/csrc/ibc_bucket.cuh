@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
                                                                 uint32_t* __restrict__ long_rows,
                                                                 uint32_t* nlong, uint32_t* maxrow) {
   pdl_wait();
-  __shared__ uint32_t s_warp[kScanThreads / 32];
+  __shared__ uint32_t s_warp[kScanThreads / 32], s_vmax[kScanThreads / 32], s_bmax[kScanThreads / 32];
   __shared__ uint32_t s_chunk, s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_chunk = atomicAdd(ticket, 1u);  // chunks start in ticket order
@@ -161,9 +161,9 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
   }
   vmax = __reduce_max_sync(0xffffffffu, vmax);
   bmax = __reduce_max_sync(0xffffffffu, bmax);
-  if (maxrow && lane == 0) {  // densest row, fullest bucket (spread batching mode)
-    atomicMax(maxrow, vmax);
-    if (group > 1) atomicMax(maxrow + 1, bmax);
+  if (lane == 0) {  // per-CTA maxima: one atomic per CTA, not per warp
+    s_vmax[warp] = vmax;
+    s_bmax[warp] = bmax;
   }
   // Block scan of the per-thread sums.
   uint32_t x = sum;
@@ -183,6 +183,14 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
     }
     s_warp[lane] = wi - w;  // exclusive warp offsets
     const uint32_t total = __shfl_sync(0xffffffffu, wi, 31);
+    if (maxrow) {  // densest row, fullest bucket (spread batching mode)
+      const uint32_t cm = __reduce_max_sync(0xffffffffu, s_vmax[lane]);
+      const uint32_t cb = __reduce_max_sync(0xffffffffu, s_bmax[lane]);
+      if (lane == 0) {
+        atomicMax(maxrow, cm);
+        if (group > 1) atomicMax(maxrow + 1, cb);
+      }
+    }
     // Publish the aggregate, then look back 32 chunks per round trip.
     if (lane == 0) st_flag(status + chunk, (chunk == 0 ? kFlagPrefix : kFlagAggregate) | total);
     uint32_t excl = 0;
