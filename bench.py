@@ -108,17 +108,25 @@ class ClockSampler:
         self._stop = threading.Event()
         self._t = None
 
-    def _run(self):
+    def sample_now(self):
+        """One sample from the calling thread (the timed loop calls this
+        between steps -- host side only, outside every event pair -- so the
+        region has samples even when the launch loop starves the thread)."""
+        if not self.ok:
+            return
         nv = self.nv
+        try:
+            self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+            mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for bit, name in self.REASONS.items():
+                if mask & bit and name != "gpu_idle":
+                    self.reasons.add(name)
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop.is_set():
-            try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for bit, name in self.REASONS.items():
-                    if mask & bit and name != "gpu_idle":
-                        self.reasons.add(name)
-            except Exception:
-                pass
+            self.sample_now()
             time.sleep(self.period)
 
     def __enter__(self):
@@ -322,6 +330,7 @@ def run_ours(args):
             ev[i][0].record()
             step()
             ev[i][1].record()
+            clk.sample_now()
         torch.cuda.synchronize()
     launches = launches_per_step * K  # our kernels per step (graph replays launch them all)
     total_ms = sum(a.elapsed_time(b) for a, b in ev)
