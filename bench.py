@@ -69,10 +69,41 @@ def dist_env():
 
 
 def host_threads() -> int:
+    """Physical cores available to this process (the reference's OpenMP team:
+    one thread per core, OMP_PLACES=cores, OMP_PROC_BIND=close)."""
     try:
-        return len(os.sched_getaffinity(0))
+        logical = len(os.sched_getaffinity(0))
     except Exception:
-        return os.cpu_count() or 1
+        logical = os.cpu_count() or 1
+    try:
+        import psutil
+
+        phys = psutil.cpu_count(logical=False) or logical
+        per_core = max(1, (psutil.cpu_count(logical=True) or logical) // phys)
+        return max(1, logical // per_core)
+    except Exception:
+        return logical
+
+
+def omp_env() -> None:
+    """Pin the reference's OpenMP team before libgomp initialises."""
+    os.environ["OMP_PLACES"] = "cores"
+    os.environ["OMP_PROC_BIND"] = "close"
+    os.environ["OMP_NUM_THREADS"] = str(host_threads())
+
+
+def bench_config(workload: str, n: int, grid) -> dict:
+    """The config dict both arms print (the driver compares them)."""
+    return {"workload": workload, "n_points": int(n), "grid": [int(v) for v in grid]}
+
+
+def lib_build_id() -> str:
+    """sha256 (16 hex) of the loaded libibcuda.so: stamps measured ncu traffic."""
+    import hashlib
+
+    from paper_2012_06646_b200 import _capi
+
+    return hashlib.sha256(_capi.LIB_PATH.read_bytes()).hexdigest()[:16]
 
 
 def peaks():
@@ -156,10 +187,33 @@ def cpu_reference_steps(data, steps, warmup, threads):
 
     N = data["N"]
     g = O.make_grid([N] * 3, data["h"], [0.5, 0.5, 0.0], [1, 1, 1])
-    os.environ.setdefault("OMP_PROC_BIND", "close")
+    omp_env()
     ts, ti = O.ref_time_step(g, data["x_star"], data["values"], data["x_n"], data["field"],
                              threads, warmup + steps)
     return (np.asarray(ts) + np.asarray(ti))[warmup:]
+
+
+def workload_name(w: str, n: int, N: int) -> str:
+    return WORKLOAD if w == "c2" else (
+        f"SURVEY 8(d) workload {w}: {n} points on a {N}^3 periodic grid, one scalar spread "
+        "(at X*) + one scalar interpolation (at X^n) per step, FP64")
+
+
+def run_config(args, world: int, n1: int, N: int) -> dict:
+    """The workload a run of `world` ranks measures (both arms print it)."""
+    if world == 1:
+        return bench_config(workload_name(args.workload, n1, N), n1, [N] * 3)
+    if args.strong:
+        return bench_config(
+            f"config 2, strong scaling: 2^20 points on one 256^3 periodic grid split into {world} "
+            "z-slabs, each rank the points homed in its slab; per step one scalar spread (local + "
+            "ghost-plane sum) and one scalar interpolation (halo fill + local gather), FP64",
+            1 << 20, [256, 256, 256])
+    return bench_config(
+        f"config 2 per GPU, weak scaling: {world} z-slabs of a 256 x 256 x {256 * world} periodic "
+        "grid, 2^20 points homed in each slab; per step one scalar spread (local + ghost-plane "
+        "sum) and one scalar interpolation (halo fill + local gather), FP64",
+        world << 20, [256, 256, 256 * world])
 
 
 def run_reference(args):
@@ -196,14 +250,12 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(t), "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.workload == "c2" else
-                   f"SURVEY 8(d) workload {args.workload}: {data['n']} points on a {data['N']}^3 "
-                   "periodic grid, one scalar spread + one scalar interpolation per step, FP64",
-                   "n_points": data["n"], "grid": [data["N"]] * 3,
-                   "parallelism": f"OpenMP {threads} threads (rank 0 only)"},
+        "config": run_config(args, world, data["n"], data["N"]),
+        "parallelism": f"OpenMP, {threads} threads = physical cores, OMP_PLACES=cores (rank 0 only)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": f"{len(t)} full {args.workload} steps ({data['n']} points, "
-                                   f"{data['N']}^3), median"},
+                                   f"{data['N']}^3{', one slab of the run' if world > 1 else ''}), "
+                                   "median"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "spread_serial_1_thread_ms": serial_ms,
     }
@@ -357,11 +409,16 @@ def run_ours(args):
     dom = max(("spread", "interp"), key=lambda k: per_launch.get(k, 0.0))
     peak, peak_src = peaks()
     achieved = alg[dom] / (per_launch[dom] * 1e-6) / 1e9
-    traffic = None
+    # dram bytes per launch from `ncu --set full` of this very build (profiles/
+    # traffic.json, written by tools/traffic.py); null when the build differs.
+    traffic, traffic_src = None, "no ncu capture of this build"
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(dom)
+            tj = json.loads(tf.read_text())
+            if tj.get("build") == lib_build_id() and tj.get("workload") == args.workload:
+                traffic = tj.get(dom)
+                traffic_src = f"ncu --set full, profiles/traffic.json (build {tj['build']})"
         except Exception:
             traffic = None
     step_bytes = 64 * n + 16 * n_omega
@@ -481,30 +538,19 @@ def run_ours(args):
                    "sample": f"failed: {exc}"}
 
     if rank == 0:
-        workload = (WORKLOAD if args.workload == "c2" else
-                    f"SURVEY 8(d) workload {args.workload}: {n} points on a {N}^3 periodic grid, "
-                    f"one scalar spread (at X*) + one scalar interpolation (at X^n) per step, FP64") \
-            if world == 1 else (
-            f"config 2, strong scaling: 2^20 points on one 256^3 periodic grid split into {world} "
-            f"z-slabs, each rank the points homed in its slab; per step one scalar spread (local + "
-            f"NCCL ghost-plane sum) and one scalar interpolation (NCCL halo fill + local gather), FP64"
-            ) if strong else (
-            f"config 2 per GPU, weak scaling: {world} z-slabs of a 256 x 256 x {256 * world} "
-            f"periodic grid, 2^20 points homed in each slab; per step one scalar spread (local + "
-            f"NCCL ghost-plane sum) and one scalar interpolation (NCCL halo fill + local gather), FP64")
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": workload, "n_points_per_gpu": n,
-                       "grid": [N, N, N if strong else N * world],
-                       "parallelism": f"z-slab x{world} (NCCL ghost/halo exchange)" if world > 1
-                       else "single GPU",
-                       "l2": "flushed between steps (256 MiB write outside the events)",
-                       "cuda_graph": graph is not None},
+            "config": run_config(args, world, n if world == 1 else total_points, N),
+            "parallelism": f"z-slab x{world} (ghost/halo exchange)" if world > 1 else "single GPU",
+            "n_points_per_gpu": n,
+            "l2": "flushed between steps (256 MiB write outside the events)",
+            "cuda_graph": graph is not None,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "traffic_source": traffic_src,
                          "peak_source": peak_src,
                          "alg_bytes_per_launch": alg[dom], "launch_us": per_launch[dom]},
             "step_roofline": {"alg_bytes": step_bytes,
@@ -522,6 +568,7 @@ def run_ours(args):
 
 
 def main():
+    omp_env()  # before libgomp / torch initialise their thread pools
     args = parse()
     if args.impl == "reference":
         run_reference(args)

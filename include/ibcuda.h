@@ -102,6 +102,20 @@ ibc_status ibc_context_reset_profile(ibc_context* ctx);
 /* Number of device kernels this context has launched so far. */
 uint64_t ibc_context_launches(const ibc_context* ctx);
 
+/* Spread path selection.  AUTO (the default) picks per call on the device
+ * from the densest row / fullest bucket of the bucket sort; the others force
+ * one path (all compute the same operator; tests run each against the
+ * oracle): BANK -- bucket sort + bank-mode sweep, PULL -- bucket sort + row
+ * ranking + pull-mode sweep, RADIX -- stable onesweep radix sort + pull-mode
+ * sweep. */
+typedef enum {
+  IBC_SPREAD_PATH_AUTO = 0,
+  IBC_SPREAD_PATH_BANK = 1,
+  IBC_SPREAD_PATH_PULL = 2,
+  IBC_SPREAD_PATH_RADIX = 3
+} ibc_spread_path;
+ibc_status ibc_context_set_spread_path(ibc_context* ctx, ibc_spread_path path);
+
 /* StaggeredGrid<D> constructor validation (grid.hpp:37-60). */
 ibc_status ibc_grid_check(const ibc_grid* grid);
 

@@ -25,6 +25,11 @@ IBC_SPREAD_FUSED = 1
 IBC_SPREAD_BUFFERED = 2
 IBC_SPREAD_OTF = 3
 
+IBC_SPREAD_PATH_AUTO = 0
+IBC_SPREAD_PATH_BANK = 1
+IBC_SPREAD_PATH_PULL = 2
+IBC_SPREAD_PATH_RADIX = 3
+
 
 class IbcGrid(C.Structure):
     _fields_ = [
@@ -75,6 +80,7 @@ SIGNATURES = {
     "ibc_context_get_profile": (_st, [_vp, C.POINTER(IbcProfile)]),
     "ibc_context_reset_profile": (_st, [_vp]),
     "ibc_context_launches": (C.c_uint64, [_vp]),
+    "ibc_context_set_spread_path": (_st, [_vp, C.c_int]),
     "ibc_grid_check": (_st, [_G]),
     "ibc_workspace_create": (_st, [_vp, _sz, _G, C.c_int, C.POINTER(_vp)]),
     "ibc_workspace_destroy": (_st, [_vp]),

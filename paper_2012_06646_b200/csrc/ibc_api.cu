@@ -147,6 +147,8 @@ ibc_status ibc_context_create(int device, ibc_context** out) {
     IBC_CUDA(cudaSetDevice(device));
     auto* ctx = new ibc_context();
     ctx->c.device = device;
+    IBC_CUDA(cudaDeviceGetAttribute(&ctx->c.sms, cudaDevAttrMultiProcessorCount, device));
+    if (ctx->c.sms < 1) ctx->c.sms = 1;
     *out = ctx;
   });
 }
@@ -172,6 +174,14 @@ ibc_status ibc_context_set_stream(ibc_context* ctx, void* stream) {
   return guarded([&] {
     if (!ctx) invalid("context is null");
     ctx->c.stream = static_cast<cudaStream_t>(stream);
+  });
+}
+
+ibc_status ibc_context_set_spread_path(ibc_context* ctx, ibc_spread_path path) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    if (path < IBC_SPREAD_PATH_AUTO || path > IBC_SPREAD_PATH_RADIX) invalid("unknown spread path");
+    ctx->c.spread_path = path;
   });
 }
 

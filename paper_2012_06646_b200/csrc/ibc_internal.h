@@ -72,6 +72,8 @@ struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool profiling = false;
+  int spread_path = IBC_SPREAD_PATH_AUTO;  // ibc_context_set_spread_path
+  int sms = 0;                             // multiprocessors of `device` (queried at creation)
   uint64_t launches = 0;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::vector<cudaEvent_t> event_pool;

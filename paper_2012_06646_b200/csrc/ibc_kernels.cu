@@ -505,6 +505,7 @@ void sort_points(Context& ctx, const DevGrid& g, const double* d_points, size_t 
   s.last_n = n;
   s.run_keys_valid = false;
   s.keys_are_rows = row_only;
+  s.obs_pending = false;  // the sorted keys / perm are current
 }
 
 void row_table(Context& ctx, const DevGrid& g, size_t n, PointScratch& s) {
@@ -649,7 +650,8 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
 // Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
 // rows_per_warp = 1: pull mode (wpc warps per CTA, one target row each);
 // > 1: bank mode (one warp per CTA, bucket::kRowsPerWarp target rows).
-bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
+bool sweep_tiling(const DevGrid& g, int sms, uint32_t pull_row, sp::SweepTiling& T,
+                  int rows_per_warp) {
   if (g.dim < 2) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   const int rl = sp::row_len(nx);
@@ -675,7 +677,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
   }
   T.wpc = wpc;
   T.rl = rl;
-  T.pull_row = sp::pull_row();
+  T.pull_row = pull_row;
   T.group = bucket::kBanks;
   const int rows_per_cta = wpc * rows_per_warp;
   T.nyg = (ny + rows_per_cta - 1) / rows_per_cta;
@@ -683,7 +685,7 @@ bool sweep_tiling(const DevGrid& g, sp::SweepTiling& T, int rows_per_warp) {
     const long max_warps = rows_per_warp == 1 ? 24 : 16;  // registers / __launch_bounds__
     const long per_sm = std::max<long>(
         1, std::min<long>(std::min<long>(max_warps / wpc, 32), (227L * 1024) / (long)(wpc * per_warp)));
-    const long chunks = std::max<long>(1, (148L * per_sm) / T.nyg);
+    const long chunks = std::max<long>(1, ((long)sms * per_sm) / T.nyg);
     T.zc = (int)std::max<long>(1, (nz + chunks - 1) / chunks);
     T.nzc = (nz + T.zc - 1) / T.zc;
   } else {
@@ -697,13 +699,20 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                      size_t n, PointScratch& s, double* d_out) {
   cudaStream_t st = ctx.stream;
   sp::SweepTiling W, WB;  // pull mode, bank mode
-  const bool sweep = sweep_tiling(g, W, 1);
-  if (!sweep_tiling(g, WB, bucket::kRowsPerWarp)) {  // bank window too large: pull mode only
+  // Bank-mode row threshold: AUTO -- rows up to kPullRow (and crowded
+  // buckets); BANK -- every row; PULL / RADIX -- none.
+  const int path = ctx.spread_path;
+  const uint32_t pull_row = path == IBC_SPREAD_PATH_BANK ? 0xfffffffeu
+                            : (path == IBC_SPREAD_PATH_PULL || path == IBC_SPREAD_PATH_RADIX)
+                                ? bucket::kNoBankMode
+                                : sp::kPullRow;
+  const bool sweep = sweep_tiling(g, ctx.sms, pull_row, W, 1);
+  if (!sweep_tiling(g, ctx.sms, pull_row, WB, bucket::kRowsPerWarp)) {  // bank window too large
     WB = W;
     W.pull_row = WB.pull_row = bucket::kNoBankMode;
   }
   s.bank_rows = W.pull_row;
-  const bool radix = getenv("IBC_SORT") && std::string(getenv("IBC_SORT")) == "radix";
+  const bool radix = path == IBC_SPREAD_PATH_RADIX;
   if (sweep && !radix) {
     bucket_points(ctx, g, d_points, d_values, n, s, true);
   } else {
@@ -795,12 +804,11 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
 namespace {
 
 // Tiling of the TMA interpolation sweep (3-D, nx % 16 == 0, nx <= 4096).
-bool interp_tma_tiling(const DevGrid& g, size_t n, sw::InterpTiling& T) {
+bool interp_tma_tiling(const DevGrid& g, size_t n, int sms, sw::InterpTiling& T) {
   if (g.dim != 3) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   if (nx % 16 != 0 || nx > 4096) return false;
   const uint32_t pitch = (uint32_t)((nx * 8 + 1023) & ~1023);
-  const int sms = 148;
   // Pick TY (home rows per CTA) minimising the bytes one SM streams, with at
   // least 3 planes in flight (slots >= 7) when possible and one CTA per SM.
   double best = 1e300;
@@ -905,7 +913,7 @@ void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
     pdl_launch(short_k, grid_for(n, bucket::kThreads), bucket::kThreads, 0, st, 
         s.rowstart.p, (uint32_t)n, s.bpair.p, s.keys[0].p, s.vals[0].p, g, d_points, d_values,
         s.rec.p, s.rec_cx.p, maxrow, s.bank_rows, mode);
-    pdl_launch(long_k, 148, bucket::kLongThreads, lsm, st, s.rowstart.p, long_rows, nlong, s.bpair.p,
+    pdl_launch(long_k, (unsigned)ctx.sms, bucket::kLongThreads, lsm, st, s.rowstart.p, long_rows, nlong, s.bpair.p,
                                                    s.keys[0].p, s.vals[0].p, g, d_points,
                                                    d_values, s.rec.p, s.rec_cx.p, maxrow,
                                                    s.bank_rows, mode);
@@ -1002,7 +1010,7 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
 bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
                      size_t n, PointScratch& s, double* d_out) {
   sw::InterpTiling T;
-  if (!interp_tma_tiling(g, n, T)) return false;
+  if (!interp_tma_tiling(g, n, ctx.sms, T)) return false;
   CUtensorMap map;
   if (!tma::encode_rows_map(&map, d_field, g.n[0], g.n[1], g.n[2])) return false;
   CUtensorMap map_box;

@@ -31,7 +31,6 @@
 // Either way the summation order is fixed by the data: bitwise reproducible.
 #pragma once
 #include <cstdint>
-#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include "ibc_device.cuh"
@@ -42,10 +41,6 @@ namespace sp {
 
 constexpr int kPadL = 4;  // padded x index xi = x + kPadL
 constexpr uint32_t kPullRow = 64;  // densest row above which batches pull instead of bank mode
-inline uint32_t pull_row() {  // IBC_PULL_ROW overrides (experiments)
-  static const uint32_t v = getenv("IBC_PULL_ROW") ? (uint32_t)atoi(getenv("IBC_PULL_ROW")) : kPullRow;
-  return v;
-}
 constexpr int kPadR = 2;
 
 struct SweepTiling {

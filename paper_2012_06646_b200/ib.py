@@ -59,6 +59,14 @@ class Context:
     def synchronize(self) -> None:
         check(self._lib.ibc_context_synchronize(self.handle))
 
+    def set_spread_path(self, path: str) -> None:
+        """'auto' (default), or force 'bank' / 'pull' / 'radix' (ibc_context_set_spread_path)."""
+        code = {"auto": _capi.IBC_SPREAD_PATH_AUTO, "bank": _capi.IBC_SPREAD_PATH_BANK,
+                "pull": _capi.IBC_SPREAD_PATH_PULL, "radix": _capi.IBC_SPREAD_PATH_RADIX}
+        if path not in code:
+            raise InvalidArgument(f"unknown spread path {path!r}")
+        check(self._lib.ibc_context_set_spread_path(self.handle, code[path]))
+
     def set_profiling(self, on: bool) -> None:
         check(self._lib.ibc_context_set_profiling(self.handle, int(bool(on))))
 

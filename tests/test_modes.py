@@ -1,56 +1,59 @@
 """Every spread path against the oracle: bank mode, pull mode and the radix
-sort path, forced through the environment overrides (read once per process,
-hence subprocesses)."""
+sort path, forced per context (ibc_context_set_spread_path)."""
 import os
 import subprocess
 import sys
 from pathlib import Path
 
+import numpy as np
 import pytest
+
+import oracle as O
+from paper_2012_06646_b200 import ib
 
 pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
-
-CHILD = r'''
-import numpy as np, torch
-import oracle as O
-from paper_2012_06646_b200 import ib
-rng = np.random.default_rng(21)
 K = ib.CosineKernel()
-cases = [([40, 36, 24], [True] * 3, 6000), ([33, 20, 18], [False, True, False], 4000),
-         ([24, 16], [True, False], 3000)]
-for ext, per, n in cases:
-    g = ib.StaggeredGrid(ext, 0.5, [0.5] * len(ext), per)
-    L = np.array(ext) * 0.5
-    lo = np.where(per, -0.2 * L, 0.0)   # closed axes: inside the domain (the
-    hi = np.where(per, 1.2 * L, L)      # reference's tests' contract)
-    pts = rng.uniform(lo, hi, (n, len(ext)))
-    pts[: n // 3] = np.clip(pts[0] + rng.normal(0, 0.3, (n // 3, len(ext))), lo, hi - 1e-9)
-    vals = rng.uniform(-1, 1, n)
-    ws = ib.SpreadWorkspace(n, g)
-    got = ib.spread_fused(pts, vals, g, K, ws, 8)
-    og = O.make_grid(g.extents, g.spacing(), g.staggerings, g.periodic, g.origin)
-    want, keys, perm, runs = O.spread_fused(og, pts, vals)
-    assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm), ext
-    assert ws.run_count == len(runs)
-    assert O.max_rel_deviation(got.values, want) <= 1e-12, ext
-    again = ib.spread_fused(pts, vals, g, K, ws, 8)
-    assert np.array_equal(again.values, got.values)  # deterministic
-print("ok")
-'''
 
 
-@pytest.mark.parametrize("env", [{"IBC_PULL_ROW": "0"}, {"IBC_PULL_ROW": "100000"},
-                                 {"IBC_SORT": "radix"}], ids=["pull", "bank", "radix"])
-def test_spread_paths_match_oracle(env):
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
     import torch
 
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
-    e = dict(os.environ, PYTHONPATH=str(ROOT), **env)
-    out = subprocess.run([sys.executable, "-c", CHILD], cwd=ROOT, env=e, capture_output=True,
-                         text=True, timeout=300)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("path", ["pull", "bank", "radix", "auto"])
+def test_spread_paths_match_oracle(path):
+    rng = np.random.default_rng(21)
+    ctx = ib.Context(0)
+    ctx.set_spread_path(path)
+    cases = [([40, 36, 24], [True] * 3, 6000), ([33, 20, 18], [False, True, False], 4000),
+             ([24, 16], [True, False], 3000), ([64, 48, 40], [True] * 3, 20000)]
+    for ext, per, n in cases:
+        g = ib.StaggeredGrid(ext, 0.5, [0.5] * len(ext), per)
+        L = np.array(ext) * 0.5
+        lo = np.where(per, -0.2 * L, 0.0)   # closed axes: inside the domain (the
+        hi = np.where(per, 1.2 * L, L)      # reference's tests' contract)
+        pts = rng.uniform(lo, hi, (n, len(ext)))
+        pts[: n // 3] = np.clip(pts[0] + rng.normal(0, 0.3, (n // 3, len(ext))), lo, hi - 1e-9)
+        vals = rng.uniform(-1, 1, n)
+        ws = ib.SpreadWorkspace(n, g, context=ctx)
+        got = ib.spread_fused(pts, vals, g, K, ws, 8)
+        og = O.make_grid(g.extents, g.spacing(), g.staggerings, g.periodic, g.origin)
+        want, keys, perm, runs = O.spread_fused(og, pts, vals)
+        assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm), ext
+        assert ws.run_count == len(runs)
+        assert O.max_rel_deviation(got.values, want) <= 1e-12, ext
+        again = ib.spread_fused(pts, vals, g, K, ws, 8)
+        assert np.array_equal(again.values, got.values)  # deterministic
+    ctx.close()
+
+
+def test_spread_path_rejects_unknown():
+    with pytest.raises(ib.InvalidArgument):
+        ib.default_context().set_spread_path("fastest")
 
 
 FAR = r'''
