@@ -69,20 +69,31 @@ def dist_env():
 
 
 def host_threads() -> int:
-    """Physical cores available to this process (the reference's OpenMP team:
-    one thread per core, OMP_PLACES=cores, OMP_PROC_BIND=close)."""
+    """Host threads available to this process: the reference's OpenMP team
+    (workers = nproc), one thread per logical CPU of the
+    affinity mask."""
     try:
-        logical = len(os.sched_getaffinity(0))
+        return max(1, len(os.sched_getaffinity(0)))
     except Exception:
-        logical = os.cpu_count() or 1
-    try:
-        import psutil
+        return os.cpu_count() or 1
 
-        phys = psutil.cpu_count(logical=False) or logical
-        per_core = max(1, (psutil.cpu_count(logical=True) or logical) // phys)
-        return max(1, logical // per_core)
+
+def physical_cores() -> int | None:
+    """Distinct physical cores behind the affinity mask (sysfs topology), or
+    None when the topology is not readable."""
+    try:
+        cpus = os.sched_getaffinity(0)
+        cores = set()
+        for c in cpus:
+            base = f"/sys/devices/system/cpu/cpu{c}/topology/"
+            with open(base + "physical_package_id") as f:
+                pkg = f.read().strip()
+            with open(base + "core_id") as f:
+                core = f.read().strip()
+            cores.add((pkg, core))
+        return len(cores) or None
     except Exception:
-        return logical
+        return None
 
 
 def omp_env() -> None:
@@ -251,8 +262,10 @@ def run_reference(args):
         "steps": len(t), "warmup": warm, "ms_per_step": per * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": run_config(args, world, data["n"], data["N"]),
-        "parallelism": f"OpenMP, {threads} threads = physical cores, OMP_PLACES=cores (rank 0 only)",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+        "parallelism": f"OpenMP, {threads} threads (all logical CPUs of the affinity mask; "
+                       f"{physical_cores()} physical cores), OMP_PLACES=cores, OMP_PROC_BIND=close "
+                       "(rank 0 only)",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "physical_cores": physical_cores(), "kind": "reference",
                          "sample": f"{len(t)} full {args.workload} steps ({data['n']} points, "
                                    f"{data['N']}^3{', one slab of the run' if world > 1 else ''}), "
                                    "median"},
@@ -530,7 +543,7 @@ def run_ours(args):
                 threads = host_threads()
                 t = cpu_reference_steps(data, 2, 1, threads)
                 cpu = {"value": n / float(statistics.median(t)), "unit": UNIT, "cores": threads,
-                       "kind": "reference",
+                       "physical_cores": physical_cores(), "kind": "reference",
                        "sample": f"2 full {args.workload} steps (ib::spread_fused + ib::interpolate, "
                                  "oracle/_ref, OpenMP) after 1 warm-up, median"}
         except Exception as exc:  # pragma: no cover

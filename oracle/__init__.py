@@ -84,6 +84,8 @@ _ORACLE_SIGS = {
     "or_spread_fused": (C.c_int, [_G, _dp, _dp, _sz, _dp, _up, _up, _up, C.POINTER(_sz)]),
     "or_interpolate": (C.c_int, [_G, _dp, _dp, _sz, _dp]),
     "or_scatter_points": (None, [C.c_uint64, C.c_double, C.c_uint64, _dp]),
+    "or_home_cells": (None, [_G, _dp, _sz, C.c_int, C.c_int,
+                             np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")]),
 }
 
 _REF_SIGS = {
@@ -177,26 +179,15 @@ def interpolate(g, field, points):
     return out
 
 
-def home_cells(g, points, wrap=True):
+def home_cells(g, points, wrap=True, support=4):
     """cell_index(wrap_position(x)) with periodic axes wrapped into [0, n)
     (grid.hpp:121-151, 197-207): the home cell of every point, (n, dim) ints.
     wrap=False leaves the cell unwrapped (it can equal n on a periodic axis)."""
-    p = _pts(points, g.dim).reshape(-1, g.dim)
-    out = np.zeros((p.shape[0], g.dim), np.int64)
-    x = (C.c_double * 3)()
-    w = (C.c_double * 3)()
-    c = (C.c_int * 3)()
-    for i in range(p.shape[0]):
-        for a in range(g.dim):
-            x[a] = p[i, a]
-        lib().or_wrap_position(C.byref(g), x, w)
-        lib().or_cell_index(C.byref(g), w, 4, c)
-        for a in range(g.dim):
-            v = c[a]
-            if g.periodic[a] and wrap:
-                v %= g.extent[a]
-            out[i, a] = v
-    return out
+    p = _pts(points, g.dim)
+    n = p.size // g.dim
+    out = np.zeros(max(n, 1) * g.dim, np.int32)
+    lib().or_home_cells(C.byref(g), p, n, int(support), 1 if wrap else 0, out)
+    return out[: n * g.dim].reshape(n, g.dim).astype(np.int64)
 
 
 def scatter_points(n, edge, seed):

@@ -347,6 +347,25 @@ int or_interpolate(const or_grid* g, const double* field, const double* points, 
   return 0;
 }
 
+/* Home cells of many points (wrap_position + cell_index, grid.hpp:121-130,
+ * 197-207), periodic axes wrapped into [0, n) when wrap != 0: the binning
+ * the sampled-parity tests use to pick the points that reach a grid region. */
+void or_home_cells(const or_grid* g, const double* points, size_t n, int support, int wrap,
+                   int32_t* out) {
+  const int D = g->dim;
+  for (size_t i = 0; i < n; ++i) {
+    double xw[3];
+    int c[3];
+    or_wrap_position(g, points + i * D, xw);
+    or_cell_index(g, xw, support, c);
+    for (int a = 0; a < D; ++a) {
+      int v = c[a];
+      if (wrap && g->periodic[a]) v = wrap_cell(v, g->extent[a]);
+      out[i * D + a] = v;
+    }
+  }
+}
+
 /* ---- std::mt19937_64 (parameters of the C++ standard, [rand.predef]) ---- */
 typedef struct {
   uint64_t mt[312];

@@ -75,6 +75,10 @@ int or_spread_fused(const or_grid* g, const double* points, const double* values
 int or_interpolate(const or_grid* g, const double* field, const double* points, size_t n,
                    double* out);
 
+/* Home cells of n points (periodic axes wrapped into [0, n) when wrap != 0). */
+void or_home_cells(const or_grid* g, const double* points, size_t n, int support, int wrap,
+                   int32_t* out /* n * dim */);
+
 /* Deterministic synthetic inputs used by tests and the CPU baseline:
  * scatter_points (bench/setup.hpp:46-53): mt19937_64(seed), (rng()>>11)*2^-53*edge. */
 void or_scatter_points(uint64_t n, double edge, uint64_t seed, double* out /* n*3 */);
