@@ -48,9 +48,31 @@ typedef enum {
   IBC_ERR_ALLOC = 4
 } ibc_status;
 
-/* Delta kernels.  The reference ships exactly one: CosineKernel,
- * phi(r) = (1 + cos(pi r / 2)) / 4 on |r| < 2, support 4 (kernel.hpp:23-36). */
-typedef enum { IBC_KERNEL_COSINE4 = 0 } ibc_kernel;
+/* Delta kernels (the reference's Kernel concept, kernel.hpp:16-21, is a
+ * compile-time template parameter; the device takes these, by id).
+ *   COSINE4  the reference's CosineKernel: phi(r) = (1 + cos(pi r / 2)) / 4 on
+ *            |r| < 2, support 4 (kernel.hpp:23-36);
+ *   PESKIN4  Peskin's standard 4-point kernel (Peskin 2002, Eq. 6.27):
+ *            (3 - 2|r| + sqrt(1 + 4|r| - 4r^2)) / 8 on |r| <= 1,
+ *            (5 - 2|r| - sqrt(-7 + 12|r| - 4r^2)) / 8 on 1 < |r| < 2;
+ *   ROMA3    the 3-point kernel of Roma, Peskin & Berger (1999), odd support
+ *            (cell_index half = 0.5, grid.hpp:121-130):
+ *            (1 + sqrt(1 - 3r^2)) / 3 on |r| <= 1/2,
+ *            (5 - 3|r| - sqrt(1 - 3(1 - |r|)^2)) / 6 on 1/2 < |r| < 3/2;
+ *   LINEAR2  the 2-point hat, 1 - |r| on |r| < 1.
+ * Support-4 kernels run the fast paths (bank / pull sweeps, TMA gather);
+ * the others the generic radix-sorted tiles.  Unknown ids are rejected with
+ * IBC_ERR_INVALID_ARGUMENT ("unsupported kernel support size",
+ * spread.hpp:64-65). */
+typedef enum {
+  IBC_KERNEL_COSINE4 = 0,
+  IBC_KERNEL_PESKIN4 = 1,
+  IBC_KERNEL_ROMA3 = 2,
+  IBC_KERNEL_LINEAR2 = 3
+} ibc_kernel;
+
+/* Kernel::support() of an id (kernel.hpp:34); 0 for an unknown id. */
+int ibc_kernel_support(ibc_kernel kernel);
 
 /* ib::SpreadAlgorithm (spread.hpp:21).  Every algorithm computes the same
  * operator; on the device all of them run the write-once tiled spread. */
@@ -192,9 +214,41 @@ ibc_status ibc_interpolate_slab_device(ibc_context* ctx, const ibc_grid* local_g
 ibc_status ibc_home_planes_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
                                   const double* d_points, size_t n, int32_t* d_planes);
 
-/* ib::stats (stats.hpp:9-25): every operation adds n_points * 4^dim. */
+/* ---- Primitives of the reference's sort / reduce API (sort.hpp, reduce.hpp).
+ * The operators never call these (their sort and reduction are fused into the
+ * bucket sort and the write-once sweeps); they are exported so the
+ * reference's own callers of the primitives (bench/verify.hpp:234-322,
+ * tests/primitives_test.cpp) run on the device too.  Host-buffer forms are
+ * synchronous; `workers` is accepted and ignored. */
+
+/* ib::key_value_sort<Payload> (sort.hpp:16-71): stable LSD radix sort of n
+ * 32-bit keys, in place, carrying a payload of payload_bytes bytes per key
+ * (4 for uint32_t; 0 = none).  Bit-identical to std::stable_sort by key. */
+ibc_status ibc_key_value_sort(ibc_context* ctx, uint32_t* keys, void* payload,
+                              size_t payload_bytes, size_t n, int workers);
+ibc_status ibc_key_value_sort_device(ibc_context* ctx, uint32_t* d_keys, void* d_payload,
+                                     size_t payload_bytes, size_t n); /* async */
+/* ib::segmented_reduce_rows (reduce.hpp:70-137; ib::segmented_reduce at
+ * width 1, :139-145): sums consecutive rows of `width` doubles while their
+ * (nondecreasing) keys match; writes q run keys and q summed rows.  Each run
+ * is a left fold in index order (the reference at workers == 1, bit for
+ * bit).  Decreasing keys -> IBC_ERR_INVALID_ARGUMENT (the reference asserts). */
+ibc_status ibc_segmented_reduce_rows(ibc_context* ctx, const uint32_t* sorted_keys,
+                                     const double* values, size_t n, size_t width,
+                                     uint32_t* out_keys, size_t out_keys_cap, double* out_values,
+                                     size_t out_values_cap, int workers, size_t* q);
+/* ib::count_unique (reduce.hpp:57-69) and detail::collect_unique_keys
+ * (:36-52): number of runs / the run keys of sorted keys. */
+ibc_status ibc_count_unique(ibc_context* ctx, const uint32_t* sorted_keys, size_t n, int workers,
+                            size_t* q);
+ibc_status ibc_collect_unique_keys(ibc_context* ctx, const uint32_t* sorted_keys, size_t n,
+                                   uint32_t* out_keys, size_t out_cap, size_t* q);
+
+/* ib::stats (stats.hpp:9-25): every operation adds n_points * support^dim. */
 uint64_t ibc_delta_evaluations(void);
 void ibc_reset_delta_evaluations(void);
+/* ib::stats::add_delta_evaluations (stats.hpp:23-25). */
+void ibc_add_delta_evaluations(uint64_t n);
 
 #ifdef __cplusplus
 }

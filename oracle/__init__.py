@@ -80,6 +80,12 @@ _ORACLE_SIGS = {
     "or_key_value_sort": (None, [_up, _up, _sz]),
     "or_segmented_reduce": (_sz, [_up, _dp, _sz, _up, _dp]),
     "or_prepare_keys": (_sz, [_G, _dp, _sz, _up, _up, _up]),
+    "or_kernel_support": (C.c_int, [C.c_int]),
+    "or_kernel_phi": (C.c_double, [C.c_int, C.c_double]),
+    "or_prepare_keys_k": (_sz, [_G, C.c_int, _dp, _sz, _up, _up, _up]),
+    "or_spread_serial_k": (C.c_int, [_G, C.c_int, _dp, _dp, _sz, _dp]),
+    "or_spread_fused_k": (C.c_int, [_G, C.c_int, _dp, _dp, _sz, _dp, _up, _up, _up, C.POINTER(_sz)]),
+    "or_interpolate_k": (C.c_int, [_G, C.c_int, _dp, _dp, _sz, _dp]),
     "or_spread_serial": (C.c_int, [_G, _dp, _dp, _sz, _dp]),
     "or_spread_fused": (C.c_int, [_G, _dp, _dp, _sz, _dp, _up, _up, _up, C.POINTER(_sz)]),
     "or_interpolate": (C.c_int, [_G, _dp, _dp, _sz, _dp]),
@@ -92,6 +98,9 @@ _REF_SIGS = {
     "ref_spread": (C.c_int, [C.c_int, _G, _dp, _dp, _sz, C.c_int, C.c_int, _dp,
                              C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_sz)]),
     "ref_interpolate": (C.c_int, [_G, _dp, _dp, _sz, C.c_int, _dp]),
+    "ref_spread_k": (C.c_int, [C.c_int, C.c_int, _G, _dp, _dp, _sz, C.c_int, C.c_int, _dp,
+                               C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_sz)]),
+    "ref_interpolate_k": (C.c_int, [C.c_int, _G, _dp, _dp, _sz, C.c_int, _dp]),
     "ref_cell_keys": (C.c_int, [_G, _dp, _sz, _up]),
     "ref_grid_check": (C.c_int, [_G]),
     "ref_key_value_sort": (None, [_up, _up, _sz, C.c_int]),
@@ -138,25 +147,34 @@ def _pts(points, d):
 
 
 # ---------------------------------------------------------------- C restatement
-def prepare_keys(g, points):
+# Kernel ids (include/ibcuda.h ibc_kernel): 0 cosine (the reference's
+# CosineKernel), 1 Peskin 4-point, 2 Roma 3-point, 3 hat.
+KERNELS = {"cosine4": 0, "peskin4": 1, "roma3": 2, "linear2": 3}
+
+
+def kernel_phi(kernel, r):
+    return lib().or_kernel_phi(int(kernel), float(r))
+
+
+def prepare_keys(g, points, kernel=0):
     p = _pts(points, g.dim)
     n = p.size // g.dim
     keys = np.zeros(max(n, 1), np.uint32)
     perm = np.zeros(max(n, 1), np.uint32)
     run = np.zeros(max(n, 1), np.uint32)
-    q = lib().or_prepare_keys(C.byref(g), p, n, keys, perm, run)
+    q = lib().or_prepare_keys_k(C.byref(g), int(kernel), p, n, keys, perm, run)
     return keys[:n], perm[:n], run[:q]
 
 
-def spread_serial(g, points, values):
+def spread_serial(g, points, values, kernel=0):
     p = _pts(points, g.dim)
     v = np.ascontiguousarray(values, dtype=np.float64)
     out = np.zeros(grid_points(g), np.float64)
-    lib().or_spread_serial(C.byref(g), p, v, v.size, out)
+    lib().or_spread_serial_k(C.byref(g), int(kernel), p, v, v.size, out)
     return out
 
 
-def spread_fused(g, points, values):
+def spread_fused(g, points, values, kernel=0):
     """Returns (field, keys, perm, run_keys) exactly as ws.* after spread_fused."""
     p = _pts(points, g.dim)
     v = np.ascontiguousarray(values, dtype=np.float64)
@@ -166,16 +184,16 @@ def spread_fused(g, points, values):
     perm = np.zeros(max(n, 1), np.uint32)
     run = np.zeros(max(n, 1), np.uint32)
     q = _sz(0)
-    lib().or_spread_fused(C.byref(g), p, v, n, out, keys, perm, run, C.byref(q))
+    lib().or_spread_fused_k(C.byref(g), int(kernel), p, v, n, out, keys, perm, run, C.byref(q))
     return out, keys[:n], perm[:n], run[: q.value]
 
 
-def interpolate(g, field, points):
+def interpolate(g, field, points, kernel=0):
     p = _pts(points, g.dim)
     f = np.ascontiguousarray(field, dtype=np.float64)
     n = p.size // g.dim
     out = np.zeros(n, np.float64)
-    lib().or_interpolate(C.byref(g), f, p, n, out)
+    lib().or_interpolate_k(C.byref(g), int(kernel), f, p, n, out)
     return out
 
 
@@ -197,7 +215,7 @@ def scatter_points(n, edge, seed):
 
 
 # ---------------------------------------------------------------- reference build
-def ref_spread(g, points, values, algo="fused", workers=1, sweep_width=8):
+def ref_spread(g, points, values, algo="fused", workers=1, sweep_width=8, kernel=0):
     codes = {"serial": 0, "fused": 1, "buffered": 2, "otf": 3}
     p = _pts(points, g.dim)
     v = np.ascontiguousarray(values, dtype=np.float64)
@@ -207,19 +225,19 @@ def ref_spread(g, points, values, algo="fused", workers=1, sweep_width=8):
     perm = np.zeros(max(n, 1), np.uint32)
     run = np.zeros(max(n, 1), np.uint32)
     q = _sz(0)
-    rc = ref().ref_spread(codes[algo], C.byref(g), p, v, n, workers, sweep_width, out,
-                          keys.ctypes.data, perm.ctypes.data, run.ctypes.data, C.byref(q))
+    rc = ref().ref_spread_k(int(kernel), codes[algo], C.byref(g), p, v, n, workers, sweep_width,
+                            out, keys.ctypes.data, perm.ctypes.data, run.ctypes.data, C.byref(q))
     if rc:
         raise ValueError(f"reference spread failed with code {rc}")
     return out, keys[:n], perm[:n], run[: q.value]
 
 
-def ref_interpolate(g, field, points, workers=1):
+def ref_interpolate(g, field, points, workers=1, kernel=0):
     p = _pts(points, g.dim)
     f = np.ascontiguousarray(field, dtype=np.float64)
     n = p.size // g.dim
     out = np.zeros(n, np.float64)
-    rc = ref().ref_interpolate(C.byref(g), f, p, n, workers, out)
+    rc = ref().ref_interpolate_k(int(kernel), C.byref(g), f, p, n, workers, out)
     if rc:
         raise ValueError(f"reference interpolate failed with code {rc}")
     return out

@@ -103,6 +103,37 @@ double or_cosine_phi(double r) {
   return 0.25 * (1.0 + cos(0.5 * OR_PI * r));
 }
 
+/* The other kernels the device takes (include/ibcuda.h ibc_kernel); the
+ * reference's Kernel concept (kernel.hpp:16-21) admits any such phi.  The
+ * same formulas are compiled into the reference build as Kernel structs
+ * (oracle/ref_driver.cpp) to pin this restatement. */
+int or_kernel_support(int kernel) {
+  switch (kernel) {
+    case 0: case 1: return 4;
+    case 2: return 3;
+    case 3: return 2;
+    default: return 0;
+  }
+}
+
+double or_kernel_phi(int kernel, double r) {
+  const double a = fabs(r);
+  switch (kernel) {
+    case 1: /* Peskin 4-point (Peskin 2002, Eq. 6.27) */
+      if (!(a < 2.0)) return 0.0;
+      if (a <= 1.0) return (3.0 - 2.0 * a + sqrt(1.0 + 4.0 * a - 4.0 * a * a)) * 0.125;
+      return (5.0 - 2.0 * a - sqrt(fmax(0.0, -7.0 + 12.0 * a - 4.0 * a * a))) * 0.125;
+    case 2: /* Roma, Peskin & Berger (1999) 3-point */
+      if (!(a < 1.5)) return 0.0;
+      if (a <= 0.5) return (1.0 + sqrt(1.0 - 3.0 * a * a)) / 3.0;
+      return (5.0 - 3.0 * a - sqrt(1.0 - 3.0 * (1.0 - a) * (1.0 - a))) / 6.0;
+    case 3: /* 2-point hat */
+      return a < 1.0 ? 1.0 - a : 0.0;
+    default:
+      return or_cosine_phi(r);
+  }
+}
+
 void or_shift(int dim, int64_t j, int support, int* sigma) {
   int64_t z = j - 1;
   for (int a = 0; a < dim; ++a) {
@@ -219,15 +250,16 @@ size_t or_segmented_reduce(const uint32_t* sorted, const double* values, size_t 
   return out;
 }
 
-size_t or_prepare_keys(const or_grid* g, const double* points, size_t n, uint32_t* keys,
-                       uint32_t* perm, uint32_t* run_keys) {
+size_t or_prepare_keys_k(const or_grid* g, int kernel, const double* points, size_t n,
+                         uint32_t* keys, uint32_t* perm, uint32_t* run_keys) {
   /* prepare_spread head (spread.hpp:93-103). */
   const int D = g->dim;
+  const int support = or_kernel_support(kernel);
   for (size_t i = 0; i < n; ++i) {
     double xw[3];
     int c[3];
     or_wrap_position(g, points + i * D, xw);
-    or_cell_index(g, xw, OR_SUPPORT, c);
+    or_cell_index(g, xw, support, c);
     keys[i] = or_cell_key(g, c);
     perm[i] = (uint32_t)i;
   }
@@ -235,10 +267,15 @@ size_t or_prepare_keys(const or_grid* g, const double* points, size_t n, uint32_
   return or_collect_unique_keys(keys, n, run_keys);
 }
 
-int or_spread_serial(const or_grid* g, const double* points, const double* values, size_t n,
-                     double* out) {
+size_t or_prepare_keys(const or_grid* g, const double* points, size_t n, uint32_t* keys,
+                       uint32_t* perm, uint32_t* run_keys) {
+  return or_prepare_keys_k(g, 0, points, n, keys, perm, run_keys);
+}
+
+int or_spread_serial_k(const or_grid* g, int kernel, const double* points, const double* values,
+                       size_t n, double* out) {
   /* spread.hpp:129-159 */
-  const int D = g->dim, s = OR_SUPPORT, half = s / 2;
+  const int D = g->dim, s = or_kernel_support(kernel), half = s / 2;
   const int64_t nshift = shift_count(D, s);
   const double h = g->spacing;
   memset(out, 0, grid_points(g) * sizeof(double));
@@ -249,10 +286,10 @@ int or_spread_serial(const or_grid* g, const double* points, const double* value
     const double value = values[i];
     int dig[3] = {0, 0, 0};
     for (int64_t j = 0; j < nshift; ++j) {
-      double w = or_cosine_phi((dig[0] - half) - t[0]) / h;
+      double w = or_kernel_phi(kernel, (dig[0] - half) - t[0]) / h;
       int64_t off = off_tab[0][dig[0]];
       for (int a = 1; a < D; ++a) {
-        w *= or_cosine_phi((dig[a] - half) - t[a]) / h;
+        w *= or_kernel_phi(kernel, (dig[a] - half) - t[a]) / h;
         off += off_tab[a][dig[a]];
       }
       if (off >= 0) out[off] += w * value;
@@ -262,11 +299,16 @@ int or_spread_serial(const or_grid* g, const double* points, const double* value
   return 0;
 }
 
-int or_spread_fused(const or_grid* g, const double* points, const double* values, size_t n,
-                    double* out, uint32_t* keys_out, uint32_t* perm_out, uint32_t* run_keys_out,
-                    size_t* q_out) {
+int or_spread_serial(const or_grid* g, const double* points, const double* values, size_t n,
+                     double* out) {
+  return or_spread_serial_k(g, 0, points, values, n, out);
+}
+
+int or_spread_fused_k(const or_grid* g, int kernel, const double* points, const double* values,
+                      size_t n, double* out, uint32_t* keys_out, uint32_t* perm_out,
+                      uint32_t* run_keys_out, size_t* q_out) {
   /* spread.hpp:165-216 with workers == 1 (segmented reduce = left fold). */
-  const int D = g->dim, s = OR_SUPPORT;
+  const int D = g->dim, s = or_kernel_support(kernel);
   const int64_t nshift = shift_count(D, s);
   const double h = g->spacing;
   size_t alloc = n ? n : 1;
@@ -278,7 +320,7 @@ int or_spread_fused(const or_grid* g, const double* points, const double* values
   double* run_values = (double*)malloc(alloc * sizeof(double));
   uint32_t* tmp_keys = (uint32_t*)malloc(alloc * sizeof(uint32_t));
 
-  const size_t q = or_prepare_keys(g, points, n, keys, perm, run_keys);
+  const size_t q = or_prepare_keys_k(g, kernel, points, n, keys, perm, run_keys);
   for (size_t i = 0; i < n; ++i) support_window(g, points + (size_t)perm[i] * D, s, disp + i * D, NULL);
   int64_t* run_offsets = (int64_t*)malloc((q ? q : 1) * D * s * sizeof(int64_t));
   for (size_t r = 0; r < q; ++r) {
@@ -298,8 +340,8 @@ int or_spread_fused(const or_grid* g, const double* points, const double* values
     for (int a = 0; a < D; ++a) col[a] = run_offsets + (size_t)(a * s + sigma[a] + s / 2) * q;
     for (size_t i = 0; i < n; ++i) {
       const double* t = disp + i * D;
-      double w = or_cosine_phi(sigma[0] - t[0]) / h;
-      for (int a = 1; a < D; ++a) w *= or_cosine_phi(sigma[a] - t[a]) / h;
+      double w = or_kernel_phi(kernel, sigma[0] - t[0]) / h;
+      for (int a = 1; a < D; ++a) w *= or_kernel_phi(kernel, sigma[a] - t[a]) / h;
       staging[i] = w * values[perm[i]];
     }
     const size_t runs = or_segmented_reduce(keys, staging, n, tmp_keys, run_values);
@@ -319,10 +361,16 @@ int or_spread_fused(const or_grid* g, const double* points, const double* values
   return 0;
 }
 
-int or_interpolate(const or_grid* g, const double* field, const double* points, size_t n,
-                   double* out) {
+int or_spread_fused(const or_grid* g, const double* points, const double* values, size_t n,
+                    double* out, uint32_t* keys_out, uint32_t* perm_out, uint32_t* run_keys_out,
+                    size_t* q_out) {
+  return or_spread_fused_k(g, 0, points, values, n, out, keys_out, perm_out, run_keys_out, q_out);
+}
+
+int or_interpolate_k(const or_grid* g, int kernel, const double* field, const double* points,
+                     size_t n, double* out) {
   /* interpolate.hpp:22-58 */
-  const int D = g->dim, s = OR_SUPPORT, half = s / 2;
+  const int D = g->dim, s = or_kernel_support(kernel), half = s / 2;
   const int64_t nshift = shift_count(D, s);
   const double hd = pow(g->spacing, (double)D);
   const double h = g->spacing;
@@ -333,10 +381,10 @@ int or_interpolate(const or_grid* g, const double* field, const double* points, 
     double acc = 0.0;
     int dig[3] = {0, 0, 0};
     for (int64_t j = 0; j < nshift; ++j) {
-      double w = or_cosine_phi((dig[0] - half) - t[0]) / h;
+      double w = or_kernel_phi(kernel, (dig[0] - half) - t[0]) / h;
       int64_t off = off_tab[0][dig[0]];
       for (int a = 1; a < D; ++a) {
-        w *= or_cosine_phi((dig[a] - half) - t[a]) / h;
+        w *= or_kernel_phi(kernel, (dig[a] - half) - t[a]) / h;
         off += off_tab[a][dig[a]];
       }
       if (off >= 0) acc += w * field[off];
@@ -345,6 +393,11 @@ int or_interpolate(const or_grid* g, const double* field, const double* points, 
     out[i] = acc * hd;
   }
   return 0;
+}
+
+int or_interpolate(const or_grid* g, const double* field, const double* points, size_t n,
+                   double* out) {
+  return or_interpolate_k(g, 0, field, points, n, out);
 }
 
 /* Home cells of many points (wrap_position + cell_index, grid.hpp:121-130,

@@ -75,6 +75,21 @@ int or_spread_fused(const or_grid* g, const double* points, const double* values
 int or_interpolate(const or_grid* g, const double* field, const double* points, size_t n,
                    double* out);
 
+/* Kernel-generic forms (kernel ids of include/ibcuda.h: 0 cosine, 1 Peskin
+ * 4-point, 2 Roma 3-point, 3 hat): the reference's templates over other
+ * Kernel types (kernel.hpp:16-21; odd support: grid.hpp:121-130). */
+int or_kernel_support(int kernel);
+double or_kernel_phi(int kernel, double r);
+size_t or_prepare_keys_k(const or_grid* g, int kernel, const double* points, size_t n,
+                         uint32_t* keys, uint32_t* perm, uint32_t* run_keys);
+int or_spread_serial_k(const or_grid* g, int kernel, const double* points, const double* values,
+                       size_t n, double* out);
+int or_spread_fused_k(const or_grid* g, int kernel, const double* points, const double* values,
+                      size_t n, double* out, uint32_t* keys, uint32_t* perm, uint32_t* run_keys,
+                      size_t* q);
+int or_interpolate_k(const or_grid* g, int kernel, const double* field, const double* points,
+                     size_t n, double* out);
+
 /* Home cells of n points (periodic axes wrapped into [0, n) when wrap != 0). */
 void or_home_cells(const or_grid* g, const double* points, size_t n, int support, int wrap,
                    int32_t* out /* n * dim */);

@@ -9,6 +9,7 @@
 //   * time the reference CPU path in bench.py (cpu_baseline / --impl reference).
 // Nothing in the product library links it.
 #include <array>
+#include <cmath>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -32,6 +33,49 @@ typedef struct {
 }
 
 namespace {
+
+// Kernels beyond the reference's CosineKernel, written as the reference's
+// tests write their own Kernel types (tests/grid_test.cpp:18-23) and with
+// exactly the formulas of oracle/ib_oracle.c or_kernel_phi and the device.
+struct Peskin4Kernel {  // Peskin 2002, Eq. 6.27
+  double phi(double r) const {
+    const double a = std::abs(r);
+    if (!(a < 2.0)) return 0.0;
+    if (a <= 1.0) return (3.0 - 2.0 * a + std::sqrt(1.0 + 4.0 * a - 4.0 * a * a)) * 0.125;
+    return (5.0 - 2.0 * a - std::sqrt(std::fmax(0.0, -7.0 + 12.0 * a - 4.0 * a * a))) * 0.125;
+  }
+  int support() const { return 4; }
+  double radius() const { return 2.0; }
+};
+struct Roma3Kernel {  // Roma, Peskin & Berger 1999
+  double phi(double r) const {
+    const double a = std::abs(r);
+    if (!(a < 1.5)) return 0.0;
+    if (a <= 0.5) return (1.0 + std::sqrt(1.0 - 3.0 * a * a)) / 3.0;
+    return (5.0 - 3.0 * a - std::sqrt(1.0 - 3.0 * (1.0 - a) * (1.0 - a))) / 6.0;
+  }
+  int support() const { return 3; }
+  double radius() const { return 1.5; }
+};
+struct Linear2Kernel {
+  double phi(double r) const {
+    const double a = std::abs(r);
+    return a < 1.0 ? 1.0 - a : 0.0;
+  }
+  int support() const { return 2; }
+  double radius() const { return 1.0; }
+};
+
+template <class F>
+void with_kernel(int kernel, F&& f) {
+  switch (kernel) {
+    case 0: f(ib::CosineKernel{}); break;
+    case 1: f(Peskin4Kernel{}); break;
+    case 2: f(Roma3Kernel{}); break;
+    case 3: f(Linear2Kernel{}); break;
+    default: throw std::invalid_argument("kernel");
+  }
+}
 
 template <std::size_t D>
 ib::StaggeredGrid<D> make_grid(const ref_grid* g) {
@@ -69,14 +113,13 @@ int guarded(F&& f) {
   }
 }
 
-template <std::size_t D>
-void spread_d(int algo, const ref_grid* gd, const double* pts, const double* vals, std::size_t n,
-              int workers, int b, double* out, std::uint32_t* keys, std::uint32_t* perm,
-              std::uint32_t* run_keys, std::size_t* q) {
+template <std::size_t D, class K>
+void spread_dk(const K& k, int algo, const ref_grid* gd, const double* pts, const double* vals,
+               std::size_t n, int workers, int b, double* out, std::uint32_t* keys,
+               std::uint32_t* perm, std::uint32_t* run_keys, std::size_t* q) {
   const auto g = make_grid<D>(gd);
   const auto points = make_points<D>(pts, n);
   std::span<const double> values(vals, n);
-  const ib::CosineKernel k;
   ib::GridField<D> res(g);
   if (algo == 0) {
     res = ib::spread_serial(points, values, g, k);
@@ -95,14 +138,25 @@ void spread_d(int algo, const ref_grid* gd, const double* pts, const double* val
 }
 
 template <std::size_t D>
-void interp_d(const ref_grid* gd, const double* field, const double* pts, std::size_t n,
-              int workers, double* out) {
+void spread_d(int kernel, int algo, const ref_grid* gd, const double* pts, const double* vals,
+              std::size_t n, int workers, int b, double* out, std::uint32_t* keys,
+              std::uint32_t* perm, std::uint32_t* run_keys, std::size_t* q) {
+  with_kernel(kernel, [&](const auto& k) {
+    spread_dk<D>(k, algo, gd, pts, vals, n, workers, b, out, keys, perm, run_keys, q);
+  });
+}
+
+template <std::size_t D>
+void interp_d(int kernel, const ref_grid* gd, const double* field, const double* pts,
+              std::size_t n, int workers, double* out) {
   const auto g = make_grid<D>(gd);
   ib::GridField<D> f(g);
   std::memcpy(f.values.data(), field, f.values.size() * sizeof(double));
   const auto points = make_points<D>(pts, n);
-  const auto r = ib::interpolate(f, points, ib::CosineKernel{}, workers);
-  std::memcpy(out, r.data(), n * sizeof(double));
+  with_kernel(kernel, [&](const auto& k) {
+    const auto r = ib::interpolate(f, points, k, workers);
+    std::memcpy(out, r.data(), n * sizeof(double));
+  });
 }
 
 template <std::size_t D>
@@ -153,18 +207,30 @@ void time_step_d(const ref_grid* gd, const double* x_star, const double* vals,
 
 extern "C" {
 
+int ref_spread_k(int kernel, int algo, const ref_grid* g, const double* pts, const double* vals,
+                 size_t n, int workers, int sweep_width, double* out, uint32_t* keys,
+                 uint32_t* perm, uint32_t* run_keys, size_t* q) {
+  return guarded([&] {
+    DISPATCH(g->dim, spread_d, kernel, algo, g, pts, vals, n, workers, sweep_width, out, keys,
+                               perm, run_keys, q);
+  });
+}
+
 int ref_spread(int algo, const ref_grid* g, const double* pts, const double* vals, size_t n,
                int workers, int sweep_width, double* out, uint32_t* keys, uint32_t* perm,
                uint32_t* run_keys, size_t* q) {
-  return guarded([&] {
-    DISPATCH(g->dim, spread_d, algo, g, pts, vals, n, workers, sweep_width, out, keys, perm,
-                               run_keys, q);
-  });
+  return ref_spread_k(0, algo, g, pts, vals, n, workers, sweep_width, out, keys, perm, run_keys,
+                      q);
+}
+
+int ref_interpolate_k(int kernel, const ref_grid* g, const double* field, const double* pts,
+                      size_t n, int workers, double* out) {
+  return guarded([&] { DISPATCH(g->dim, interp_d, kernel, g, field, pts, n, workers, out); });
 }
 
 int ref_interpolate(const ref_grid* g, const double* field, const double* pts, size_t n,
                     int workers, double* out) {
-  return guarded([&] { DISPATCH(g->dim, interp_d, g, field, pts, n, workers, out); });
+  return ref_interpolate_k(0, g, field, pts, n, workers, out);
 }
 
 int ref_cell_keys(const ref_grid* g, const double* pts, size_t n, uint32_t* keys) {

@@ -19,6 +19,9 @@ IBC_ERR_CUDA = 3
 IBC_ERR_ALLOC = 4
 
 IBC_KERNEL_COSINE4 = 0
+IBC_KERNEL_PESKIN4 = 1
+IBC_KERNEL_ROMA3 = 2
+IBC_KERNEL_LINEAR2 = 3
 
 IBC_SPREAD_SERIAL = 0
 IBC_SPREAD_FUSED = 1
@@ -96,6 +99,14 @@ SIGNATURES = {
     "ibc_spread_slab_device": (_st, [_vp, _G, C.POINTER(IbcSlab), C.c_int, _vp, _vp, _sz, _vp, _vp]),
     "ibc_interpolate_slab_device": (_st, [_vp, _G, C.POINTER(IbcSlab), C.c_int, _vp, _vp, _sz, _vp]),
     "ibc_home_planes_device": (_st, [_vp, _G, C.c_int, _vp, _sz, _vp]),
+    "ibc_kernel_support": (C.c_int, [C.c_int]),
+    "ibc_key_value_sort": (_st, [_vp, _vp, _vp, _sz, _sz, C.c_int]),
+    "ibc_key_value_sort_device": (_st, [_vp, _vp, _vp, _sz, _sz]),
+    "ibc_segmented_reduce_rows": (_st, [_vp, _vp, _vp, _sz, _sz, _vp, _sz, _vp, _sz, C.c_int,
+                                        C.POINTER(_sz)]),
+    "ibc_count_unique": (_st, [_vp, _vp, _sz, C.c_int, C.POINTER(_sz)]),
+    "ibc_collect_unique_keys": (_st, [_vp, _vp, _sz, _vp, _sz, C.POINTER(_sz)]),
+    "ibc_add_delta_evaluations": (None, [C.c_uint64]),
     "ibc_delta_evaluations": (C.c_uint64, []),
     "ibc_reset_delta_evaluations": (None, []),
 }

@@ -80,17 +80,23 @@ size_t grid_points(const ibc_grid* g) {
   return p;
 }
 
+static_assert(IBC_KERNEL_COSINE4 == ibc::kKernelCosine4 && IBC_KERNEL_PESKIN4 == ibc::kKernelPeskin4 &&
+                  IBC_KERNEL_ROMA3 == ibc::kKernelRoma3 && IBC_KERNEL_LINEAR2 == ibc::kKernelLinear2,
+              "kernel ids");
+
+// check_spread_args (spread.hpp:64-65): support in [1, max_support]; the
+// device takes the kernels of ibc_kernel.
 void check_kernel(ibc_kernel k) {
-  if (k != IBC_KERNEL_COSINE4) invalid("unsupported kernel support size");
+  if (ibc::kernel_support((int)k) == 0) invalid("unsupported kernel support size");
 }
 
 void check_points(size_t n) {
   if (n > ibc::kMaxPoints) invalid("point count exceeds the device limit of 2^30 - 1");
 }
 
-uint64_t shift_count(int dim) {
+uint64_t shift_count(int dim, ibc_kernel k) {  // kernel.hpp:40-45
   uint64_t s = 1;
-  for (int a = 0; a < dim; ++a) s *= ibc::kSupport;
+  for (int a = 0; a < dim; ++a) s *= (uint64_t)ibc::kernel_support((int)k);
   return s;
 }
 
@@ -160,6 +166,7 @@ ibc_status ibc_context_destroy(ibc_context* ctx) {
     cudaStreamSynchronize(ctx->c.stream);
     ctx->c.spread_scratch.release_all();
     ctx->c.interp_scratch.release_all();
+    ctx->c.prim_scratch.release_all();
     for (auto& b : ctx->c.h_stage) b.release();
     for (auto& p : ctx->c.pending) {
       cudaEventDestroy(p.second.first);
@@ -261,7 +268,7 @@ ibc_status ibc_workspace_create(ibc_context* ctx, size_t n, const ibc_grid* grid
       ws->w.grid_points = grid_points(grid);
       ws->w.sweep_width = sweep_width;
       ws->w.s.reserve_points(n, true);
-      ws->w.s.reserve_rows(ibc::make_devgrid(*grid).nrows);
+      ws->w.s.reserve_rows(ibc::make_devgrid(*grid, IBC_KERNEL_COSINE4).nrows);
     } catch (...) {
       ws->w.s.release_all();
       delete ws;
@@ -380,7 +387,7 @@ ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
     if (!out) invalid("null output buffer");
     auto& c = ctx->c;
     use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
     // Serial/otf own no caller workspace: they run on the context's scratch.
     ibc_workspace* use_ws =
         (algorithm == IBC_SPREAD_FUSED || algorithm == IBC_SPREAD_BUFFERED) ? ws : nullptr;
@@ -398,7 +405,7 @@ ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
     ibc::spread_pipeline(c, g, c.h_stage[0].p, c.h_stage[1].p, n_points, s, c.h_stage[2].p);
     IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream));
     IBC_CUDA(cudaStreamSynchronize(c.stream));
-    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim), std::memory_order_relaxed);
+    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
 }
 
@@ -415,7 +422,7 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
     if (n_points && (!points || !out)) invalid("null point buffer");
     auto& c = ctx->c;
     use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
     const size_t np = grid_points(grid);
     c.interp_scratch.reserve_points(n_points, false);
     c.interp_scratch.reserve_rows(g.nrows);
@@ -432,7 +439,7 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
       IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[3].p, n_points * 8, cudaMemcpyDeviceToHost,
                                c.stream));
     IBC_CUDA(cudaStreamSynchronize(c.stream));
-    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim), std::memory_order_relaxed);
+    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
 }
 
@@ -451,10 +458,10 @@ ibc_status ibc_spread_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel 
     if (!d_out) invalid("null output buffer");
     auto& c = ctx->c;
     use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
     ibc::PointScratch& s = spread_scratch_for(c, ws, n, g);
     ibc::spread_pipeline(c, g, d_points, d_values, n, s, d_out);
-    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
 }
 
@@ -468,16 +475,18 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
     check_points(n);
     auto& c = ctx->c;
     use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
     c.interp_scratch.reserve_points(n, false);
     c.interp_scratch.reserve_rows(g.nrows);
     ibc::interp_pipeline(c, g, d_field, d_points, n, c.interp_scratch, d_out);
-    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
 }
 
-static void check_slab(const ibc_grid* grid, const ibc_slab* slab) {
+static void check_slab(const ibc_grid* grid, const ibc_slab* slab, ibc_kernel kernel) {
   if (!slab) invalid("slab is null");
+  if (ibc::kernel_support((int)kernel) != ibc::kSupport)
+    invalid("the slab decomposition takes 4-point kernels (2 ghost planes below, 1 above)");
   if (grid->dim < 2) invalid("slab decomposition needs a 2- or 3-dimensional grid");
   const int a = grid->dim - 1;
   if (grid->periodic[a]) invalid("the slab axis of a local grid is not periodic");
@@ -491,7 +500,7 @@ ibc_status ibc_spread_slab_device(ibc_context* ctx, const ibc_grid* grid, const 
   return guarded([&] {
     if (!ctx) invalid("context is null");
     check_grid(grid);
-    check_slab(grid, slab);
+    check_slab(grid, slab, kernel);
     check_kernel(kernel);
     check_points(n);
     if (ws) {
@@ -501,10 +510,10 @@ ibc_status ibc_spread_slab_device(ibc_context* ctx, const ibc_grid* grid, const 
     if (!d_out) invalid("null output buffer");
     auto& c = ctx->c;
     use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid, *slab);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, *slab, (int)kernel);
     ibc::PointScratch& s = spread_scratch_for(c, ws, n, g);
     ibc::spread_pipeline(c, g, d_points, d_values, n, s, d_out);
-    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
 }
 
@@ -515,16 +524,16 @@ ibc_status ibc_interpolate_slab_device(ibc_context* ctx, const ibc_grid* grid,
   return guarded([&] {
     if (!ctx) invalid("context is null");
     check_grid(grid);
-    check_slab(grid, slab);
+    check_slab(grid, slab, kernel);
     check_kernel(kernel);
     check_points(n);
     auto& c = ctx->c;
     use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid, *slab);
+    const ibc::DevGrid g = ibc::make_devgrid(*grid, *slab, (int)kernel);
     c.interp_scratch.reserve_points(n, false);
     c.interp_scratch.reserve_rows(g.nrows);
     ibc::interp_pipeline(c, g, d_field, d_points, n, c.interp_scratch, d_out);
-    g_delta_evaluations.fetch_add(n * shift_count(grid->dim), std::memory_order_relaxed);
+    g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
 }
 
@@ -538,8 +547,114 @@ ibc_status ibc_home_planes_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
     if (n && (!d_points || !d_planes)) invalid("null buffer");
     auto& c = ctx->c;
     use_device(c);
-    ibc::home_planes(c, ibc::make_devgrid(*grid), d_points, n, d_planes);
+    ibc::home_planes(c, ibc::make_devgrid(*grid, (int)kernel), d_points, n, d_planes);
   });
+}
+
+int ibc_kernel_support(ibc_kernel kernel) { return ibc::kernel_support((int)kernel); }
+
+// ---------------------------------------------------------------- Primitives
+ibc_status ibc_key_value_sort_device(ibc_context* ctx, uint32_t* d_keys, void* d_payload,
+                                     size_t payload_bytes, size_t n) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    if (n && !d_keys) invalid("null key buffer");
+    if (n && payload_bytes && !d_payload) invalid("null payload buffer");
+    check_points(n);
+    use_device(ctx->c);
+    ibc::sort_keys_device(ctx->c, d_keys, payload_bytes ? d_payload : nullptr, payload_bytes, n,
+                          ctx->c.prim_scratch);
+  });
+}
+
+ibc_status ibc_key_value_sort(ibc_context* ctx, uint32_t* keys, void* payload, size_t payload_bytes,
+                              size_t n, int workers) {
+  (void)workers;
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    if (n && !keys) invalid("null key buffer");
+    if (n && payload_bytes && !payload) invalid("null payload buffer");
+    check_points(n);
+    if (n < 2) return;
+    auto& c = ctx->c;
+    use_device(c);
+    c.h_stage[0].ensure((n * 4 + 7) / 8);
+    c.h_stage[1].ensure((n * payload_bytes + 7) / 8 + 1);
+    auto* dk = reinterpret_cast<uint32_t*>(c.h_stage[0].p);
+    void* dp = payload_bytes ? static_cast<void*>(c.h_stage[1].p) : nullptr;
+    IBC_CUDA(cudaMemcpyAsync(dk, keys, n * 4, cudaMemcpyHostToDevice, c.stream));
+    if (dp) IBC_CUDA(cudaMemcpyAsync(dp, payload, n * payload_bytes, cudaMemcpyHostToDevice, c.stream));
+    ibc::sort_keys_device(c, dk, dp, payload_bytes, n, c.prim_scratch);
+    IBC_CUDA(cudaMemcpyAsync(keys, dk, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (dp) IBC_CUDA(cudaMemcpyAsync(payload, dp, n * payload_bytes, cudaMemcpyDeviceToHost, c.stream));
+    IBC_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+static void reduce_host(ibc_context* ctx, const uint32_t* keys, const double* values, size_t n,
+                        size_t width, uint32_t* out_keys, size_t out_keys_cap, double* out_values,
+                        size_t out_values_cap, size_t* q) {
+  if (!ctx || !q) invalid("null argument");
+  if (n && !keys) invalid("null key buffer");
+  if (values && width < 1) invalid("row width must be >= 1");
+  check_points(n);
+  *q = 0;
+  if (n == 0) return;
+  auto& c = ctx->c;
+  use_device(c);
+  c.h_stage[0].ensure((n * 4 + 7) / 8);
+  auto* dk = reinterpret_cast<uint32_t*>(c.h_stage[0].p);
+  IBC_CUDA(cudaMemcpyAsync(dk, keys, n * 4, cudaMemcpyHostToDevice, c.stream));
+  double* dv = nullptr;
+  double* dout = nullptr;
+  if (values) {
+    c.h_stage[1].ensure(n * width);
+    c.h_stage[2].ensure(n * width);
+    dv = c.h_stage[1].p;
+    dout = c.h_stage[2].p;
+    IBC_CUDA(cudaMemcpyAsync(dv, values, n * width * 8, cudaMemcpyHostToDevice, c.stream));
+  }
+  c.h_stage[3].ensure((n * 4 + 7) / 8);
+  auto* drk = reinterpret_cast<uint32_t*>(c.h_stage[3].p);
+  bool unsorted = false;
+  const size_t runs = ibc::runs_device(c, dk, n, c.prim_scratch, drk, dv, width, dout, &unsorted);
+  if (unsorted) invalid("keys must be sorted (nondecreasing)");
+  if (out_keys && out_keys_cap < runs) invalid("run key buffer too small");
+  if (out_values && out_values_cap < runs * width) invalid("run value buffer too small");
+  if (out_keys) IBC_CUDA(cudaMemcpyAsync(out_keys, drk, runs * 4, cudaMemcpyDeviceToHost, c.stream));
+  if (out_values && dout)
+    IBC_CUDA(cudaMemcpyAsync(out_values, dout, runs * width * 8, cudaMemcpyDeviceToHost, c.stream));
+  IBC_CUDA(cudaStreamSynchronize(c.stream));
+  *q = runs;
+}
+
+ibc_status ibc_segmented_reduce_rows(ibc_context* ctx, const uint32_t* sorted_keys,
+                                     const double* values, size_t n, size_t width,
+                                     uint32_t* out_keys, size_t out_keys_cap, double* out_values,
+                                     size_t out_values_cap, int workers, size_t* q) {
+  (void)workers;
+  return guarded([&] {
+    if (n && !values) invalid("null value buffer");
+    reduce_host(ctx, sorted_keys, values, n, width, out_keys, out_keys_cap, out_values,
+                out_values_cap, q);
+  });
+}
+
+ibc_status ibc_count_unique(ibc_context* ctx, const uint32_t* sorted_keys, size_t n, int workers,
+                            size_t* q) {
+  (void)workers;
+  return guarded([&] { reduce_host(ctx, sorted_keys, nullptr, n, 0, nullptr, 0, nullptr, 0, q); });
+}
+
+ibc_status ibc_collect_unique_keys(ibc_context* ctx, const uint32_t* sorted_keys, size_t n,
+                                   uint32_t* out_keys, size_t out_cap, size_t* q) {
+  return guarded([&] {
+    reduce_host(ctx, sorted_keys, nullptr, n, 0, out_keys, out_cap, nullptr, 0, q);
+  });
+}
+
+void ibc_add_delta_evaluations(uint64_t n) {
+  g_delta_evaluations.fetch_add(n, std::memory_order_relaxed);
 }
 
 uint64_t ibc_delta_evaluations(void) { return g_delta_evaluations.load(std::memory_order_relaxed); }

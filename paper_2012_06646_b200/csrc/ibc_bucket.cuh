@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
   for (int a = 0; a < D; ++a) {
     double w;
     c[a] = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(X + (size_t)i * D + a), &w);
-    sincos_half_pi(w, &tr[a][0], &tr[a][1]);
+    kernel_pair(g.kernel, w, &tr[a][0], &tr[a][1]);
   }
   double* r = rec + 8 * (size_t)slot;
   st_v4(r, tr[0][0], tr[0][1], tr[1][0], tr[1][1]);
@@ -291,7 +291,7 @@ __device__ __forceinline__ void write_record_from(const DevGrid& g, const double
     double u;
     const int c = cell_and_u(axis_of(g, a), g.h, g.inv_h, x[a], &u);
     if (a == 0) cx = c;
-    sincos_half_pi(u, &tr[a][0], &tr[a][1]);
+    kernel_pair(g.kernel, u, &tr[a][0], &tr[a][1]);
   }
   const double gq = gv * (0.25 * g.inv_h);
   double* r = rec + 8 * (size_t)o;

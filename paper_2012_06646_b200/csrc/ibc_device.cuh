@@ -11,7 +11,13 @@
 
 namespace ibc {
 
-constexpr int kSupport = 4;  // CosineKernel::support (kernel.hpp:34)
+constexpr int kSupport = 4;     // support of the fast paths (4-point kernels)
+constexpr int kMaxSupport = 4;  // largest support the generic paths take
+// Delta kernels (ibc_kernel in include/ibcuda.h).
+constexpr int kKernelCosine4 = 0;  // CosineKernel (kernel.hpp:23-36)
+constexpr int kKernelPeskin4 = 1;  // Peskin's standard 4-point kernel
+constexpr int kKernelRoma3 = 2;    // Roma-Peskin-Berger 3-point kernel (odd support)
+constexpr int kKernelLinear2 = 3;  // 2-point hat kernel
 // The onesweep look-back packs per-digit counts into 30 bits.
 constexpr uint32_t kMaxPoints = (1u << 30) - 1;
 
@@ -40,6 +46,13 @@ struct DevGrid {
   int zg_n;             // global extent of the last axis
   int zg_periodic;      // global periodicity of the last axis
   double zg_len;        // global axis length
+  // Delta kernel (kernel.hpp:16-21): id, support s, first shift -floor(s/2)
+  // (kernel.hpp:49-58) and cell_index's half = 0 / 0.5 for even / odd s
+  // (grid.hpp:121-130).
+  int kernel;
+  int support;
+  int slo;
+  double half;
 };
 
 __device__ __forceinline__ int wrap_cell(int i, int e) {  // grid.hpp:97-101
@@ -73,11 +86,11 @@ __device__ __forceinline__ int cell_of(const DevGrid& g, int a, double x, double
   *xw = w;
   const double d = __dsub_rn(w, g.origin[a]);
   const double q = __dmul_rn(d, g.inv_h);
-  const double t = __dsub_rn(q, g.alpha[a]);
+  const double t = __dsub_rn(__dsub_rn(q, g.alpha[a]), g.half);
   const double c = ceil(t);
   const double margin = 1e-13 * (fabs(q) + 1.0);
   if (c - t > margin && t - (c - 1.0) > margin) return (int)c;
-  return (int)ceil(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]));
+  return (int)ceil(__dsub_rn(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]), g.half));
 }
 
 // Last axis of a slab grid: global wrap and cell (same arithmetic as
@@ -95,10 +108,11 @@ __device__ __forceinline__ int cell_of_slab(const DevGrid& g, double x, double* 
   }
   const double d = __dsub_rn(w, g.origin[a]);
   const double q = __dmul_rn(d, g.inv_h);
-  const double t = __dsub_rn(q, g.alpha[a]);
+  const double t = __dsub_rn(__dsub_rn(q, g.alpha[a]), g.half);
   double c = ceil(t);
   const double margin = 1e-13 * (fabs(q) + 1.0);
-  if (!(c - t > margin && t - (c - 1.0) > margin)) c = ceil(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]));
+  if (!(c - t > margin && t - (c - 1.0) > margin))
+    c = ceil(__dsub_rn(__dsub_rn(__ddiv_rn(d, g.h), g.alpha[a]), g.half));
   const int cu = (int)c;
   const int cw = g.zg_periodic ? wrap_cell(cu, g.zg_n) : cu;
   *xw = w - (double)(cu - cw) * g.h;
@@ -108,7 +122,7 @@ __device__ __forceinline__ int cell_of_slab(const DevGrid& g, double x, double* 
 // One axis of a DevGrid picked with a runtime index (selects, so the grid
 // stays in the parameter bank instead of being copied to local memory).
 struct Axis {
-  double o, len, alpha;
+  double o, len, alpha, half;
   int n, periodic;
   int shift;  // slab axis: local = global - shift
 };
@@ -120,6 +134,7 @@ __device__ __forceinline__ Axis axis_of(const DevGrid& g, int a) {
   r.alpha = a == 0 ? g.alpha[0] : (a == 1 ? g.alpha[1] : g.alpha[2]);
   r.n = a == 0 ? g.n[0] : (a == 1 ? g.n[1] : g.n[2]);
   r.periodic = a == 0 ? g.periodic[0] : (a == 1 ? g.periodic[1] : g.periodic[2]);
+  r.half = g.half;
   r.shift = 0;
   if (g.zslab && a == g.dim - 1) {  // global wrap, then the local shift
     r.len = g.zg_len;
@@ -142,10 +157,11 @@ __device__ __forceinline__ int cell_and_u(const Axis& A, double h, double inv_h,
   }
   const double d = __dsub_rn(w, A.o);
   const double q = __dmul_rn(d, inv_h);
-  const double t = __dsub_rn(q, A.alpha);
+  const double t = __dsub_rn(__dsub_rn(q, A.alpha), A.half);
   double c = ceil(t);
   const double margin = 1e-13 * (fabs(q) + 1.0);
-  if (!(c - t > margin && t - (c - 1.0) > margin)) c = ceil(__dsub_rn(__ddiv_rn(d, h), A.alpha));
+  if (!(c - t > margin && t - (c - 1.0) > margin))
+    c = ceil(__dsub_rn(__dsub_rn(__ddiv_rn(d, h), A.alpha), A.half));
   const int ci = (int)c;
   const double hp = __dadd_rn(__dmul_rn(h, __dadd_rn(c, A.alpha)), A.o);
   *u = -((w - hp) * inv_h);
@@ -217,9 +233,65 @@ __device__ __forceinline__ void cosine_weights(double t, double inv_h, double w[
   w[3] = (0.25 * (1.0 - s)) * inv_h;
 }
 
-// Padded axis (a >= dim): only sigma = 0 contributes, with factor 1.
-__device__ __forceinline__ void unit_weights(double w[4]) {
-  w[0] = 0.0; w[1] = 0.0; w[2] = 1.0; w[3] = 0.0;
+// Padded axis (a >= dim): only sigma = 0 (index -slo) contributes, factor 1.
+__device__ __forceinline__ void unit_weights(double w[4], int slo = -2) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w[k] = k == -slo ? 1.0 : 0.0;
+}
+
+// phi(r) of every supported kernel, written as the oracle writes it
+// (oracle/ib_oracle.c or_kernel_phi):
+//  COSINE4  (1 + cos(pi r / 2)) / 4 on |r| < 2 (kernel.hpp:24-27);
+//  PESKIN4  (3 - 2|r| + sqrt(1 + 4|r| - 4r^2)) / 8 on |r| <= 1,
+//           (5 - 2|r| - sqrt(-7 + 12|r| - 4r^2)) / 8 on 1 < |r| < 2;
+//  ROMA3    (1 + sqrt(1 - 3r^2)) / 3 on |r| <= 1/2,
+//           (5 - 3|r| - sqrt(1 - 3(1 - |r|)^2)) / 6 on 1/2 < |r| < 3/2;
+//  LINEAR2  1 - |r| on |r| < 1.
+__device__ __forceinline__ double kernel_phi(int k, double r) {
+  const double a = fabs(r);
+  if (k == kKernelPeskin4) {
+    if (!(a < 2.0)) return 0.0;
+    if (a <= 1.0) return (3.0 - 2.0 * a + sqrt(1.0 + 4.0 * a - 4.0 * a * a)) * 0.125;
+    return (5.0 - 2.0 * a - sqrt(fmax(0.0, -7.0 + 12.0 * a - 4.0 * a * a))) * 0.125;
+  }
+  if (k == kKernelRoma3) {
+    if (!(a < 1.5)) return 0.0;
+    if (a <= 0.5) return (1.0 + sqrt(1.0 - 3.0 * a * a)) / 3.0;
+    const double b = 1.0 - a;
+    return (5.0 - 3.0 * a - sqrt(1.0 - 3.0 * b * b)) / 6.0;
+  }
+  if (k == kKernelLinear2) return a < 1.0 ? 1.0 - a : 0.0;
+  if (!(a < 2.0)) return 0.0;
+  return 0.25 * (1.0 + cospi(0.5 * r));
+}
+
+// Weights phi(sigma - t) / h for sigma = slo .. slo + s - 1 (index sigma -
+// slo; entries past the support are 0) of any kernel: the generic paths.
+__device__ __forceinline__ void kernel_weights(const DevGrid& g, double t, double w[4]) {
+  if (g.kernel == kKernelCosine4) {
+    cosine_weights(t, g.inv_h, w);
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    w[k] = k < g.support ? kernel_phi(g.kernel, (double)(g.slo + k) - t) * g.inv_h : 0.0;
+}
+
+// The 4-point kernels' weight pair.  Both satisfy the even/odd partition of
+// unity (phi(-2+u) + phi(u) = phi(-1+u) + phi(1+u) = 1/2), so with u = -t in
+// [0, 1) their four weights are (1 - c)/4, (1 + s)/4, (1 + c)/4, (1 - s)/4 for
+// one pair (s, c) per axis -- the fast paths' records carry that pair:
+//   COSINE4  s = sin(pi u / 2), c = cos(pi u / 2);
+//   PESKIN4  with R = sqrt(1 + 4u - 4u^2): c = (1 - 2u + R) / 2,
+//            s = (2u - 1 + R) / 2.
+__device__ __forceinline__ void kernel_pair(int k, double u, double* sn, double* cs) {
+  if (k == kKernelPeskin4) {
+    const double R = sqrt(fma(4.0 * u, 1.0 - u, 1.0));
+    *cs = 0.5 * (1.0 - 2.0 * u + R);
+    *sn = 0.5 * (2.0 * u - 1.0 + R);
+    return;
+  }
+  sincos_half_pi(u, sn, cs);
 }
 
 // Programmatic dependent launch: the pipeline's kernels are launched with

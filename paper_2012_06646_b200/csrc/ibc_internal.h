@@ -58,6 +58,8 @@ struct PointScratch {
   DevBuf<double> rec;         // 12 x cap weight records (spread)
   DevBuf<uint32_t> run_keys;  // lazily filled
   DevBuf<uint32_t> block_counts;
+  DevBuf<uint32_t> prim_u32;          // primitives: run keys + run starts
+  DevBuf<unsigned char> prim_bytes;   // primitives: payload gather
   const uint32_t* sorted_keys = nullptr;
   const uint32_t* sorted_perm = nullptr;
   size_t last_n = 0;
@@ -81,6 +83,7 @@ struct Context {
   uint64_t spread_calls = 0, interp_calls = 0;
   PointScratch spread_scratch;  // spreads without a user workspace
   PointScratch interp_scratch;  // interpolation
+  PointScratch prim_scratch;    // sort / reduce primitives
   DevBuf<double> h_stage[4];    // device staging for host-buffer calls
   cudaEvent_t acquire_event();
   void prof_begin(int cls, cudaEvent_t* ev);
@@ -97,8 +100,17 @@ struct Workspace {
 };
 
 // Pipelines (ibc_kernels.cu).  All enqueue on ctx.stream; no host sync.
-DevGrid make_devgrid(const ibc_grid& g);
-DevGrid make_devgrid(const ibc_grid& g, const ibc_slab& slab);  // z-slab of a larger grid
+DevGrid make_devgrid(const ibc_grid& g, int kernel);
+DevGrid make_devgrid(const ibc_grid& g, const ibc_slab& slab, int kernel);  // z-slab of a larger grid
+// Support of a kernel id (ibc_kernel); 0 for an unknown id.
+inline int kernel_support(int k) {
+  switch (k) {
+    case kKernelCosine4: case kKernelPeskin4: return 4;
+    case kKernelRoma3: return 3;
+    case kKernelLinear2: return 2;
+    default: return 0;
+  }
+}
 // Wrapped home cell along the last axis of every point (slab binning key).
 void home_planes(Context& ctx, const DevGrid& g, const double* d_points, size_t n, int* d_planes);
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points,
@@ -110,5 +122,17 @@ size_t compute_run_keys(Context& ctx, PointScratch& s);
 // The stable (key, index) order of the last spread (ws.keys / ws.perm), on request.
 void ensure_observables(Context& ctx, PointScratch& s);
 size_t read_run_count(Context& ctx, PointScratch& s);
+
+// Primitives (sort.hpp / reduce.hpp) on device buffers, in the context stream.
+// Stable sort of n 32-bit keys in place, with a payload of `bytes` bytes per
+// key (may be null).
+void sort_keys_device(Context& ctx, uint32_t* d_keys, void* d_payload, size_t bytes, size_t n,
+                      PointScratch& s);
+// Runs of sorted keys: q (synchronizes); run keys to d_run_keys (may be
+// null); with values, the left fold of each run's rows of `width` doubles to
+// d_out.  *unsorted: some key decreases.
+size_t runs_device(Context& ctx, const uint32_t* d_keys, size_t n, PointScratch& s,
+                   uint32_t* d_run_keys, const double* d_values, size_t width, double* d_out,
+                   bool* unsorted);
 
 }  // namespace ibc

@@ -181,10 +181,10 @@ __global__ void __launch_bounds__(kBlock) prep_records_kernel(DevGrid g, const d
     if (a < D) {
       double xw;
       const int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
-      cosine_weights(displacement(g, a, xw, c), g.inv_h, w[a]);
+      kernel_weights(g, displacement(g, a, xw, c), w[a]);
       if (a == 0) c0 = g.periodic[0] ? wrap_cell(c, g.n[0]) : c;
     } else {
-      unit_weights(w[a]);
+      unit_weights(w[a], g.slo);
     }
   }
   const double gv = __ldg(G + i);
@@ -230,8 +230,11 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
 
   const double* wy = rec + (size_t)4 * n;
   const double* wz = rec + (size_t)8 * n;
-  const int szlo = g.dim >= 3 ? -2 : 0, szhi = g.dim >= 3 ? 1 : 0;
-  const int sylo = g.dim >= 2 ? -2 : 0, syhi = g.dim >= 2 ? 1 : 0;
+  // Shifts sigma = slo .. slo + s - 1 per axis (kernel.hpp:49-58); record
+  // weight index sigma - slo.
+  const int slo = g.slo, shi = g.slo + g.support - 1;
+  const int szlo = g.dim >= 3 ? slo : 0, szhi = g.dim >= 3 ? shi : 0;
+  const int sylo = g.dim >= 2 ? slo : 0, syhi = g.dim >= 2 ? shi : 0;
   const uint32_t le = lanemask_le();
 
   for (int tr = warp; tr < rows; tr += nwarps) {
@@ -255,8 +258,8 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
         const uint32_t row = (g.dim >= 2 ? (uint32_t)(cy + 1) : 0u) +
                              (g.dim >= 3 ? (uint32_t)(cz + 1) * (uint32_t)(g.n[1] + 2) : 0u);
         const uint32_t rb = __ldg(rowstart + row), re = __ldg(rowstart + row + 1);
-        const double* wyc = wy + (size_t)(sy + 2) * n;
-        const double* wzc = wz + (size_t)(sz + 2) * n;
+        const double* wyc = wy + (size_t)(sy - slo) * n;
+        const double* wzc = wz + (size_t)(sz - slo) * n;
         for (uint32_t base = rb; base < re; base += 32) {
           const uint32_t r = base + lane;
           const bool valid = r < re;
@@ -275,8 +278,8 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
           const int maxrank = __reduce_max_sync(0xffffffffu, (unsigned)rank);
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            int xt = cx + k - 2;
-            bool ok = valid;
+            int xt = cx + k + slo;
+            bool ok = valid && k < g.support;
             if (g.periodic[0]) xt = wrap_cell(xt, g.n[0]);
             else ok = ok && xt >= 0 && xt < g.n[0];
             xt -= x0;
@@ -322,22 +325,24 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(DevGrid g, const double*
     if (a < D) {
       double xw;
       const int c = cell_of(g, a, __ldg(X + (size_t)i * D + a), &xw);
-      cosine_weights(displacement(g, a, xw, c), g.inv_h, w[a]);
+      kernel_weights(g, displacement(g, a, xw, c), w[a]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        int cc = c + k - 2;
+        int cc = c + k + g.slo;
         if (g.periodic[a]) off[a][k] = stride * wrap_cell(cc, g.n[a]);
         else off[a][k] = (cc < 0 || cc >= g.n[a]) ? kInvalid : stride * cc;
       }
       stride *= g.n[a];
     } else {
-      unit_weights(w[a]);
+      unit_weights(w[a], g.slo);
 #pragma unroll
       for (int k = 0; k < 4; ++k) off[a][k] = 0;
     }
   }
-  const int zlo = D >= 3 ? 0 : 2, zhi = D >= 3 ? 3 : 2;
-  const int ylo = D >= 2 ? 0 : 2, yhi = D >= 2 ? 3 : 2;
+  // Weight indices 0 .. s-1; a padded axis contributes only sigma = 0.
+  const int s1 = g.support - 1, k0 = -g.slo;
+  const int zlo = D >= 3 ? 0 : k0, zhi = D >= 3 ? s1 : k0;
+  const int ylo = D >= 2 ? 0 : k0, yhi = D >= 2 ? s1 : k0;
   double acc = 0.0;
 #pragma unroll
   for (int kz = 0; kz < 4; ++kz) {
@@ -349,7 +354,7 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(DevGrid g, const double*
 #pragma unroll
       for (int kx = 0; kx < 4; ++kx) {
         const int64_t o = off[0][kx] + oyz;
-        if (o >= 0) {
+        if (kx <= s1 && o >= 0) {
           const double wt = (w[0][kx] * w[1][ky]) * w[2][kz];
           acc += wt * __ldg(field + o);
         }
@@ -550,9 +555,13 @@ SpreadTiling choose_tiling(const DevGrid& g) {
 
 }  // namespace
 
-DevGrid make_devgrid(const ibc_grid& gi) {
+DevGrid make_devgrid(const ibc_grid& gi, int kernel) {
   DevGrid g{};
   g.dim = gi.dim;
+  g.kernel = kernel;
+  g.support = kernel_support(kernel);
+  g.slo = -(g.support / 2);
+  g.half = (g.support % 2 == 0) ? 0.0 : 0.5;
   g.h = gi.spacing;
   g.inv_h = 1.0 / gi.spacing;
   uint64_t ks = 1;
@@ -583,8 +592,8 @@ DevGrid make_devgrid(const ibc_grid& gi) {
   return g;
 }
 
-DevGrid make_devgrid(const ibc_grid& gi, const ibc_slab& slab) {
-  DevGrid g = make_devgrid(gi);
+DevGrid make_devgrid(const ibc_grid& gi, const ibc_slab& slab, int kernel) {
+  DevGrid g = make_devgrid(gi, kernel);
   const int a = gi.dim - 1;
   g.zslab = 1;
   g.zfirst = slab.z_first;
@@ -640,6 +649,8 @@ void PointScratch::release_all() {
   hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
   bpair.release();
+  prim_u32.release();
+  prim_bytes.release();
   cap = 0;
 }
 
@@ -706,7 +717,10 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                             : (path == IBC_SPREAD_PATH_PULL || path == IBC_SPREAD_PATH_RADIX)
                                 ? bucket::kNoBankMode
                                 : sp::kPullRow;
-  const bool sweep = sweep_tiling(g, ctx.sms, pull_row, W, 1);
+  // The sweeps take the 4-point kernels (their records carry one weight pair
+  // per axis, ibc_device.cuh kernel_pair); other supports run the generic
+  // radix-sort + tiled path.
+  const bool sweep = g.support == kSupport && sweep_tiling(g, ctx.sms, pull_row, W, 1);
   if (!sweep_tiling(g, ctx.sms, pull_row, WB, bucket::kRowsPerWarp)) {  // bank window too large
     WB = W;
     W.pull_row = WB.pull_row = bucket::kNoBankMode;
@@ -1039,7 +1053,7 @@ bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, cons
 void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
                      size_t n, PointScratch& s, double* d_out) {
   if (n == 0) return;
-  if (interp_tma_path(ctx, g, d_field, d_points, n, s, d_out)) return;
+  if (g.support == kSupport && interp_tma_path(ctx, g, d_field, d_points, n, s, d_out)) return;
   // Generic gather (1-D/2-D grids, x extents the TMA rows do not take): one
   // thread per point in sorted order.
   cudaStream_t st = ctx.stream;
@@ -1089,5 +1103,199 @@ size_t compute_run_keys(Context& ctx, PointScratch& s) {
 }
 
 size_t read_run_count(Context& ctx, PointScratch& s) { return compute_run_keys(ctx, s); }
+
+// ---------------------------------------------------------------- primitives
+// ib::key_value_sort (sort.hpp:16-71), ib::count_unique (reduce.hpp:57-69)
+// and ib::segmented_reduce(_rows) (reduce.hpp:80-145) on the device, for
+// callers of the reference's primitive API (the operators above never call
+// them: their sort and reduction are fused into the bucket sort and sweeps).
+namespace {
+
+// Digit histograms of every pass over raw 32-bit keys (keys_hist_kernel
+// without the cell arithmetic).
+__global__ void __launch_bounds__(kKeysThreads) raw_hist_kernel(const uint32_t* __restrict__ keys,
+                                                                uint32_t n, uint32_t* __restrict__ gcount,
+                                                                uint32_t* __restrict__ cnt0, KeyDigits kd) {
+  __shared__ uint32_t sh[sort::kMaxPasses][sort::kMaxRadix];
+  for (int t = threadIdx.x; t < sort::kMaxPasses * sort::kMaxRadix; t += blockDim.x)
+    (&sh[0][0])[t] = 0u;
+  __syncthreads();
+  const uint32_t base = blockIdx.x * (uint32_t)sort::kTile;
+  for (int j = 0; j < sort::kTile / kKeysThreads; ++j) {
+    const uint32_t i = base + (uint32_t)j * kKeysThreads + threadIdx.x;
+    if (i < n) {
+      const uint32_t key = __ldg(keys + i);
+#pragma unroll
+      for (int p = 0; p < sort::kMaxPasses; ++p)
+        if (p < kd.passes) atomicAdd(&sh[p][(key >> kd.shift[p]) & ((1u << kd.bits[p]) - 1u)], 1u);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < (1 << kd.bits[0]); t += blockDim.x)
+    cnt0[(size_t)blockIdx.x * sort::kMaxRadix + t] = sh[0][t];
+#pragma unroll
+  for (int p = 0; p < sort::kMaxPasses; ++p) {
+    if (p >= kd.passes) break;
+    for (int t = threadIdx.x; t < (1 << kd.bits[p]); t += blockDim.x) {
+      const uint32_t c = sh[p][t];
+      if (c) atomicAdd(gcount + p * sort::kMaxRadix + t, c);
+    }
+  }
+}
+
+// out[i] = in[perm[i]] for elements of `bytes` bytes (4-byte words when the
+// size allows).
+__global__ void __launch_bounds__(kBlock) gather_payload_kernel(const unsigned char* __restrict__ in,
+                                                                unsigned char* __restrict__ out,
+                                                                const uint32_t* __restrict__ perm,
+                                                                size_t n, size_t bytes) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const size_t src = (size_t)__ldg(perm + i) * bytes, dst = i * bytes;
+  if (bytes % 4 == 0) {
+    for (size_t b = 0; b < bytes; b += 4)
+      *reinterpret_cast<uint32_t*>(out + dst + b) = *reinterpret_cast<const uint32_t*>(in + src + b);
+  } else {
+    for (size_t b = 0; b < bytes; ++b) out[dst + b] = in[src + b];
+  }
+}
+
+// Run heads -> run keys and run start positions (head_write_kernel + starts),
+// plus an "unsorted" flag if any key decreases.
+__global__ void __launch_bounds__(kBlock) head_start_kernel(const uint32_t* __restrict__ sk, uint32_t n,
+                                                            const uint32_t* __restrict__ offsets,
+                                                            uint32_t* __restrict__ run_keys,
+                                                            uint32_t* __restrict__ run_start,
+                                                            uint32_t* __restrict__ unsorted) {
+  __shared__ uint32_t s_w[kBlock / 32];
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool head = i < n && (i == 0 || sk[i] != sk[i - 1]);
+  if (i < n && i > 0 && sk[i] < sk[i - 1]) atomicOr(unsorted, 1u);
+  const uint32_t hb = __ballot_sync(0xffffffffu, head);
+  if (lane == 0) s_w[warp] = __popc(hb);
+  __syncthreads();
+  uint32_t base = offsets[blockIdx.x];
+  for (int w = 0; w < warp; ++w) base += s_w[w];
+  if (head) {
+    const uint32_t r = base + __popc(hb & ((1u << lane) - 1u));
+    run_keys[r] = sk[i];
+    run_start[r] = i;
+  }
+}
+
+// One thread per (run, column): the left fold of the run's rows in index
+// order -- segmented_reduce_rows at workers == 1 (reduce.hpp:80-137), so the
+// sums are the reference's bit for bit at one worker.
+__global__ void __launch_bounds__(kBlock) run_fold_kernel(const double* __restrict__ values,
+                                                          size_t width, const uint32_t* __restrict__ run_start,
+                                                          const uint32_t* __restrict__ qp, uint32_t n,
+                                                          double* __restrict__ out) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t q = *qp;
+  if (t >= (size_t)q * width) return;
+  const size_t r = t / width, k = t - r * width;
+  const uint32_t b = __ldg(run_start + r), e = r + 1 < q ? __ldg(run_start + r + 1) : n;
+  double acc = __ldg(values + (size_t)b * width + k);
+  for (uint32_t i = b + 1; i < e; ++i) acc += __ldg(values + (size_t)i * width + k);
+  out[r * width + k] = acc;
+}
+
+}  // namespace
+
+void sort_keys_device(Context& ctx, uint32_t* d_keys, void* d_payload, size_t bytes, size_t n,
+                      PointScratch& s) {
+  if (n < 2) return;
+  cudaStream_t st = ctx.stream;
+  s.reserve_points(n, false);
+  const sort::DigitPlan plan = sort::plan_digits(32);
+  const int ntiles = (int)((n + sort::kTile - 1) / sort::kTile);
+  const size_t table = (size_t)ntiles * sort::kMaxRadix;
+  uint32_t* gcount = s.hist.p;
+  uint32_t* offs = s.hist.p + kOffOff;
+  auto cnt = [&](int p) { return s.hist.p + kOffOff + table * (size_t)(1 + p); };
+  IBC_CUDA(cudaMemsetAsync(gcount, 0, kOffOff * 4, st));
+  IBC_CUDA(cudaMemsetAsync(cnt(1), 0, table * (size_t)(plan.passes - 1) * 4, st));
+  static bool attr_set[64] = {};
+  if (!attr_set[ctx.device & 63]) {
+    IBC_CUDA(cudaFuncSetAttribute(sort::onesweep_pass<sort::kPayloadNone>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_smem()));
+    attr_set[ctx.device & 63] = true;
+  }
+  KeyDigits kd{};
+  kd.passes = plan.passes;
+  for (int p = 0; p < plan.passes; ++p) {
+    kd.shift[p] = plan.shift[p];
+    kd.bits[p] = plan.bits[p];
+  }
+  raw_hist_kernel<<<ntiles, kKeysThreads, 0, st>>>(d_keys, (uint32_t)n, gcount, cnt(0), kd);
+  ++ctx.launches;
+  // A 4-byte payload rides along as the sort's value; any other is gathered
+  // through the permutation afterwards.
+  const bool word = bytes == 4 && d_payload;
+  const uint32_t* first_vals = word ? static_cast<const uint32_t*>(d_payload) : nullptr;
+  const uint32_t* src_k = d_keys;
+  int dst = 0;
+  for (int p = 0; p < plan.passes; ++p) {
+    const bool last = p + 1 == plan.passes;
+    const int radix = 1 << plan.bits[p];
+    sort::tile_offsets_kernel<<<(radix + 31) / 32, sort::kThreads, 0, st>>>(
+        cnt(p), offs, gcount + (size_t)p * sort::kMaxRadix, radix, ntiles);
+    sort::onesweep_pass<sort::kPayloadNone><<<ntiles, sort::kThreads, sort_smem(), st>>>(
+        src_k, p == 0 ? first_vals : s.vals[dst ^ 1].p, s.keys[dst].p, s.vals[dst].p, (uint32_t)n,
+        plan.shift[p], plan.bits[p], offs, last ? nullptr : cnt(p + 1), last ? 0 : plan.shift[p + 1],
+        last ? 1 : plan.bits[p + 1], nullptr, nullptr, nullptr, DevGrid{}, nullptr);
+    ctx.launches += 2;
+    src_k = s.keys[dst].p;
+    dst ^= 1;
+  }
+  const int fin = dst ^ 1;  // buffers of the last pass
+  IBC_CUDA(cudaMemcpyAsync(d_keys, s.keys[fin].p, n * 4, cudaMemcpyDeviceToDevice, st));
+  if (word) {
+    IBC_CUDA(cudaMemcpyAsync(d_payload, s.vals[fin].p, n * 4, cudaMemcpyDeviceToDevice, st));
+  } else if (d_payload && bytes) {
+    s.prim_bytes.ensure(n * bytes);
+    gather_payload_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(
+        static_cast<const unsigned char*>(d_payload), s.prim_bytes.p, s.vals[fin].p, n, bytes);
+    ++ctx.launches;
+    IBC_CUDA(cudaMemcpyAsync(d_payload, s.prim_bytes.p, n * bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  IBC_CUDA(cudaGetLastError());
+  s.last_n = 0;  // the scratch no longer holds a spread's observables
+  s.obs_pending = false;
+}
+
+size_t runs_device(Context& ctx, const uint32_t* d_keys, size_t n, PointScratch& s,
+                   uint32_t* d_run_keys, const double* d_values, size_t width, double* d_out,
+                   bool* unsorted) {
+  if (unsorted) *unsorted = false;
+  if (n == 0) return 0;
+  cudaStream_t st = ctx.stream;
+  s.counters.ensure(kCounters + 2);
+  uint32_t* qp = s.counters.p + kMaxPasses;
+  uint32_t* flag = qp + 1;
+  const unsigned nb = grid_for(n, kBlock);
+  s.block_counts.ensure(nb);
+  s.prim_u32.ensure(2 * n);
+  uint32_t* rk = d_run_keys ? d_run_keys : s.prim_u32.p;
+  uint32_t* starts = s.prim_u32.p + n;
+  IBC_CUDA(cudaMemsetAsync(flag, 0, 4, st));
+  head_count_kernel<<<nb, kBlock, 0, st>>>(d_keys, (uint32_t)n, s.block_counts.p);
+  block_scan_kernel<<<1, sort::kThreads, 0, st>>>(s.block_counts.p, nb, qp);
+  head_start_kernel<<<nb, kBlock, 0, st>>>(d_keys, (uint32_t)n, s.block_counts.p, rk, starts, flag);
+  ctx.launches += 3;
+  if (d_values && d_out && width) {
+    // q <= n runs: launch for n * width threads, idle past q * width.
+    run_fold_kernel<<<grid_for(n * width, kBlock), kBlock, 0, st>>>(d_values, width, starts, qp,
+                                                                    (uint32_t)n, d_out);
+    ++ctx.launches;
+  }
+  IBC_CUDA(cudaGetLastError());
+  uint32_t h[2] = {0, 0};
+  IBC_CUDA(cudaMemcpyAsync(h, qp, 8, cudaMemcpyDeviceToHost, st));
+  IBC_CUDA(cudaStreamSynchronize(st));
+  if (unsorted) *unsorted = h[1] != 0;
+  return h[0];
+}
 
 }  // namespace ibc

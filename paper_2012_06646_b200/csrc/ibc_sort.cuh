@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kThreads) onesweep_pass(
             double u;
             const int c = cell_and_u(axis_of(g, a), g.h, g.inv_h, __ldg(x + a), &u);
             if (a == 0) cx = c;
-            sincos_half_pi(u, &tr[a][0], &tr[a][1]);
+            kernel_pair(g.kernel, u, &tr[a][0], &tr[a][1]);
           }
         }
         const double gq = __ldg(gvals + v) * (0.25 * g.inv_h);

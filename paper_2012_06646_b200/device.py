@@ -11,7 +11,7 @@ import ctypes as C
 
 from . import _capi
 from ._capi import InvalidArgument, check, load
-from .ib import Context, SpreadWorkspace, StaggeredGrid
+from .ib import Context, CosineKernel, SpreadWorkspace, StaggeredGrid, _kernel_code
 
 
 def _ptr(t) -> C.c_void_p:
@@ -48,7 +48,8 @@ class DeviceOperators:
             self._ws[key] = SpreadWorkspace(n, grid, 0, context=self.context)
         return self._ws[key]
 
-    def spread(self, points, values, grid: StaggeredGrid, out=None, workspace=None):
+    def spread(self, points, values, grid: StaggeredGrid, out=None, workspace=None,
+               kernel=CosineKernel):
         """points (n, D) float64 cuda, values (n,) -> out (prod(extent),) float64 cuda."""
         import torch
 
@@ -61,12 +62,12 @@ class DeviceOperators:
         ws = workspace if workspace is not None else self.workspace(n, grid)
         self._sync_stream()
         check(load().ibc_spread_device(self.context.handle, C.byref(grid.c_grid),
-                                       _capi.IBC_KERNEL_COSINE4, _ptr(points), _ptr(values), n,
+                                       _kernel_code(kernel), _ptr(points), _ptr(values), n,
                                        ws.handle, _ptr(out)))
         ws._mark(n)
         return out
 
-    def interpolate(self, field, points, grid: StaggeredGrid, out=None):
+    def interpolate(self, field, points, grid: StaggeredGrid, out=None, kernel=CosineKernel):
         """field (prod(extent),) + points (n, D) -> out (n,), all float64 cuda."""
         import torch
 
@@ -78,7 +79,7 @@ class DeviceOperators:
         _require(out, "out", n)
         self._sync_stream()
         check(load().ibc_interpolate_device(self.context.handle, C.byref(grid.c_grid),
-                                            _capi.IBC_KERNEL_COSINE4, _ptr(field), _ptr(points),
+                                            _kernel_code(kernel), _ptr(field), _ptr(points),
                                             n, _ptr(out)))
         return out
 

@@ -35,7 +35,8 @@ from . import _capi
 from ._capi import InvalidArgument, LengthError, check, load  # noqa: F401
 
 __all__ = [
-    "StaggeredGrid", "GridField", "CosineKernel", "SpreadAlgorithm", "SpreadWorkspace",
+    "StaggeredGrid", "GridField", "CosineKernel", "Peskin4Kernel", "Roma3Kernel", "Linear2Kernel",
+    "KERNELS", "SpreadAlgorithm", "SpreadWorkspace",
     "interpolate", "interpolate_vector", "spread_serial", "spread_fused", "spread_buffered",
     "spread_buffered_otf", "spread_vector", "stats", "Context", "default_context",
     "InvalidArgument", "LengthError",
@@ -189,6 +190,79 @@ class CosineKernel:
         return 2.0
 
 
+class Peskin4Kernel:
+    """Peskin's standard 4-point kernel (Peskin 2002, Eq. 6.27), support 4:
+    (3 - 2|r| + sqrt(1 + 4|r| - 4r^2)) / 8 on |r| <= 1,
+    (5 - 2|r| - sqrt(-7 + 12|r| - 4r^2)) / 8 on 1 < |r| < 2."""
+
+    code = _capi.IBC_KERNEL_PESKIN4
+
+    @staticmethod
+    def phi(r: float) -> float:
+        a = abs(r)
+        if not a < 2.0:
+            return 0.0
+        if a <= 1.0:
+            return (3.0 - 2.0 * a + math.sqrt(1.0 + 4.0 * a - 4.0 * a * a)) * 0.125
+        return (5.0 - 2.0 * a - math.sqrt(max(0.0, -7.0 + 12.0 * a - 4.0 * a * a))) * 0.125
+
+    @staticmethod
+    def support() -> int:
+        return 4
+
+    @staticmethod
+    def radius() -> float:
+        return 2.0
+
+
+class Roma3Kernel:
+    """The 3-point kernel of Roma, Peskin & Berger (1999), odd support 3
+    (cell_index associates the nearest grid point, grid.hpp:121-130):
+    (1 + sqrt(1 - 3r^2)) / 3 on |r| <= 1/2,
+    (5 - 3|r| - sqrt(1 - 3(1 - |r|)^2)) / 6 on 1/2 < |r| < 3/2."""
+
+    code = _capi.IBC_KERNEL_ROMA3
+
+    @staticmethod
+    def phi(r: float) -> float:
+        a = abs(r)
+        if not a < 1.5:
+            return 0.0
+        if a <= 0.5:
+            return (1.0 + math.sqrt(1.0 - 3.0 * a * a)) / 3.0
+        return (5.0 - 3.0 * a - math.sqrt(1.0 - 3.0 * (1.0 - a) * (1.0 - a))) / 6.0
+
+    @staticmethod
+    def support() -> int:
+        return 3
+
+    @staticmethod
+    def radius() -> float:
+        return 1.5
+
+
+class Linear2Kernel:
+    """The 2-point hat kernel, 1 - |r| on |r| < 1, support 2."""
+
+    code = _capi.IBC_KERNEL_LINEAR2
+
+    @staticmethod
+    def phi(r: float) -> float:
+        a = abs(r)
+        return 1.0 - a if a < 1.0 else 0.0
+
+    @staticmethod
+    def support() -> int:
+        return 2
+
+    @staticmethod
+    def radius() -> float:
+        return 1.0
+
+
+KERNELS = (CosineKernel, Peskin4Kernel, Roma3Kernel, Linear2Kernel)
+
+
 class SpreadAlgorithm(enum.IntEnum):
     serial = _capi.IBC_SPREAD_SERIAL
     fused = _capi.IBC_SPREAD_FUSED
@@ -197,10 +271,14 @@ class SpreadAlgorithm(enum.IntEnum):
 
 
 def _kernel_code(kernel) -> int:
-    code = getattr(kernel, "code", None)
-    if code is None:
-        raise InvalidArgument("unsupported kernel support size")
-    return int(code)
+    """Device kernel id of one of KERNELS (class or instance).  Any other
+    Kernel type is rejected: the device evaluates phi itself, so a caller's
+    own phi cannot silently be replaced by another kernel's."""
+    cls = kernel if isinstance(kernel, type) else type(kernel)
+    if cls not in KERNELS:
+        raise InvalidArgument(f"unsupported kernel type {cls.__name__}: the device takes "
+                              + ", ".join(k.__name__ for k in KERNELS))
+    return int(cls.code)
 
 
 def _points(points, dim: int) -> np.ndarray:

@@ -172,3 +172,44 @@ def test_oracle_invariants():
         interp = O.interpolate(g, e, pts)
         point_side = float(w @ interp)
         assert abs(grid_side - point_side) <= 1e-12 * float(np.abs(w * interp).sum())
+
+
+# ------------------------------------------------------------------ other kernels
+def test_kernel_kats():
+    # Peskin 4-point: phi(0) = 1/2, phi(1) = 1/4, phi(2) = 0 (as kernel_test.cpp:16-22
+    # pins the cosine kernel); Roma 3-point: phi(0) = 2/3, phi(1) = 1/6, phi(3/2) = 0;
+    # hat: phi(0) = 1, phi(1/2) = 1/2, phi(1) = 0.
+    for k, r, want in [(0, 0.0, 0.5), (0, 1.0, 0.25), (0, 2.0, 0.0), (1, 0.0, 0.5), (1, 1.0, 0.25),
+                       (1, -1.0, 0.25), (1, 2.0, 0.0), (2, 0.0, 2 / 3), (2, 1.0, 1 / 6),
+                       (2, 1.5, 0.0), (3, 0.0, 1.0), (3, 0.5, 0.5), (3, 1.0, 0.0)]:
+        assert O.kernel_phi(k, r) == pytest.approx(want, abs=1e-15), (k, r)
+    assert [O.lib().or_kernel_support(k) for k in range(5)] == [4, 4, 3, 2, 0]
+    # zeroth moment and the even/odd split every 4-point kernel satisfies
+    rng = np.random.default_rng(3)
+    for k in range(4):
+        s = O.lib().or_kernel_support(k)
+        for u in rng.uniform(0.0, 1.0, 50):
+            w = [O.kernel_phi(k, j + u) for j in range(-s, s + 1)]
+            assert sum(w) == pytest.approx(1.0, abs=1e-14)
+        if s == 4:
+            for u in rng.uniform(0.0, 1.0, 50):
+                w = [O.kernel_phi(k, -2 + u + j) for j in range(4)]
+                assert w[0] + w[2] == pytest.approx(0.5, abs=1e-15)
+                assert w[1] + w[3] == pytest.approx(0.5, abs=1e-15)
+
+
+def test_oracle_matches_reference_golden_for_every_kernel():
+    z = np.load(GOLD / "golden_kernels.npz")
+    for c in range(int(z["ncases"][0])):
+        p = f"c{c}_"
+        k = int(z[p + "kernel"][0])
+        g = O.make_grid(list(z[p + "ext"]), float(z[p + "h"][0]), list(z[p + "alpha"]),
+                        list(z[p + "per"]), list(z[p + "origin"]))
+        pts, vals = z[p + "pts"], z[p + "vals"]
+        field, keys, perm, run_keys = O.spread_fused(g, pts, vals, kernel=k)
+        assert np.array_equal(keys, z[p + "keys"]), c
+        assert np.array_equal(perm, z[p + "perm"]), c
+        assert np.array_equal(run_keys, z[p + "run_keys"]), c
+        assert O.max_rel_deviation(field, z[p + "spread"]) <= 1e-12, c
+        assert O.max_rel_deviation(O.spread_serial(g, pts, vals, kernel=k), z[p + "serial"]) <= 1e-12, c
+        assert O.max_rel_deviation(O.interpolate(g, z[p + "field"], pts, kernel=k), z[p + "interp"]) <= 1e-12, c
