@@ -52,20 +52,48 @@ def build_oracle() -> None:
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
 
 
+def _cxx() -> str:
+    return "/usr/bin/g++" if Path("/usr/bin/g++").exists() else (shutil.which("g++") or "g++")
+
+
+REF_INCLUDE = Path(os.environ.get("IB_REF_INCLUDE", "/root/reference/proj/include"))
+OVERLAY = sorted((ROOT / "include" / "ib_b200").rglob("*.hpp"))
+
+
 def build_cpp_tests() -> Path | None:
-    """C++ drop-in shim test (include/ib_b200/ib.hpp), linked against libibcuda.so."""
+    """C++ drop-in tests, linked against libibcuda.so:
+    * tests/cpp/build/shim_test -- the reference's call pattern through
+      include/ib_b200/ib.hpp, checked against the C oracle;
+    * tests/cpp/build/overlay_test -- the reference's own ib/bench/run.hpp and
+      ib/bench/verify.hpp compiled unmodified with include/ib_b200 ahead of the
+      reference's include directory (built only where /root/reference is
+      present; the binary travels to the GPU box)."""
     src = ROOT / "tests" / "cpp" / "shim_test.cpp"
     if not src.exists():
         return None
     out = ROOT / "tests" / "cpp" / "build" / "shim_test"
-    deps = [src, ROOT / "include" / "ib_b200" / "ib.hpp", ROOT / "include" / "ibcuda.h", LIB,
-            ROOT / "oracle" / "ib_oracle.h"]
-    if not _stale(out, deps):
-        return out
+    deps = [src, ROOT / "include" / "ibcuda.h", LIB, ROOT / "oracle" / "ib_oracle.h", *OVERLAY]
     out.parent.mkdir(parents=True, exist_ok=True)
-    cxx = "/usr/bin/g++" if Path("/usr/bin/g++").exists() else (shutil.which("g++") or "g++")
-    cmd = [cxx, "-O2", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{ROOT / 'oracle'}", str(src),
-           "-o", str(out), f"-L{LIB.parent}", "-libcuda", f"-Wl,-rpath,{LIB.parent}",
-           f"-L{ROOT / 'oracle'}", "-loracle", f"-Wl,-rpath,{ROOT / 'oracle'}"]
-    subprocess.run(cmd, check=True)
+    if _stale(out, deps):
+        cmd = [_cxx(), "-O2", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{ROOT / 'oracle'}", str(src),
+               "-o", str(out), f"-L{LIB.parent}", "-libcuda", f"-Wl,-rpath,{LIB.parent}",
+               f"-L{ROOT / 'oracle'}", "-loracle", f"-Wl,-rpath,{ROOT / 'oracle'}"]
+        subprocess.run(cmd, check=True)
+    build_overlay_test()
+    return out
+
+
+def build_overlay_test() -> Path | None:
+    src = ROOT / "tests" / "cpp" / "overlay_test.cpp"
+    out = ROOT / "tests" / "cpp" / "build" / "overlay_test"
+    if not (REF_INCLUDE / "ib" / "bench" / "run.hpp").exists():
+        return out if out.exists() else None  # prebuilt (GPU box) or absent
+    deps = [src, ROOT / "include" / "ibcuda.h", LIB, *OVERLAY]
+    if _stale(out, deps):
+        out.parent.mkdir(parents=True, exist_ok=True)
+        cmd = [_cxx(), "-O2", "-std=c++20", "-DIB_OVERLAY_DEVICE",
+               f"-I{ROOT / 'include' / 'ib_b200'}", f"-I{ROOT / 'include'}", f"-I{REF_INCLUDE}",
+               str(src), "-o", str(out), f"-L{LIB.parent}", "-libcuda",
+               f"-Wl,-rpath,{LIB.parent}"]
+        subprocess.run(cmd, check=True)
     return out
