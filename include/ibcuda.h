@@ -184,6 +184,24 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
                                   const double* d_field, const double* d_points, size_t n,
                                   double* d_out);
 
+/* Binned points: the field-independent half of an interpolation (cell keys,
+ * row bucket sort, per-point weight records), kept so several fields can be
+ * interpolated at the same points -- the reference's step interpolates the
+ * same velocity at X^n twice (bench/run.hpp:94-115) and a vector field is 3
+ * fields.  ibc_interpolate_binned_device(ctx, b, f, out) equals
+ * ibc_interpolate_device(ctx, grid, kernel, f, points, n, out) bit for bit.
+ * The binning refers to d_points (the generic path re-reads them): they must
+ * stay allocated and unchanged until it is rebinned or destroyed.  Both calls
+ * are asynchronous on the context stream; a binning is not shared between
+ * concurrent calls. */
+typedef struct ibc_binned ibc_binned;
+ibc_status ibc_binned_create(ibc_context* ctx, ibc_binned** out);
+ibc_status ibc_binned_destroy(ibc_binned* b);
+ibc_status ibc_bin_points_device(ibc_context* ctx, ibc_binned* b, const ibc_grid* grid,
+                                 ibc_kernel kernel, const double* d_points, size_t n);
+ibc_status ibc_interpolate_binned_device(ibc_context* ctx, const ibc_binned* b,
+                                         const double* d_field, double* d_out);
+
 /* Multi-GPU z-slab decomposition (no reference analog: the
  * paper defers multi-device runs).  A rank owns home planes
  * [z0, z1) of the last axis of a global grid and works on a LOCAL grid of
@@ -247,6 +265,10 @@ ibc_status ibc_collect_unique_keys(ibc_context* ctx, const uint32_t* sorted_keys
 /* ib::stats (stats.hpp:9-25): every operation adds n_points * support^dim. */
 uint64_t ibc_delta_evaluations(void);
 void ibc_reset_delta_evaluations(void);
+/* ib::bench::fnv1a (bench/run.hpp:44-52): 64-bit FNV-1a of `bytes` bytes
+ * continuing from `hash` (14695981039346656037 to start) -- the step loop's
+ * physics fingerprint (run.hpp:120-126), host memory. */
+uint64_t ibc_fnv1a(const void* data, size_t bytes, uint64_t hash);
 /* ib::stats::add_delta_evaluations (stats.hpp:23-25). */
 void ibc_add_delta_evaluations(uint64_t n);
 

@@ -107,6 +107,11 @@ SIGNATURES = {
     "ibc_count_unique": (_st, [_vp, _vp, _sz, C.c_int, C.POINTER(_sz)]),
     "ibc_collect_unique_keys": (_st, [_vp, _vp, _sz, _vp, _sz, C.POINTER(_sz)]),
     "ibc_add_delta_evaluations": (None, [C.c_uint64]),
+    "ibc_fnv1a": (C.c_uint64, [_vp, _sz, C.c_uint64]),
+    "ibc_binned_create": (_st, [_vp, C.POINTER(_vp)]),
+    "ibc_binned_destroy": (_st, [_vp]),
+    "ibc_bin_points_device": (_st, [_vp, _vp, _G, C.c_int, _vp, _sz]),
+    "ibc_interpolate_binned_device": (_st, [_vp, _vp, _vp, _vp]),
     "ibc_delta_evaluations": (C.c_uint64, []),
     "ibc_reset_delta_evaluations": (None, []),
 }

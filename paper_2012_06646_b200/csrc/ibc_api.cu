@@ -26,6 +26,16 @@ struct ibc_context {
 struct ibc_workspace {
   ibc::Workspace w;
 };
+struct ibc_binned {
+  ibc::PointScratch s;
+  ibc::DevGrid g{};
+  ibc::InterpPlan P;
+  const double* d_points = nullptr;
+  size_t n = 0;
+  size_t grid_points = 0;
+  int device = 0;
+  bool ready = false;
+};
 
 namespace {
 
@@ -47,6 +57,9 @@ ibc_status guarded(F&& f) {
   } catch (const ApiError& e) {
     g_last_error = e.msg;
     return e.status;
+  } catch (const ibc::ArgError& e) {
+    g_last_error = e.msg;
+    return IBC_ERR_INVALID_ARGUMENT;
   } catch (const ibc::CudaError& e) {
     g_last_error = e.where + ": " + cudaGetErrorString(e.code);
     return e.code == cudaErrorMemoryAllocation ? IBC_ERR_ALLOC : IBC_ERR_CUDA;
@@ -553,6 +566,62 @@ ibc_status ibc_home_planes_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
 
 int ibc_kernel_support(ibc_kernel kernel) { return ibc::kernel_support((int)kernel); }
 
+// ---------------------------------------------------------------- Binned points
+ibc_status ibc_binned_create(ibc_context* ctx, ibc_binned** out) {
+  return guarded([&] {
+    if (!ctx || !out) invalid("null argument");
+    auto* b = new ibc_binned();
+    b->device = ctx->c.device;
+    *out = b;
+  });
+}
+
+ibc_status ibc_binned_destroy(ibc_binned* b) {
+  return guarded([&] {
+    if (!b) return;
+    cudaSetDevice(b->device);
+    b->s.release_all();
+    delete b;
+  });
+}
+
+ibc_status ibc_bin_points_device(ibc_context* ctx, ibc_binned* b, const ibc_grid* grid,
+                                 ibc_kernel kernel, const double* d_points, size_t n) {
+  return guarded([&] {
+    if (!ctx || !b) invalid("null argument");
+    check_grid(grid);
+    check_kernel(kernel);
+    check_points(n);
+    if (n && !d_points) invalid("null point buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    b->ready = false;
+    b->g = ibc::make_devgrid(*grid, (int)kernel);
+    b->s.reserve_points(n, false);
+    b->s.reserve_rows(b->g.nrows);
+    b->P = ibc::interp_bin(c, b->g, d_points, n, b->s, true);
+    b->d_points = d_points;
+    b->n = n;
+    b->grid_points = grid_points(grid);
+    b->ready = true;
+  });
+}
+
+ibc_status ibc_interpolate_binned_device(ibc_context* ctx, const ibc_binned* b,
+                                         const double* d_field, double* d_out) {
+  return guarded([&] {
+    if (!ctx || !b) invalid("null argument");
+    if (!b->ready) invalid("points have not been binned");
+    if (b->n && (!d_field || !d_out)) invalid("null buffer");
+    auto& c = ctx->c;
+    use_device(c);
+    ibc::interp_gather(c, b->g, b->P, d_field, b->d_points, b->n,
+                       const_cast<ibc::PointScratch&>(b->s), d_out);
+    g_delta_evaluations.fetch_add(b->n * (uint64_t)std::pow(b->g.support, b->g.dim),
+                                  std::memory_order_relaxed);
+  });
+}
+
 // ---------------------------------------------------------------- Primitives
 ibc_status ibc_key_value_sort_device(ibc_context* ctx, uint32_t* d_keys, void* d_payload,
                                      size_t payload_bytes, size_t n) {
@@ -651,6 +720,15 @@ ibc_status ibc_collect_unique_keys(ibc_context* ctx, const uint32_t* sorted_keys
   return guarded([&] {
     reduce_host(ctx, sorted_keys, nullptr, n, 0, out_keys, out_cap, nullptr, 0, q);
   });
+}
+
+uint64_t ibc_fnv1a(const void* data, size_t bytes, uint64_t hash) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  for (size_t i = 0; i < bytes; ++i) {
+    hash ^= p[i];
+    hash *= 1099511628211ull;
+  }
+  return hash;
 }
 
 void ibc_add_delta_evaluations(uint64_t n) {

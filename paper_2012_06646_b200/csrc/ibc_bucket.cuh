@@ -249,17 +249,20 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
 // K3, interpolation: each point's 64-byte record at row start + rank --
 // {sin/cos(pi u_a / 2) for a = x, y, z; input index, home cx, home cy} -- so
 // the gather does no cell or trig math.
+// Points homed outside the grid (extra row g.nrows) get a record holding only
+// their index: the gather zeroes their outputs (no support point reaches them).
 template <int D>
 __global__ void __launch_bounds__(kThreads) scatter_interp_kernel(
     DevGrid g, const double* __restrict__ X, const uint32_t* __restrict__ rows,
     const uint32_t* __restrict__ rank, uint32_t n, const uint32_t* __restrict__ start,
-    double* __restrict__ rec, double* __restrict__ out) {
+    double* __restrict__ rec) {
   pdl_wait();
   const uint32_t i = blockIdx.x * kThreads + threadIdx.x;
   if (i >= n) return;
   const uint32_t rk = __ldg(rank + i);
-  if (rk & kOutside) {  // homed outside the grid: no gather reaches it
-    out[i] = 0.0;
+  if (rk & kOutside) {
+    rec[8 * (size_t)(__ldg(start + g.nrows) + (rk & ~kOutside)) + 6] =
+        __longlong_as_double((long long)i);
     return;
   }
   const uint32_t slot = __ldg(start + __ldg(rows + i)) + rk;

@@ -294,6 +294,21 @@ __device__ __forceinline__ void kernel_pair(int k, double u, double* sn, double*
   sincos_half_pi(u, sn, cs);
 }
 
+namespace sw {
+// Tiling of the TMA interpolation gather (ibc_sweep.cuh, chosen on the host).
+struct InterpTiling {
+  int ty, zc, nty, nzc;
+  int frmax;             // field rows per slot (ty + 3, + ghost rows on closed y)
+  int slots;             // ring depth (>= 5)
+  uint32_t pitch;        // bytes per field row in shared memory (multiple of 1024)
+  uint32_t slot_bytes;   // frmax * pitch
+  int rec_cap;           // point records staged per step (32 B each)
+  int hmax;              // max home planes per CTA (row-range table entries)
+  uint32_t slot_stride;  // slot_bytes + rec_cap * 64, rounded up to 1024
+  int box_ok;            // one TMA per plane allowed (nx % 128 == 0)
+};
+}  // namespace sw
+
 // Programmatic dependent launch: the pipeline's kernels are launched with
 // programmatic stream serialization (their launch and block scheduling
 // overlap the predecessor's tail) and wait here, before touching memory,

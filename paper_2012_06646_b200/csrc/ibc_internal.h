@@ -16,6 +16,11 @@ struct CudaError {
   std::string where;
 };
 
+// A device-side precondition the caller violated (-> IBC_ERR_INVALID_ARGUMENT).
+struct ArgError {
+  std::string msg;
+};
+
 inline void check_cuda(cudaError_t e, const char* where) {
   if (e != cudaSuccess) throw CudaError{e, where};
 }
@@ -115,6 +120,15 @@ inline int kernel_support(int k) {
 void home_planes(Context& ctx, const DevGrid& g, const double* d_points, size_t n, int* d_planes);
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points,
                      const double* d_values, size_t n, PointScratch& s, double* d_out);
+// Interpolation split into a field-independent binning and the gather.
+struct InterpPlan {
+  bool tma = false;
+  sw::InterpTiling T{};
+};
+InterpPlan interp_bin(Context& ctx, const DevGrid& g, const double* d_points, size_t n,
+                      PointScratch& s, bool allow_tma);
+void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const double* d_field,
+                   const double* d_points, size_t n, PointScratch& s, double* d_out);
 void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field,
                      const double* d_points, size_t n, PointScratch& s, double* d_out);
 // ws.run_keys on the device; returns q (synchronizes).

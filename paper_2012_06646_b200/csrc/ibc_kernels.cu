@@ -656,7 +656,7 @@ void PointScratch::release_all() {
 
 namespace {
 void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
-                   size_t n, PointScratch& s, bool spread, double* d_out = nullptr);
+                   size_t n, PointScratch& s, bool spread);
 
 // Tiling of the write-once spread sweep (ibc_spread.cuh), 2-D and 3-D grids.
 // rows_per_warp = 1: pull mode (wpc warps per CTA, one target row each);
@@ -943,7 +943,7 @@ void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
 // rows' key order.  The stable (key, index) order the reference exposes as
 // ws.keys / ws.perm is materialised on request (ensure_observables).
 void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
-                   size_t n, PointScratch& s, bool spread, double* d_out) {
+                   size_t n, PointScratch& s, bool spread) {
   cudaStream_t st = ctx.stream;
   const uint32_t nrows = g.nrows + 1;  // + the row of points homed outside (K1)
   const int group = spread ? bucket::kBanks : 1;     // buckets per grid row
@@ -997,10 +997,10 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   if (!spread) {
     if (g.dim == 3)
       pdl_launch(bucket::scatter_interp_kernel<3>, blocks, bucket::kThreads, 0, st, 
-          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p, d_out);
+          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     else
       pdl_launch(bucket::scatter_interp_kernel<2>, blocks, bucket::kThreads, 0, st, 
-          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p, d_out);
+          g, d_points, s.keys[0].p, s.vals[0].p, (uint32_t)n, s.rowstart.p, s.rec.p);
     ctx.launches += 1;
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
@@ -1021,53 +1021,67 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   IBC_CUDA(cudaGetLastError());
 }
 
-bool interp_tma_path(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
-                     size_t n, PointScratch& s, double* d_out) {
-  sw::InterpTiling T;
-  if (!interp_tma_tiling(g, n, ctx.sms, T)) return false;
-  CUtensorMap map;
-  if (!tma::encode_rows_map(&map, d_field, g.n[0], g.n[1], g.n[2])) return false;
-  CUtensorMap map_box;
-  if (!tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax)) return false;
+}  // namespace
+
+// Interpolation binning -- everything that depends on the points and the
+// grid but not on the field, so one binning serves any number of fields at
+// the same points (the reference's step interpolates twice at X^n,
+// run.hpp:94-115): TMA path -- row bucket sort + 64-byte records (points
+// homed outside the grid get their index in the extra row, zeroed by the
+// gather); generic path -- the stable radix sort (permutation).
+InterpPlan interp_bin(Context& ctx, const DevGrid& g, const double* d_points, size_t n,
+                      PointScratch& s, bool allow_tma) {
+  InterpPlan P;
+  if (n == 0) return P;
+  P.tma = allow_tma && g.support == kSupport && interp_tma_tiling(g, n, ctx.sms, P.T);
+  if (P.tma) bucket_points(ctx, g, d_points, nullptr, n, s, false);
+  else sort_points(ctx, g, d_points, n, s, false, sort::kPayloadNone);
+  return P;
+}
+
+// The gather over a binning (d_points is read again on the generic path).
+void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const double* d_field,
+                   const double* d_points, size_t n, PointScratch& s, double* d_out) {
+  if (n == 0) return;
   cudaStream_t st = ctx.stream;
-  bucket_points(ctx, g, d_points, nullptr, n, s, false, d_out);
-  const size_t smem = interp_tma_smem(T);
-  static bool attr_set[64] = {};
-  if (!attr_set[ctx.device & 63]) {
-    IBC_CUDA(cudaFuncSetAttribute(sw::interp_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  227 * 1024));
-    attr_set[ctx.device & 63] = true;
-  }
   cudaEvent_t ev = nullptr;
-  ctx.prof_begin(kProfInterp, &ev);
-  pdl_launch(sw::interp_tma_kernel, (unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st, 
-      g, T, map, map_box, s.rowstart.p, s.rec.p, d_out);
+  if (P.tma) {
+    const sw::InterpTiling& T = P.T;
+    CUtensorMap map, map_box;
+    if (!tma::encode_rows_map(&map, d_field, g.n[0], g.n[1], g.n[2]) ||
+        !tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax))
+      throw ArgError{"field must be 16-byte aligned device memory"};
+    const size_t smem = interp_tma_smem(T);
+    static bool attr_set[64] = {};
+    if (!attr_set[ctx.device & 63]) {
+      IBC_CUDA(cudaFuncSetAttribute(sw::interp_tma_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr_set[ctx.device & 63] = true;
+    }
+    ctx.prof_begin(kProfInterp, &ev);
+    pdl_launch(sw::interp_tma_kernel, (unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st, g, T, map,
+               map_box, s.rowstart.p, s.rec.p, d_out);
+  } else {
+    // Generic gather (1-D/2-D grids, x extents the TMA rows do not take,
+    // other supports): one thread per point in sorted order.
+    ctx.prof_begin(kProfInterp, &ev);
+    interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
+                                                          (uint32_t)n, d_out);
+  }
   ++ctx.launches;
   ctx.prof_end(kProfInterp, ev);
   IBC_CUDA(cudaGetLastError());
   ++ctx.interp_calls;
-  return true;
 }
-}  // namespace
 
 void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
                      size_t n, PointScratch& s, double* d_out) {
   if (n == 0) return;
-  if (g.support == kSupport && interp_tma_path(ctx, g, d_field, d_points, n, s, d_out)) return;
-  // Generic gather (1-D/2-D grids, x extents the TMA rows do not take): one
-  // thread per point in sorted order.
-  cudaStream_t st = ctx.stream;
-  sort_points(ctx, g, d_points, n, s, false, sort::kPayloadNone);
-  cudaEvent_t ev = nullptr;
-  ctx.prof_begin(kProfInterp, &ev);
-  interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
-                                                        (uint32_t)n, d_out);
-  ++ctx.launches;
-  ctx.prof_end(kProfInterp, ev);
-  IBC_CUDA(cudaGetLastError());
-  ++ctx.interp_calls;
+  // The TMA tensor maps need a 16-byte aligned field.
+  const bool aligned = reinterpret_cast<uintptr_t>(d_field) % 16 == 0;
+  const InterpPlan P = interp_bin(ctx, g, d_points, n, s, aligned);
+  interp_gather(ctx, g, P, d_field, d_points, n, s, d_out);
 }
-
 
 // ws.run_keys and ws.run_count (= q) on the device, computed on demand from
 // the sorted keys (reduce.hpp:36-69); cached until the next sort.

@@ -37,17 +37,6 @@ constexpr int kIConsumers = 16;                    // consumer warps
 constexpr int kIThreads = 32 * (kIConsumers + 1);  // + 1 producer warp
 constexpr int kMaxSlots = 16;
 
-struct InterpTiling {
-  int ty, zc, nty, nzc;
-  int frmax;             // field rows per slot (ty + 3, + ghost rows on closed y)
-  int slots;             // ring depth (>= 5)
-  uint32_t pitch;        // bytes per field row in shared memory (multiple of 1024)
-  uint32_t slot_bytes;   // frmax * pitch
-  int rec_cap;           // point records staged per step (32 B each)
-  int hmax;              // max home planes per CTA (row-range table entries)
-  uint32_t slot_stride;  // slot_bytes + rec_cap * 64, rounded up to 1024
-  int box_ok;            // one TMA per plane allowed (nx % 128 == 0)
-};
 
 __device__ __forceinline__ uint32_t row_id(const DevGrid& g, int cyw, int czw) {
   return (uint32_t)(cyw + 1) + (uint32_t)(czw + 1) * (uint32_t)(g.n[1] + 2);
@@ -114,6 +103,14 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
     }
   }
   __syncthreads();
+
+  // Points homed outside the grid (the extra bucket row, normally empty):
+  // their interpolated value is 0 -- every support offset is invalid.
+  {
+    const uint32_t o0 = __ldg(rowstart + g.nrows), o1 = __ldg(rowstart + g.nrows + 1);
+    for (uint32_t r = o0 + blockIdx.x * kIThreads + tid; r < o1; r += gridDim.x * kIThreads)
+      out[(uint32_t)__double_as_longlong(rec[8 * (size_t)r + 6])] = 0.0;
+  }
 
   if (warp == kIConsumers) {
     // ------------------------------------------------------------ producer

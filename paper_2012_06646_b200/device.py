@@ -29,6 +29,28 @@ def _require(t, name, numel=None):
         raise InvalidArgument(f"{name} has {t.numel()} elements, expected {numel}")
 
 
+class BinnedPoints:
+    """ibc_binned: points bucketed for interpolation on one grid."""
+
+    def __init__(self, context: Context):
+        h = C.c_void_p()
+        check(load().ibc_binned_create(context.handle, C.byref(h)))
+        self.handle = h
+        self.n = 0
+        self.grid = None
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            load().ibc_binned_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class DeviceOperators:
     """Spread / interpolate on one GPU with a persistent context + workspace."""
 
@@ -81,6 +103,33 @@ class DeviceOperators:
         check(load().ibc_interpolate_device(self.context.handle, C.byref(grid.c_grid),
                                             _kernel_code(kernel), _ptr(field), _ptr(points),
                                             n, _ptr(out)))
+        return out
+
+    def bin_points(self, points, grid: StaggeredGrid, kernel=CosineKernel, binned=None):
+        """Bin device points for interpolation on `grid` (ibc_bin_points_device):
+        the field-independent half of `interpolate`, reusable for any number
+        of fields at the same points.  `points` must stay unchanged."""
+        n = points.shape[0] if points.dim() == 2 else points.numel() // grid.dim
+        _require(points, "points", n * grid.dim)
+        b = binned if binned is not None else BinnedPoints(self.context)
+        self._sync_stream()
+        check(load().ibc_bin_points_device(self.context.handle, b.handle, C.byref(grid.c_grid),
+                                           _kernel_code(kernel), _ptr(points), n))
+        b.n, b.grid = n, grid
+        b._points = points  # keep the binned tensor alive
+        return b
+
+    def interpolate_binned(self, field, binned, out=None):
+        """Interpolate `field` at binned points (ibc_interpolate_binned_device)."""
+        import torch
+
+        _require(field, "field", binned.grid.point_count())
+        if out is None:
+            out = torch.empty(binned.n, dtype=torch.float64, device=field.device)
+        _require(out, "out", binned.n)
+        self._sync_stream()
+        check(load().ibc_interpolate_binned_device(self.context.handle, binned.handle,
+                                                   _ptr(field), _ptr(out)))
         return out
 
     @property

@@ -19,12 +19,20 @@ the per-point updates (b), (c), (f) are a few elementwise torch ops on (n, 3)
 tensors (plumbing around the operators, as the reference's loops are around
 its calls).
 
+Steps (a) and (e) interpolate the same field at the same points, so each
+component's points are binned once per step (`DeviceOperators.bin_points`,
+ibc_bin_points_device) and both gathers reuse the binning.  `run_benchmark`
+times each vector operation on the device and returns the reference's
+`TimingReport` fields; `write_csv` writes the reference's CSV schema
+(`report.hpp:16-18, 50-66`) and `fnv1a` the physics fingerprint
+(`run.hpp:44-52, 120-126`).
+
 This is SURVEY.md 8(f) item 2 and the "MAC vector step" secondary figure of
 8(d); the headline metric stays the scalar spread + interpolation pair.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 from .ib import StaggeredGrid
 
@@ -40,6 +48,10 @@ class StepConfig:
     shear_rate: float = 1000.0       # 1/s
     spring_constant: float = 0.01    # dyn/cm
     seed: int = 1
+    steps: int = 100
+    workers: int = 1                  # accepted for the CSV; the device picks its own
+    sweep_width: int = 8
+    algorithm: str = "fused"
 
     @property
     def edge_cm(self) -> float:
@@ -123,6 +135,8 @@ class MacStepLoop:
         self.Xs = torch.empty((n, 3), **f64)         # X*
         self.F = torch.empty((3, n), **f64)          # tether forces
         self.ell = [torch.empty(g.point_count(), **f64) for g in self.grids]
+        # One binning of X^n per component, shared by steps (a) and (e).
+        self.binned = [None, None, None]
 
     def _components(self, fn):
         """fn(a) for the three components, concurrently when configured."""
@@ -140,21 +154,119 @@ class MacStepLoop:
         for a in range(3):
             main.wait_stream(self.streams[a])
 
-    def _interpolate_vector(self):
-        self._components(lambda a: self.comp_ops[a].interpolate(
-            self.velocity[a], self.X, self.grids[a], out=self.U[a]))
+    def _bin_and_interpolate(self, a):
+        ops = self.comp_ops[a]
+        self.binned[a] = ops.bin_points(self.X, self.grids[a], binned=self.binned[a])
+        ops.interpolate_binned(self.velocity[a], self.binned[a], out=self.U[a])
 
-    def step(self):
-        c = self.cfg
-        self._interpolate_vector()                                        # (a)
-        torch = __import__("torch")
-        torch.add(self.X, self.U.t(), alpha=c.dt_s, out=self.Xs)          # (b)
-        hookean_force(self.Xs, self.anchors, c.spring_constant, c.edge_cm, out=self.F)  # (c)
-        self._components(lambda a: self.comp_ops[a].spread(               # (d)
+    def _interpolate_vector(self, rebin: bool):
+        if rebin:
+            self._components(self._bin_and_interpolate)
+        else:
+            self._components(lambda a: self.comp_ops[a].interpolate_binned(
+                self.velocity[a], self.binned[a], out=self.U[a]))
+
+    def _spread_vector(self):
+        self._components(lambda a: self.comp_ops[a].spread(
             self.Xs, self.F[a], self.grids[a], out=self.ell[a]))
-        self._interpolate_vector()                                        # (e)
-        self.X.add_(self.U.t(), alpha=c.dt_s)                             # (f)
+
+    def step(self, events=None):
+        """One reference step; `events` (optional) receives CUDA event pairs
+        around (a), (d), (e) on the caller's stream."""
+        import torch
+
+        c = self.cfg
+
+        def timed(key, fn):
+            if events is None:
+                fn()
+                return
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            events.setdefault(key, []).append((e0, e1))
+
+        timed("interpolate", lambda: self._interpolate_vector(rebin=True))      # (a)
+        torch.add(self.X, self.U.t(), alpha=c.dt_s, out=self.Xs)                # (b)
+        hookean_force(self.Xs, self.anchors, c.spring_constant, c.edge_cm, out=self.F)  # (c)
+        timed("spread", self._spread_vector)                                    # (d)
+        # X^n is unchanged since (a): its binning is reused.
+        timed("interpolate", lambda: self._interpolate_vector(rebin=False))     # (e)
+        self.X.add_(self.U.t(), alpha=c.dt_s)                                   # (f)
 
     @property
     def spread_result(self):
         return self.ell
+
+
+# ---------------------------------------------------------------- reporting
+def fnv1a(data, h: int = 14695981039346656037) -> int:
+    """ib::bench::fnv1a (run.hpp:44-52), 64-bit FNV-1a over raw bytes
+    (a numpy array or bytes; computed by libibcuda's ibc_fnv1a)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from . import _capi
+
+    buf = np.ascontiguousarray(np.frombuffer(data, dtype=np.uint8) if isinstance(data, (bytes, bytearray))
+                               else data)
+    return int(_capi.load().ibc_fnv1a(buf.ctypes.data_as(C.c_void_p), buf.nbytes, h))
+
+
+@dataclass
+class TimingReport:
+    """ib::bench::TimingReport (run.hpp:36-42); seconds are device times."""
+
+    config: StepConfig
+    interpolate_seconds: list = field(default_factory=list)
+    spread_seconds: list = field(default_factory=list)
+    final_positions: object = None
+    physics_fingerprint: int = 0
+
+
+def run_benchmark(cfg: StepConfig, device: int = 0, fingerprint: bool = True) -> TimingReport:
+    """ib::bench::run_benchmark (run.hpp:59-128) on one GPU: cfg.steps steps,
+    two interpolate_vector timings and one spread_vector timing per step
+    (CUDA events), the final positions and the physics fingerprint (FNV-1a of
+    the positions, then of each spread component, run.hpp:120-126)."""
+    import torch
+
+    loop = MacStepLoop(cfg, device)
+    events: dict = {}
+    for _ in range(cfg.steps):
+        loop.step(events)
+    torch.cuda.synchronize(device)
+    rep = TimingReport(cfg)
+    rep.interpolate_seconds = [a.elapsed_time(b) * 1e-3 for a, b in events.get("interpolate", [])]
+    rep.spread_seconds = [a.elapsed_time(b) * 1e-3 for a, b in events.get("spread", [])]
+    rep.final_positions = loop.X.cpu().numpy()
+    if fingerprint:
+        h = fnv1a(rep.final_positions)
+        if cfg.steps > 0:
+            for comp in loop.ell:
+                h = fnv1a(comp.cpu().numpy(), h)
+        rep.physics_fingerprint = h
+    return rep
+
+
+CSV_HEADER = ("algorithm,refinement,n_points,workers,sweep_width,operation,calls,mean_s,min_s,"
+              "max_s,seed")  # report.hpp:16-18
+
+
+def _csv_row(rep: TimingReport, op: str, secs) -> str:
+    c = rep.config
+    mean = sum(secs) / len(secs) if secs else 0.0
+    mn, mx = (min(secs), max(secs)) if secs else (0.0, 0.0)
+    return (f"{c.algorithm},{c.refinement},{c.point_count},{c.workers},{c.sweep_width},{op},"
+            f"{len(secs)},{mean:.9e},{mn:.9e},{mx:.9e},{c.seed}")
+
+
+def write_csv(reports, stream) -> None:
+    """ib::bench::write_csv (report.hpp:60-66): header, then per report the
+    interpolate row and the spread row."""
+    stream.write(CSV_HEADER + "\n")
+    for r in reports:
+        stream.write(_csv_row(r, "interpolate", r.interpolate_seconds) + "\n")
+        stream.write(_csv_row(r, "spread", r.spread_seconds) + "\n")
