@@ -83,6 +83,21 @@ def build_cpp_tests() -> Path | None:
     return out
 
 
+SHIM_STEP = ROOT / "tools" / "build" / "shim_step"
+
+
+def build_tools() -> Path:
+    """tools/shim_step: bench.py's end-to-end figure through the C++ drop-in."""
+    src = ROOT / "tools" / "shim_step.cpp"
+    deps = [src, ROOT / "include" / "ibcuda.h", LIB, *OVERLAY]
+    if _stale(SHIM_STEP, deps):
+        SHIM_STEP.parent.mkdir(parents=True, exist_ok=True)
+        cmd = [_cxx(), "-O2", "-std=c++20", "-pthread", f"-I{ROOT / 'include'}", str(src), "-o",
+               str(SHIM_STEP), f"-L{LIB.parent}", "-libcuda", f"-Wl,-rpath,{LIB.parent}"]
+        subprocess.run(cmd, check=True)
+    return SHIM_STEP
+
+
 def build_overlay_test() -> Path | None:
     src = ROOT / "tests" / "cpp" / "overlay_test.cpp"
     out = ROOT / "tests" / "cpp" / "build" / "overlay_test"

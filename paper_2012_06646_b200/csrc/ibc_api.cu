@@ -11,6 +11,7 @@
 //   interpolate               interpolate.hpp:27-28
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -115,6 +116,19 @@ uint64_t shift_count(int dim, ibc_kernel k) {  // kernel.hpp:40-45
 
 void use_device(ibc::Context& c) { IBC_CUDA(cudaSetDevice(c.device)); }
 
+// Host <-> device copy in 8 MiB pieces.  A copy engine works through its
+// queue in order, so one large transfer would hold back every other
+// stream's copy in the same direction; in pieces, the copies of concurrent
+// host calls (other lanes) interleave with it.
+void copy_pieces(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
+  constexpr size_t kPiece = size_t{8} << 20;
+  for (size_t o = 0; o < bytes; o += kPiece) {
+    const size_t b = bytes - o < kPiece ? bytes - o : kPiece;
+    IBC_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, b,
+                             kind, st));
+  }
+}
+
 ibc::PointScratch& spread_scratch_for(ibc::Context& c, ibc_workspace* ws, size_t n,
                                       const ibc::DevGrid& g) {
   ibc::PointScratch& s = ws ? ws->w.s : c.spread_scratch;
@@ -150,6 +164,80 @@ void Context::prof_end(int cls, cudaEvent_t ev) {
   IBC_CUDA(cudaEventRecord(e, stream));
   pending.push_back({cls, {ev, e}});
 }
+
+Context* Context::acquire_lane() {
+  // A thread gets back the lane it used last when it is free: its staging and
+  // scratch are already sized for that thread's calls (a lane that has to grow
+  // a buffer calls cudaMalloc, which synchronizes the whole device).
+  thread_local const Context* last_owner = nullptr;
+  thread_local Context* last_lane = nullptr;
+  Context* lane = nullptr;
+  {
+    std::lock_guard<std::mutex> lock(*lanes_mu);
+    auto it = free_lanes.end();
+    if (last_owner == this) it = std::find(free_lanes.begin(), free_lanes.end(), last_lane);
+    if (it != free_lanes.end()) {
+      lane = *it;
+      free_lanes.erase(it);
+    } else if (!free_lanes.empty()) {
+      lane = free_lanes.back();
+      free_lanes.pop_back();
+    } else {
+      auto l = std::make_unique<Context>();
+      l->device = device;
+      l->sms = sms;
+      l->parent = this;
+      IBC_CUDA(cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking));
+      IBC_CUDA(cudaStreamCreateWithFlags(&l->copy_stream, cudaStreamNonBlocking));
+      lane = l.get();
+      lanes.push_back(std::move(l));
+    }
+    lane->spread_path = spread_path;
+    lane->profiling = profiling;
+  }
+  last_owner = this;
+  last_lane = lane;
+  // Ordered after everything already enqueued on the context's stream.
+  cudaEvent_t e = lane->acquire_event();
+  IBC_CUDA(cudaEventRecord(e, stream));
+  IBC_CUDA(cudaStreamWaitEvent(lane->stream, e, 0));
+  lane->event_pool.push_back(e);
+  return lane;
+}
+
+void Context::release_lane(Context* lane) {
+  std::lock_guard<std::mutex> lock(*lanes_mu);
+  free_lanes.push_back(lane);
+}
+
+uint64_t Context::total_launches() const {
+  uint64_t n = launches;
+  std::lock_guard<std::mutex> lock(*lanes_mu);
+  for (const auto& l : lanes) n += l->launches;
+  return n;
+}
+
+void Context::release_resources() {
+  for (auto& l : lanes) {
+    cudaStreamSynchronize(l->stream);
+    l->release_resources();
+    cudaStreamDestroy(l->stream);
+    cudaStreamDestroy(l->copy_stream);
+  }
+  lanes.clear();
+  free_lanes.clear();
+  spread_scratch.release_all();
+  interp_scratch.release_all();
+  prim_scratch.release_all();
+  for (auto& b : h_stage) b.release();
+  for (auto& p : pending) {
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  pending.clear();
+  for (auto e : event_pool) cudaEventDestroy(e);
+  event_pool.clear();
+}
 }  // namespace ibc
 
 extern "C" {
@@ -177,15 +265,7 @@ ibc_status ibc_context_destroy(ibc_context* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->c.device);
     cudaStreamSynchronize(ctx->c.stream);
-    ctx->c.spread_scratch.release_all();
-    ctx->c.interp_scratch.release_all();
-    ctx->c.prim_scratch.release_all();
-    for (auto& b : ctx->c.h_stage) b.release();
-    for (auto& p : ctx->c.pending) {
-      cudaEventDestroy(p.second.first);
-      cudaEventDestroy(p.second.second);
-    }
-    for (auto e : ctx->c.event_pool) cudaEventDestroy(e);
+    ctx->c.release_resources();
     delete ctx;
   });
 }
@@ -220,28 +300,42 @@ ibc_status ibc_context_set_profiling(ibc_context* ctx, int on) {
   });
 }
 
+static void fold_profile(ibc::Context& c) {
+  IBC_CUDA(cudaStreamSynchronize(c.stream));
+  for (auto& p : c.pending) {
+    float ms = 0.f;
+    IBC_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+    c.prof_ms[p.first] += ms;
+    c.event_pool.push_back(p.second.first);
+    c.event_pool.push_back(p.second.second);
+  }
+  c.pending.clear();
+}
+
 ibc_status ibc_context_get_profile(ibc_context* ctx, ibc_profile* out) {
   return guarded([&] {
     if (!ctx || !out) invalid("null argument");
     auto& c = ctx->c;
     use_device(c);
-    IBC_CUDA(cudaStreamSynchronize(c.stream));
-    for (auto& p : c.pending) {
-      float ms = 0.f;
-      IBC_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
-      c.prof_ms[p.first] += ms;
-      c.event_pool.push_back(p.second.first);
-      c.event_pool.push_back(p.second.second);
-    }
-    c.pending.clear();
-    out->keys_ms = c.prof_ms[ibc::kProfKeys];
-    out->sort_ms = c.prof_ms[ibc::kProfSort];
-    out->rows_ms = c.prof_ms[ibc::kProfRows];
-    out->prep_ms = c.prof_ms[ibc::kProfPrep];
-    out->spread_ms = c.prof_ms[ibc::kProfSpread];
-    out->interp_ms = c.prof_ms[ibc::kProfInterp];
-    out->spread_calls = c.spread_calls;
-    out->interp_calls = c.interp_calls;
+    std::lock_guard<std::mutex> lock(*c.lanes_mu);
+    double ms[ibc::kProfCount] = {0, 0, 0, 0, 0, 0};
+    uint64_t sc = 0, ic = 0;
+    auto add = [&](ibc::Context& x) {
+      fold_profile(x);
+      for (int k = 0; k < ibc::kProfCount; ++k) ms[k] += x.prof_ms[k];
+      sc += x.spread_calls;
+      ic += x.interp_calls;
+    };
+    add(c);
+    for (auto& l : c.lanes) add(*l);
+    out->keys_ms = ms[ibc::kProfKeys];
+    out->sort_ms = ms[ibc::kProfSort];
+    out->rows_ms = ms[ibc::kProfRows];
+    out->prep_ms = ms[ibc::kProfPrep];
+    out->spread_ms = ms[ibc::kProfSpread];
+    out->interp_ms = ms[ibc::kProfInterp];
+    out->spread_calls = sc;
+    out->interp_calls = ic;
   });
 }
 
@@ -249,18 +343,23 @@ ibc_status ibc_context_reset_profile(ibc_context* ctx) {
   return guarded([&] {
     if (!ctx) invalid("context is null");
     auto& c = ctx->c;
-    IBC_CUDA(cudaStreamSynchronize(c.stream));
-    for (auto& p : c.pending) {
-      c.event_pool.push_back(p.second.first);
-      c.event_pool.push_back(p.second.second);
-    }
-    c.pending.clear();
-    for (double& v : c.prof_ms) v = 0.0;
-    c.spread_calls = c.interp_calls = 0;
+    std::lock_guard<std::mutex> lock(*c.lanes_mu);
+    auto reset = [](ibc::Context& x) {
+      IBC_CUDA(cudaStreamSynchronize(x.stream));
+      for (auto& p : x.pending) {
+        x.event_pool.push_back(p.second.first);
+        x.event_pool.push_back(p.second.second);
+      }
+      x.pending.clear();
+      for (double& v : x.prof_ms) v = 0.0;
+      x.spread_calls = x.interp_calls = 0;
+    };
+    reset(c);
+    for (auto& l : c.lanes) reset(*l);
   });
 }
 
-uint64_t ibc_context_launches(const ibc_context* ctx) { return ctx ? ctx->c.launches : 0; }
+uint64_t ibc_context_launches(const ibc_context* ctx) { return ctx ? ctx->c.total_launches() : 0; }
 
 ibc_status ibc_grid_check(const ibc_grid* grid) { return guarded([&] { check_grid(grid); }); }
 
@@ -398,8 +497,9 @@ ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
     spread_checks(grid, kernel, algorithm, n_points, n_values, sweep_width, ws);
     if ((!points || !values) && n_points) invalid("null input buffer");
     if (!out) invalid("null output buffer");
-    auto& c = ctx->c;
-    use_device(c);
+    use_device(ctx->c);
+    ibc::Lane lane(ctx->c);
+    auto& c = *lane;
     const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
     // Serial/otf own no caller workspace: they run on the context's scratch.
     ibc_workspace* use_ws =
@@ -416,7 +516,7 @@ ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
                                c.stream));
     }
     ibc::spread_pipeline(c, g, c.h_stage[0].p, c.h_stage[1].p, n_points, s, c.h_stage[2].p);
-    IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream));
+    copy_pieces(out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream);
     IBC_CUDA(cudaStreamSynchronize(c.stream));
     g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
@@ -433,8 +533,9 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
     check_points(n_points);
     if (!field) invalid("null field");
     if (n_points && (!points || !out)) invalid("null point buffer");
-    auto& c = ctx->c;
-    use_device(c);
+    use_device(ctx->c);
+    ibc::Lane lane(ctx->c);
+    auto& c = *lane;
     const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
     const size_t np = grid_points(grid);
     c.interp_scratch.reserve_points(n_points, false);
@@ -442,12 +543,19 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
     c.h_stage[2].ensure(np);
     c.h_stage[0].ensure(n_points * grid->dim);
     c.h_stage[3].ensure(n_points);
-    IBC_CUDA(cudaMemcpyAsync(c.h_stage[2].p, field, np * 8, cudaMemcpyHostToDevice, c.stream));
+    // Points first: their binning (keys, row sort, records) runs while the
+    // field is still arriving on the lane's copy stream.
     if (n_points)
       IBC_CUDA(cudaMemcpyAsync(c.h_stage[0].p, points, n_points * grid->dim * 8,
                                cudaMemcpyHostToDevice, c.stream));
-    ibc::interp_pipeline(c, g, c.h_stage[2].p, c.h_stage[0].p, n_points, c.interp_scratch,
-                         c.h_stage[3].p);
+    cudaEvent_t field_in = c.acquire_event();
+    copy_pieces(c.h_stage[2].p, field, np * 8, cudaMemcpyHostToDevice, c.copy_stream);
+    IBC_CUDA(cudaEventRecord(field_in, c.copy_stream));
+    const ibc::InterpPlan P = ibc::interp_bin(c, g, c.h_stage[0].p, n_points, c.interp_scratch, true);
+    IBC_CUDA(cudaStreamWaitEvent(c.stream, field_in, 0));
+    c.event_pool.push_back(field_in);
+    ibc::interp_gather(c, g, P, c.h_stage[2].p, c.h_stage[0].p, n_points, c.interp_scratch,
+                       c.h_stage[3].p);
     if (n_points)
       IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[3].p, n_points * 8, cudaMemcpyDeviceToHost,
                                c.stream));
@@ -645,8 +753,9 @@ ibc_status ibc_key_value_sort(ibc_context* ctx, uint32_t* keys, void* payload, s
     if (n && payload_bytes && !payload) invalid("null payload buffer");
     check_points(n);
     if (n < 2) return;
-    auto& c = ctx->c;
-    use_device(c);
+    use_device(ctx->c);
+    ibc::Lane lane(ctx->c);
+    auto& c = *lane;
     c.h_stage[0].ensure((n * 4 + 7) / 8);
     c.h_stage[1].ensure((n * payload_bytes + 7) / 8 + 1);
     auto* dk = reinterpret_cast<uint32_t*>(c.h_stage[0].p);
@@ -669,8 +778,9 @@ static void reduce_host(ibc_context* ctx, const uint32_t* keys, const double* va
   check_points(n);
   *q = 0;
   if (n == 0) return;
-  auto& c = ctx->c;
-  use_device(c);
+  use_device(ctx->c);
+  ibc::Lane lane(ctx->c);
+  auto& c = *lane;
   c.h_stage[0].ensure((n * 4 + 7) / 8);
   auto* dk = reinterpret_cast<uint32_t*>(c.h_stage[0].p);
   IBC_CUDA(cudaMemcpyAsync(dk, keys, n * 4, cudaMemcpyHostToDevice, c.stream));

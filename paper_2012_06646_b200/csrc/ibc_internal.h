@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -93,6 +95,35 @@ struct Context {
   cudaEvent_t acquire_event();
   void prof_begin(int cls, cudaEvent_t* ev);
   void prof_end(int cls, cudaEvent_t ev);
+
+  // Host-buffer calls run on a lane: a sub-context with its own stream,
+  // staging and scratch, ordered after the work already on `stream`.  Host
+  // calls from different threads (the reference's threading contract:
+  // concurrent calls on disjoint outputs are safe, spread.hpp:26) then
+  // overlap on the device and on both PCIe directions.
+  Context* parent = nullptr;
+  cudaStream_t copy_stream = nullptr;  // lanes: a second stream for overlapped copies
+  std::unique_ptr<std::mutex> lanes_mu = std::make_unique<std::mutex>();
+  std::vector<std::unique_ptr<Context>> lanes;
+  std::vector<Context*> free_lanes;
+  Context* acquire_lane();
+  void release_lane(Context* lane);
+  uint64_t total_launches() const;
+  void release_resources();  // scratch, staging, events, lanes (not the user's stream)
+};
+
+// RAII lane of a context for one host-buffer call.
+class Lane {
+ public:
+  explicit Lane(Context& c) : parent_(c), lane_(c.acquire_lane()) {}
+  ~Lane() { parent_.release_lane(lane_); }
+  Lane(const Lane&) = delete;
+  Lane& operator=(const Lane&) = delete;
+  Context& operator*() const { return *lane_; }
+
+ private:
+  Context& parent_;
+  Context* lane_;
 };
 
 struct Workspace {

@@ -475,3 +475,29 @@ def test_config_clustered_full_array_parity():
     from paper_2012_06646_b200 import synth
 
     _full_size_parity(512, synth.clustered_points(1 << 22, 16e-4, 64, 8 * 16e-4 / 512, 5), 32)
+
+
+def test_concurrent_host_calls_from_threads_match_serial():
+    """The reference's threading contract (spread.hpp:26):
+    concurrent calls on disjoint outputs are safe.  Host-buffer calls run on
+    per-call lanes of the context; results equal the one-thread calls bit for
+    bit."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    rng = np.random.default_rng(77)
+    g = ib.StaggeredGrid([64, 48, 40], 0.1, [0.5, 0.5, 0.0], [True] * 3)
+    n = 30000
+    pts = [rand_points(g, n, rng) for _ in range(4)]
+    vals = [rng.uniform(-1, 1, n) for _ in range(4)]
+    e = ib.GridField(g, rng.uniform(-1, 1, g.point_count()))
+    want_s = [ib.spread_serial(p, v, g, K).values for p, v in zip(pts, vals)]
+    want_i = [ib.interpolate(e, p, K) for p in pts]
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        fs = [pool.submit(lambda p=p, v=v: ib.spread_serial(p, v, g, K).values) for p, v in zip(pts, vals)]
+        fi = [pool.submit(lambda p=p: ib.interpolate(e, p, K)) for p in pts]
+        got_s = [f.result() for f in fs]
+        got_i = [f.result() for f in fi]
+    for a, b in zip(got_s, want_s):
+        assert np.array_equal(a, b)
+    for a, b in zip(got_i, want_i):
+        assert np.array_equal(a, b)
