@@ -116,16 +116,71 @@ uint64_t shift_count(int dim, ibc_kernel k) {  // kernel.hpp:40-45
 
 void use_device(ibc::Context& c) { IBC_CUDA(cudaSetDevice(c.device)); }
 
-// Host <-> device copy in 8 MiB pieces.  A copy engine works through its
-// queue in order, so one large transfer would hold back every other
-// stream's copy in the same direction; in pieces, the copies of concurrent
-// host calls (other lanes) interleave with it.
-void copy_pieces(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t st) {
-  constexpr size_t kPiece = size_t{8} << 20;
-  for (size_t o = 0; o < bytes; o += kPiece) {
-    const size_t b = bytes - o < kPiece ? bytes - o : kPiece;
-    IBC_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, b,
-                             kind, st));
+constexpr size_t kPiece = size_t{8} << 20;
+
+// Page-locked (or device / managed) memory: the copy engines reach it directly.
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type != cudaMemoryTypeUnregistered;
+}
+
+// Host memcpy over the OpenMP team (one pageable <-> pinned stage piece).
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kSlice = size_t{1} << 20;
+  const long slices = (long)((bytes + kSlice - 1) / kSlice);
+#pragma omp parallel for schedule(static)
+  for (long i = 0; i < slices; ++i) {
+    const size_t o = (size_t)i * kSlice, b = bytes - o < kSlice ? bytes - o : kSlice;
+    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, b);
+  }
+}
+
+// Host <-> device copy of a host-buffer call, in 8 MiB pieces.  A copy
+// engine works through its queue in order, so one large transfer would hold
+// back every other stream's copy in the same direction; in pieces, the copies
+// of concurrent host calls (other lanes) interleave with it.  Pageable host
+// memory (a std::vector behind the C++ drop-in) goes through the lane's
+// pinned stage: the host copies piece k while the engine moves piece k - 1.
+void host_copy(ibc::Context& c, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind,
+               cudaStream_t st) {
+  if (!bytes) return;
+  const bool h2d = kind == cudaMemcpyHostToDevice;
+  const void* host = h2d ? src : dst;
+  if (is_pinned(host)) {
+    for (size_t o = 0; o < bytes; o += kPiece) {
+      const size_t b = bytes - o < kPiece ? bytes - o : kPiece;
+      IBC_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, b,
+                               kind, st));
+    }
+    return;
+  }
+  c.ensure_stage(kPiece);
+  const size_t pieces = (bytes + kPiece - 1) / kPiece;
+  for (size_t k = 0; k <= pieces; ++k) {
+    // H2D: fill stage k % S on the host, then queue its DMA.
+    // D2H: queue the DMA of piece k, then drain piece k - 1 on the host.
+    if (k < pieces) {
+      const size_t o = k * kPiece, b = bytes - o < kPiece ? bytes - o : kPiece;
+      const int sl = (int)(k % ibc::Context::kStages);
+      IBC_CUDA(cudaEventSynchronize(c.stage_free[sl]));  // its previous DMA is done
+      if (h2d) {
+        parallel_memcpy(c.stage[sl], static_cast<const char*>(src) + o, b);
+        IBC_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + o, c.stage[sl], b, kind, st));
+      } else {
+        IBC_CUDA(cudaMemcpyAsync(c.stage[sl], static_cast<const char*>(src) + o, b, kind, st));
+      }
+      IBC_CUDA(cudaEventRecord(c.stage_free[sl], st));
+    }
+    if (!h2d && k > 0) {
+      const size_t o = (k - 1) * kPiece, b = bytes - o < kPiece ? bytes - o : kPiece;
+      const int sl = (int)((k - 1) % ibc::Context::kStages);
+      IBC_CUDA(cudaEventSynchronize(c.stage_free[sl]));
+      parallel_memcpy(static_cast<char*>(dst) + o, c.stage[sl], b);
+    }
   }
 }
 
@@ -210,6 +265,17 @@ void Context::release_lane(Context* lane) {
   free_lanes.push_back(lane);
 }
 
+void Context::ensure_stage(size_t bytes) {
+  if (stage_bytes >= bytes) return;
+  for (int i = 0; i < kStages; ++i) {
+    if (stage[i]) cudaFreeHost(stage[i]);
+    stage[i] = nullptr;
+    IBC_CUDA(cudaHostAlloc(&stage[i], bytes, cudaHostAllocDefault));
+    if (!stage_free[i]) IBC_CUDA(cudaEventCreateWithFlags(&stage_free[i], cudaEventDisableTiming));
+  }
+  stage_bytes = bytes;
+}
+
 uint64_t Context::total_launches() const {
   uint64_t n = launches;
   std::lock_guard<std::mutex> lock(*lanes_mu);
@@ -237,6 +303,13 @@ void Context::release_resources() {
   pending.clear();
   for (auto e : event_pool) cudaEventDestroy(e);
   event_pool.clear();
+  for (int i = 0; i < kStages; ++i) {
+    if (stage[i]) cudaFreeHost(stage[i]);
+    if (stage_free[i]) cudaEventDestroy(stage_free[i]);
+    stage[i] = nullptr;
+    stage_free[i] = nullptr;
+  }
+  stage_bytes = 0;
 }
 }  // namespace ibc
 
@@ -510,13 +583,12 @@ ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
     c.h_stage[1].ensure(n_points);
     c.h_stage[2].ensure(np);
     if (n_points) {
-      IBC_CUDA(cudaMemcpyAsync(c.h_stage[0].p, points, n_points * grid->dim * 8,
-                               cudaMemcpyHostToDevice, c.stream));
-      IBC_CUDA(cudaMemcpyAsync(c.h_stage[1].p, values, n_points * 8, cudaMemcpyHostToDevice,
-                               c.stream));
+      host_copy(c, c.h_stage[0].p, points, n_points * grid->dim * 8, cudaMemcpyHostToDevice,
+                c.stream);
+      host_copy(c, c.h_stage[1].p, values, n_points * 8, cudaMemcpyHostToDevice, c.stream);
     }
     ibc::spread_pipeline(c, g, c.h_stage[0].p, c.h_stage[1].p, n_points, s, c.h_stage[2].p);
-    copy_pieces(out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream);
+    host_copy(c, out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream);
     IBC_CUDA(cudaStreamSynchronize(c.stream));
     g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });
@@ -546,19 +618,17 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
     // Points first: their binning (keys, row sort, records) runs while the
     // field is still arriving on the lane's copy stream.
     if (n_points)
-      IBC_CUDA(cudaMemcpyAsync(c.h_stage[0].p, points, n_points * grid->dim * 8,
-                               cudaMemcpyHostToDevice, c.stream));
+      host_copy(c, c.h_stage[0].p, points, n_points * grid->dim * 8, cudaMemcpyHostToDevice,
+                c.stream);
     cudaEvent_t field_in = c.acquire_event();
-    copy_pieces(c.h_stage[2].p, field, np * 8, cudaMemcpyHostToDevice, c.copy_stream);
+    host_copy(c, c.h_stage[2].p, field, np * 8, cudaMemcpyHostToDevice, c.copy_stream);
     IBC_CUDA(cudaEventRecord(field_in, c.copy_stream));
     const ibc::InterpPlan P = ibc::interp_bin(c, g, c.h_stage[0].p, n_points, c.interp_scratch, true);
     IBC_CUDA(cudaStreamWaitEvent(c.stream, field_in, 0));
     c.event_pool.push_back(field_in);
     ibc::interp_gather(c, g, P, c.h_stage[2].p, c.h_stage[0].p, n_points, c.interp_scratch,
                        c.h_stage[3].p);
-    if (n_points)
-      IBC_CUDA(cudaMemcpyAsync(out, c.h_stage[3].p, n_points * 8, cudaMemcpyDeviceToHost,
-                               c.stream));
+    if (n_points) host_copy(c, out, c.h_stage[3].p, n_points * 8, cudaMemcpyDeviceToHost, c.stream);
     IBC_CUDA(cudaStreamSynchronize(c.stream));
     g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
   });

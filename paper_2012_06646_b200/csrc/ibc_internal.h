@@ -103,6 +103,12 @@ struct Context {
   // overlap on the device and on both PCIe directions.
   Context* parent = nullptr;
   cudaStream_t copy_stream = nullptr;  // lanes: a second stream for overlapped copies
+  // Pinned stage for pageable host buffers (host_copy in ibc_api.cu).
+  static constexpr int kStages = 3;
+  void* stage[kStages] = {nullptr, nullptr, nullptr};
+  cudaEvent_t stage_free[kStages] = {nullptr, nullptr, nullptr};
+  size_t stage_bytes = 0;
+  void ensure_stage(size_t bytes);
   std::unique_ptr<std::mutex> lanes_mu = std::make_unique<std::mutex>();
   std::vector<std::unique_ptr<Context>> lanes;
   std::vector<Context*> free_lanes;

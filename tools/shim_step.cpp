@@ -48,19 +48,26 @@ int main(int argc, char** argv) {
   for (auto& v : e.values) v = 2.0 * unit(r4) - 1.0;
   ib::SpreadWorkspace<3> ws(n, g);
   const ib::CosineKernel k;
-  std::vector<double> t;
+  std::vector<double> t, ts, ti;
   double check = 0.0;
   for (int rep = 0; rep <= reps; ++rep) {
     const auto t0 = std::chrono::steady_clock::now();
     std::size_t q = 0;
     ib::LagrangianValues E;
     double ell_probe = 0.0;
+    double t_s = 0.0, t_i = 0.0;
     auto spread = [&] {
+      const auto a = std::chrono::steady_clock::now();
       const auto ell = ib::spread_fused(xs, std::span<const double>(G), g, k, ws, 8);
       q = ws.run_count;
       ell_probe = ell.values[ell.values.size() / 3];
+      t_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
     };
-    auto interp = [&] { E = ib::interpolate(e, xn, k, 8); };
+    auto interp = [&] {
+      const auto a = std::chrono::steady_clock::now();
+      E = ib::interpolate(e, xn, k, 8);
+      t_i = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count();
+    };
     if (concurrent) {
       std::thread ti(interp);
       spread();
@@ -70,11 +77,18 @@ int main(int argc, char** argv) {
       interp();
     }
     const auto t1 = std::chrono::steady_clock::now();
-    if (rep > 0) t.push_back(std::chrono::duration<double>(t1 - t0).count());
+    if (rep > 0) {
+      t.push_back(std::chrono::duration<double>(t1 - t0).count());
+      ts.push_back(t_s);
+      ti.push_back(t_i);
+    }
     check = ell_probe + E[n / 2] + static_cast<double>(q);
   }
   std::sort(t.begin(), t.end());
-  std::printf("step_s_median %.9e min %.9e reps %d concurrent %d check %.17g\n", t[t.size() / 2],
-              t[0], reps, concurrent ? 1 : 0, check);
+  std::sort(ts.begin(), ts.end());
+  std::sort(ti.begin(), ti.end());
+  std::printf("step_s_median %.9e min %.9e reps %d concurrent %d spread_s %.3e interp_s %.3e check %.17g\n",
+              t[t.size() / 2], t[0], reps, concurrent ? 1 : 0, ts[ts.size() / 2], ti[ti.size() / 2],
+              check);
   return 0;
 }
