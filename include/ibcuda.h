@@ -227,6 +227,51 @@ ibc_status ibc_interpolate_slab_device(ibc_context* ctx, const ibc_grid* local_g
                                        const ibc_slab* slab, ibc_kernel kernel,
                                        const double* d_field, const double* d_points, size_t n,
                                        double* d_out);
+/* ---- Peer-memory exchanges of the slab decomposition (NVLink / NVSwitch).
+ * Each rank shares its local slab buffer and an 8-word signal block with its
+ * ring neighbours -- CUDA IPC handles across processes (ibc_ipc_*), plain
+ * device pointers within one process -- and each exchange pulls the
+ * neighbours' planes straight out of their buffers with one kernel, ordered
+ * across ranks by device-side release/acquire flags (a handshake kernel
+ * before and after it).  No NCCL, no host synchronisation: capturable in a
+ * CUDA graph with the local operators.  Every rank calls the same sequence of
+ * exchanges with the same strictly increasing epochs.  A neighbour that never
+ * arrives sets the signal block's timeout flag after ~2 s instead of hanging
+ * the device (ibc_slab_link_error). */
+typedef struct {
+  int nloc;              /* owned planes of this rank, z1 - z0 (>= 2) */
+  int nloc_down;         /* owned planes of the rank below */
+  size_t plane;          /* values per plane: prod of the other extents */
+  int has_down, has_up;  /* 0 at a closed end of the global axis */
+  double* d_local;       /* this rank's local slab: nloc + 3 planes */
+  const double* d_down;  /* the rank below's local slab (peer pointer) */
+  const double* d_up;    /* the rank above's local slab (peer pointer) */
+  uint64_t* d_sig;       /* this rank's signal block (ibc_slab_signals_create) */
+  uint64_t* d_sig_down;  /* the rank below's signal block (peer pointer) */
+  uint64_t* d_sig_up;    /* the rank above's signal block (peer pointer) */
+} ibc_slab_link;
+
+typedef struct {
+  unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} ibc_ipc_handle;
+
+/* cudaMalloc'd device memory (a whole allocation: shareable by IPC). */
+ibc_status ibc_device_alloc(ibc_context* ctx, size_t bytes, void** d_ptr);
+ibc_status ibc_device_free(ibc_context* ctx, void* d_ptr);
+ibc_status ibc_ipc_get_handle(ibc_context* ctx, void* d_ptr, ibc_ipc_handle* out);
+ibc_status ibc_ipc_open_handle(ibc_context* ctx, const ibc_ipc_handle* h, void** d_peer);
+ibc_status ibc_ipc_close_handle(ibc_context* ctx, void* d_peer);
+/* An 8 x uint64 signal block, zeroed (a whole allocation). */
+ibc_status ibc_slab_signals_create(ibc_context* ctx, uint64_t** d_sig);
+/* Ghost-plane sum after the local spread into link->d_local (ibc_spread_slab_device):
+ * own[2] += below's plane z0, own[nloc], own[nloc+1] += above's planes z1-2, z1-1. */
+ibc_status ibc_slab_ghost_sum_device(ibc_context* ctx, const ibc_slab_link* link, uint64_t epoch);
+/* Halo fill before the local gather: link->d_local's planes 0, 1 and nloc+2 from
+ * the neighbours' owned planes (zero at a closed end). */
+ibc_status ibc_slab_halo_fill_device(ibc_context* ctx, const ibc_slab_link* link, uint64_t epoch);
+/* 1 if a handshake on this rank timed out (synchronizes the context stream). */
+ibc_status ibc_slab_link_error(ibc_context* ctx, const ibc_slab_link* link, int* timed_out);
+
 /* Wrapped home cell along the last axis (cell_index + wrap, grid.hpp:121-151)
  * of every point of a global grid: the slab each point belongs to. */
 ibc_status ibc_home_planes_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,

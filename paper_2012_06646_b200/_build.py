@@ -10,7 +10,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "_lib" / "libibcuda.so"
-SOURCES = ["ibc_kernels.cu", "ibc_api.cu"]
+SOURCES = ["ibc_kernels.cu", "ibc_api.cu", "ibc_slab.cu"]
 HEADERS = ["ibc_device.cuh", "ibc_sort.cuh", "ibc_internal.h", "ibc_sweep.cuh", "ibc_tma.cuh", "ibc_bucket.cuh", "ibc_spread.cuh"]
 
 NVCC_FLAGS = [
@@ -80,6 +80,22 @@ def build_cpp_tests() -> Path | None:
                f"-L{ROOT / 'oracle'}", "-loracle", f"-Wl,-rpath,{ROOT / 'oracle'}"]
         subprocess.run(cmd, check=True)
     build_overlay_test()
+    build_slab_test()
+    return out
+
+
+def build_slab_test() -> Path:
+    """tests/cpp/build/slab_test: a multi-rank C++ caller of the z-slab C ABI."""
+    src = ROOT / "tests" / "cpp" / "slab_test.cpp"
+    out = ROOT / "tests" / "cpp" / "build" / "slab_test"
+    if _stale(out, [src, ROOT / "include" / "ibcuda.h", LIB]):
+        out.parent.mkdir(parents=True, exist_ok=True)
+        cuda = Path(nvcc()).resolve().parents[1]
+        cmd = [_cxx(), "-O2", "-std=c++17", "-pthread", f"-I{ROOT / 'include'}",
+               f"-I{cuda / 'include'}", str(src), "-o", str(out), f"-L{LIB.parent}", "-libcuda",
+               f"-Wl,-rpath,{LIB.parent}", f"-L{cuda / 'lib64'}", "-lcudart",
+               f"-Wl,-rpath,{cuda / 'lib64'}"]
+        subprocess.run(cmd, check=True)
     return out
 
 

@@ -66,6 +66,26 @@ class IbcSlab(C.Structure):
     ]
 
 
+class IbcSlabLink(C.Structure):
+    _fields_ = [
+        ("nloc", C.c_int),
+        ("nloc_down", C.c_int),
+        ("plane", C.c_size_t),
+        ("has_down", C.c_int),
+        ("has_up", C.c_int),
+        ("d_local", C.c_void_p),
+        ("d_down", C.c_void_p),
+        ("d_up", C.c_void_p),
+        ("d_sig", C.c_void_p),
+        ("d_sig_down", C.c_void_p),
+        ("d_sig_up", C.c_void_p),
+    ]
+
+
+class IbcIpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 _vp = C.c_void_p
 _sz = C.c_size_t
 _G = C.POINTER(IbcGrid)
@@ -108,6 +128,15 @@ SIGNATURES = {
     "ibc_collect_unique_keys": (_st, [_vp, _vp, _sz, _vp, _sz, C.POINTER(_sz)]),
     "ibc_add_delta_evaluations": (None, [C.c_uint64]),
     "ibc_fnv1a": (C.c_uint64, [_vp, _sz, C.c_uint64]),
+    "ibc_device_alloc": (_st, [_vp, _sz, C.POINTER(_vp)]),
+    "ibc_device_free": (_st, [_vp, _vp]),
+    "ibc_ipc_get_handle": (_st, [_vp, _vp, C.POINTER(IbcIpcHandle)]),
+    "ibc_ipc_open_handle": (_st, [_vp, C.POINTER(IbcIpcHandle), C.POINTER(_vp)]),
+    "ibc_ipc_close_handle": (_st, [_vp, _vp]),
+    "ibc_slab_signals_create": (_st, [_vp, C.POINTER(_vp)]),
+    "ibc_slab_ghost_sum_device": (_st, [_vp, C.POINTER(IbcSlabLink), C.c_uint64]),
+    "ibc_slab_halo_fill_device": (_st, [_vp, C.POINTER(IbcSlabLink), C.c_uint64]),
+    "ibc_slab_link_error": (_st, [_vp, C.POINTER(IbcSlabLink), C.POINTER(C.c_int)]),
     "ibc_binned_create": (_st, [_vp, C.POINTER(_vp)]),
     "ibc_binned_destroy": (_st, [_vp]),
     "ibc_bin_points_device": (_st, [_vp, _vp, _G, C.c_int, _vp, _sz]),

@@ -902,6 +902,101 @@ ibc_status ibc_collect_unique_keys(ibc_context* ctx, const uint32_t* sorted_keys
   });
 }
 
+// ---------------------------------------------------------------- Slab peers
+ibc_status ibc_device_alloc(ibc_context* ctx, size_t bytes, void** d_ptr) {
+  return guarded([&] {
+    if (!ctx || !d_ptr) invalid("null argument");
+    use_device(ctx->c);
+    IBC_CUDA(cudaMalloc(d_ptr, bytes ? bytes : 1));
+  });
+}
+
+ibc_status ibc_device_free(ibc_context* ctx, void* d_ptr) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    use_device(ctx->c);
+    if (d_ptr) IBC_CUDA(cudaFree(d_ptr));
+  });
+}
+
+ibc_status ibc_ipc_get_handle(ibc_context* ctx, void* d_ptr, ibc_ipc_handle* out) {
+  static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(ibc_ipc_handle), "IPC handle size");
+  return guarded([&] {
+    if (!ctx || !d_ptr || !out) invalid("null argument");
+    use_device(ctx->c);
+    cudaIpcMemHandle_t h;
+    IBC_CUDA(cudaIpcGetMemHandle(&h, d_ptr));
+    std::memcpy(out->bytes, &h, sizeof(h));
+  });
+}
+
+ibc_status ibc_ipc_open_handle(ibc_context* ctx, const ibc_ipc_handle* h, void** d_peer) {
+  return guarded([&] {
+    if (!ctx || !h || !d_peer) invalid("null argument");
+    use_device(ctx->c);
+    cudaIpcMemHandle_t m;
+    std::memcpy(&m, h->bytes, sizeof(m));
+    IBC_CUDA(cudaIpcOpenMemHandle(d_peer, m, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+
+ibc_status ibc_ipc_close_handle(ibc_context* ctx, void* d_peer) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    use_device(ctx->c);
+    if (d_peer) IBC_CUDA(cudaIpcCloseMemHandle(d_peer));
+  });
+}
+
+ibc_status ibc_slab_signals_create(ibc_context* ctx, uint64_t** d_sig) {
+  return guarded([&] {
+    if (!ctx || !d_sig) invalid("null argument");
+    use_device(ctx->c);
+    IBC_CUDA(cudaMalloc(reinterpret_cast<void**>(d_sig), 8 * sizeof(uint64_t)));
+    IBC_CUDA(cudaMemset(*d_sig, 0, 8 * sizeof(uint64_t)));
+  });
+}
+
+static void check_link(const ibc_slab_link* L) {
+  if (!L) invalid("link is null");
+  if (L->nloc < 2 || (L->has_down && L->nloc_down < 2)) invalid("a slab owns at least 2 planes");
+  if (!L->d_local || !L->d_sig) invalid("null local slab or signal block");
+  if (L->has_down && (!L->d_down || !L->d_sig_down)) invalid("missing the rank below's buffers");
+  if (L->has_up && (!L->d_up || !L->d_sig_up)) invalid("missing the rank above's buffers");
+}
+
+ibc_status ibc_slab_ghost_sum_device(ibc_context* ctx, const ibc_slab_link* link, uint64_t epoch) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_link(link);
+    if (epoch == 0) invalid("epochs start at 1");
+    use_device(ctx->c);
+    ibc::slab_exchange(ctx->c, *link, epoch, true);
+  });
+}
+
+ibc_status ibc_slab_halo_fill_device(ibc_context* ctx, const ibc_slab_link* link, uint64_t epoch) {
+  return guarded([&] {
+    if (!ctx) invalid("context is null");
+    check_link(link);
+    if (epoch == 0) invalid("epochs start at 1");
+    use_device(ctx->c);
+    ibc::slab_exchange(ctx->c, *link, epoch, false);
+  });
+}
+
+ibc_status ibc_slab_link_error(ibc_context* ctx, const ibc_slab_link* link, int* timed_out) {
+  return guarded([&] {
+    if (!ctx || !timed_out) invalid("null argument");
+    check_link(link);
+    use_device(ctx->c);
+    uint64_t v = 0;
+    IBC_CUDA(cudaMemcpyAsync(&v, link->d_sig + 7, 8, cudaMemcpyDeviceToHost, ctx->c.stream));
+    IBC_CUDA(cudaStreamSynchronize(ctx->c.stream));
+    *timed_out = v != 0;
+  });
+}
+
 uint64_t ibc_fnv1a(const void* data, size_t bytes, uint64_t hash) {
   const auto* p = static_cast<const unsigned char*>(data);
   for (size_t i = 0; i < bytes; ++i) {

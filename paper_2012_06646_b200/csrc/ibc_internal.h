@@ -174,6 +174,9 @@ size_t compute_run_keys(Context& ctx, PointScratch& s);
 void ensure_observables(Context& ctx, PointScratch& s);
 size_t read_run_count(Context& ctx, PointScratch& s);
 
+// Peer-memory slab exchange (ibc_slab.cu): ghost_sum or halo fill.
+void slab_exchange(Context& ctx, const ibc_slab_link& L, uint64_t epoch, bool ghost_sum);
+
 // Primitives (sort.hpp / reduce.hpp) on device buffers, in the context stream.
 // Stable sort of n 32-bit keys in place, with a payload of `bytes` bytes per
 // key (may be null).
