@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
     ap.add_argument("--mac-steps", type=int, default=5, help="MAC vector step timing (0: skip)")
     ap.add_argument("--no-serial", action="store_true", help="reference arm: skip the spread_serial timing")
+    ap.add_argument("--transport", default="peer", choices=["peer", "collective"],
+                    help="N > 1: slab exchange over peer memory (C ABI, one CUDA graph per step) "
+                         "or torch.distributed send/recv between graph replays")
     ap.add_argument("--strong", action="store_true",
                     help="N > 1: strong scaling -- config 2 (2^20 points, one 256^3 grid) split into N z-slabs")
     ap.add_argument("--workload", default="c2", choices=["c2", "c1", "w128", "w256", "rbc", "clustered"],
@@ -220,6 +223,12 @@ def run_config(args, world: int, n1: int, N: int) -> dict:
             "z-slabs, each rank the points homed in its slab; per step one scalar spread (local + "
             "ghost-plane sum) and one scalar interpolation (halo fill + local gather), FP64",
             1 << 20, [256, 256, 256])
+    if args.workload == "w256":
+        return bench_config(
+            f"config 3 (1 point per cell) at constant load, weak scaling: {world} z-slabs of a "
+            f"256 x 256 x {256 * world} periodic grid, 256^3 points homed in each slab; per step "
+            "one scalar spread (local + ghost-plane sum) and one scalar interpolation (halo fill "
+            "+ local gather), FP64", world * 256 ** 3, [256, 256, 256 * world])
     return bench_config(
         f"config 2 per GPU, weak scaling: {world} z-slabs of a 256 x 256 x {256 * world} periodic "
         "grid, 2^20 points homed in each slab; per step one scalar spread (local + ghost-plane "
@@ -349,7 +358,7 @@ def run_ours(args):
                         np.asarray(data["field"]).reshape(N, N * N)[zb[rank]:zb[rank + 1]].reshape(-1)))
         n = len(data["x_n"])
     else:
-        data = synth.slab_config(rank, world)
+        data = synth.slab_config(rank, world, 256 ** 3 if args.workload == "w256" else 1 << 20)
         n, N, h = data["n"], data["N"], data["h"]
         grid = ib.StaggeredGrid([N, N, data["nz_global"]], h, [0.5, 0.5, 0.0], [True] * 3)
         ops = DeviceOperators(local)
@@ -364,15 +373,34 @@ def run_ours(args):
     E = torch.empty(n, dtype=torch.float64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
 
+    transport = args.transport if dec is not None else None
     if dec is not None:
         local_out = torch.empty(dec.local.point_count(), dtype=torch.float64, device=dev)
         field_local = torch.empty(dec.local.point_count(), dtype=torch.float64, device=dev)
+        # Size every scratch buffer before any cross-rank handshake.
+        dec._device_spread(xs, gv, out=local_out)
+        dec._device_interpolate(field_local, xn, out=E)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if transport == "peer":
+            # Peer-memory exchange: CUDA IPC handles swapped once over the
+            # process group; the field's owned planes live in the shared slab.
+            peer = dec.use_peer_transport()
+            peer.owned_field.copy_(fe)
+            torch.cuda.synchronize()
+            dist.barrier()
     # The device-side pieces of a step: both operators on one GPU; for slabs
-    # the local spread and the local gather, with the NCCL ghost-plane sum and
-    # halo fill between them (eager: they go through torch.distributed).
-    local_ops = [(lambda: (ops.spread(xs, gv, grid, out=ell), ops.interpolate(fe, xn, grid, out=E)))] \
-        if dec is None else [lambda: dec._device_spread(xs, gv, out=local_out),
-                             lambda: dec._device_interpolate(field_local, xn, out=E)]
+    # the local spread, the ghost-plane sum, the halo fill and the local
+    # gather -- one piece over peer memory (the whole step is one CUDA graph),
+    # or the local operators with the NCCL exchanges between them (eager:
+    # they go through torch.distributed).
+    if dec is None:
+        local_ops = [lambda: (ops.spread(xs, gv, grid, out=ell), ops.interpolate(fe, xn, grid, out=E))]
+    elif transport == "peer":
+        local_ops = [lambda: (dec.spread(xs, gv), dec.interpolate(None, xn, out=E))]
+    else:
+        local_ops = [lambda: dec._device_spread(xs, gv, out=local_out),
+                     lambda: dec._device_interpolate(field_local, xn, out=E)]
     graphs = [None] * len(local_ops)
 
     def step(eager=False):
@@ -383,7 +411,7 @@ def run_ours(args):
                 local_ops[k]()
 
         run(0)
-        if dec is not None:
+        if dec is not None and transport != "peer":
             dec.ghost_sum(local_out)
             dec.halo_fill(fe, out=field_local)
             run(1)
@@ -611,7 +639,10 @@ def run_ours(args):
             "scaling": "strong" if strong else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": run_config(args, world, n if world == 1 else total_points, N),
-            "parallelism": f"z-slab x{world} (ghost/halo exchange)" if world > 1 else "single GPU",
+            "parallelism": (f"z-slab x{world} (ghost-plane sum + halo fill over "
+                            + ("NVLink peer memory, one CUDA graph per step)" if transport == "peer"
+                               else "torch.distributed send/recv)"))
+                           if world > 1 else "single GPU",
             "n_points_per_gpu": n,
             "l2": "flushed between steps (256 MiB write outside the events)",
             "cuda_graph": graph is not None,

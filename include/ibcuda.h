@@ -235,7 +235,9 @@ ibc_status ibc_interpolate_slab_device(ibc_context* ctx, const ibc_grid* local_g
  * across ranks by device-side release/acquire flags (a handshake kernel
  * before and after it).  No NCCL, no host synchronisation: capturable in a
  * CUDA graph with the local operators.  Every rank calls the same sequence of
- * exchanges with the same strictly increasing epochs.  A neighbour that never
+ * exchanges, either with the same strictly increasing epochs (>= 1) or with
+ * epoch 0 = automatic (a device-side counter per rank: what a replayed CUDA
+ * graph needs; do not mix the two on one signal block).  A neighbour that never
  * arrives sets the signal block's timeout flag after ~2 s instead of hanging
  * the device (ibc_slab_link_error). */
 typedef struct {

@@ -969,7 +969,6 @@ ibc_status ibc_slab_ghost_sum_device(ibc_context* ctx, const ibc_slab_link* link
   return guarded([&] {
     if (!ctx) invalid("context is null");
     check_link(link);
-    if (epoch == 0) invalid("epochs start at 1");
     use_device(ctx->c);
     ibc::slab_exchange(ctx->c, *link, epoch, true);
   });
@@ -979,7 +978,6 @@ ibc_status ibc_slab_halo_fill_device(ibc_context* ctx, const ibc_slab_link* link
   return guarded([&] {
     if (!ctx) invalid("context is null");
     check_link(link);
-    if (epoch == 0) invalid("epochs start at 1");
     use_device(ctx->c);
     ibc::slab_exchange(ctx->c, *link, epoch, false);
   });

@@ -17,7 +17,9 @@
 //              local[nloc + 2] = above.local[2]
 // Signal block (8 x uint64, one per rank, written by the neighbours):
 //   [0] ready epoch from below  [1] ready epoch from above
-//   [2] done epoch from below   [3] done epoch from above   [7] timeout flag
+//   [2] done epoch from below   [3] done epoch from above
+//   [4] this rank's exchange counter, [5] its current epoch (automatic epochs)
+//   [7] timeout flag
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -27,7 +29,8 @@
 namespace ibc {
 namespace {
 
-constexpr int kSigReadyDown = 0, kSigReadyUp = 1, kSigDoneDown = 2, kSigDoneUp = 3, kSigError = 7;
+constexpr int kSigReadyDown = 0, kSigReadyUp = 1, kSigDoneDown = 2, kSigDoneUp = 3;
+constexpr int kSigCount = 4, kSigEpoch = 5, kSigError = 7;
 constexpr long long kSpinCycles = 4LL << 30;  // ~2 s at 1.9 GHz: a lost neighbour is an error, not a hang
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
@@ -42,10 +45,23 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
 // Tell the neighbours "epoch e" in slot `slot_for_below` of the rank below's
 // block and `slot_for_above` of the rank above's, then wait until both
 // neighbours told this rank the same (slots own_a / own_b).  One thread.
+// e == 0: automatic epochs -- the "ready" handshake takes the next value of
+// this rank's device-side exchange counter, the "done" handshake reuses it
+// (every rank runs the same exchange sequence, so the counters agree; a
+// replayed CUDA graph advances them like eager calls).
 __global__ void handshake_kernel(ibc_slab_link L, uint64_t e, int slot_at_below, int slot_at_above,
-                                 int own_from_below, int own_from_above) {
+                                 int own_from_below, int own_from_above, int first) {
   pdl_wait();
   if (threadIdx.x != 0) return;
+  if (e == 0) {
+    if (first) {
+      e = L.d_sig[kSigCount] + 1;
+      L.d_sig[kSigCount] = e;
+      L.d_sig[kSigEpoch] = e;
+    } else {
+      e = L.d_sig[kSigEpoch];
+    }
+  }
   __threadfence_system();  // this rank's earlier writes (slab planes) before the flag
   if (L.has_down) st_release_sys(L.d_sig_down + slot_at_below, e);
   if (L.has_up) st_release_sys(L.d_sig_up + slot_at_above, e);
@@ -122,12 +138,13 @@ void slab_exchange(Context& ctx, const ibc_slab_link& L, uint64_t epoch, bool gh
   const unsigned blocks = (unsigned)ctx.sms * 4;
   // 1. "my planes are ready for epoch e" <-> the neighbours'.
   handshake_kernel<<<1, 32, 0, st>>>(L, epoch, kSigReadyUp, kSigReadyDown, kSigReadyDown,
-                                     kSigReadyUp);
+                                     kSigReadyUp, 1);
   // 2. pull.
   if (ghost_sum) ghost_add_kernel<<<blocks, 256, 0, st>>>(L);
   else halo_copy_kernel<<<blocks, 256, 0, st>>>(L);
   // 3. "done reading your planes": afterwards both sides may overwrite.
-  handshake_kernel<<<1, 32, 0, st>>>(L, epoch, kSigDoneUp, kSigDoneDown, kSigDoneDown, kSigDoneUp);
+  handshake_kernel<<<1, 32, 0, st>>>(L, epoch, kSigDoneUp, kSigDoneDown, kSigDoneDown, kSigDoneUp,
+                                     0);
   ctx.launches += 3;
   IBC_CUDA(cudaGetLastError());
 }

@@ -15,9 +15,17 @@ grid.
 * interpolate: a **halo fill** -- the two planes below the slab from the rank
   below, one plane above from the rank above -- then a local gather.
 
-These two exchanges are the only collective on the path (NCCL send/recv
-between ring neighbours; a ``gloo`` group stages through host memory, which is
-what the CPU tests use).  On a closed (non-periodic) axis the outer ghost
+These two exchanges are the only communication on the path.  Two transports:
+
+* ``"peer"`` (``PeerSlab``, the GPU default): the C ABI's peer-memory
+  exchange -- each rank's local slab and signal block are shared with its
+  ring neighbours through CUDA IPC handles (swapped once over the process
+  group), and ``ibc_slab_ghost_sum_device`` / ``ibc_slab_halo_fill_device``
+  pull the neighbours' planes over NVLink with device-side handshakes: no
+  NCCL, no host synchronisation, the whole step capturable in one CUDA graph;
+* ``"collective"``: torch.distributed send/recv between ring neighbours (NCCL
+  batch_isend_irecv; a ``gloo`` group stages through host memory, which is
+  what the CPU tests use).  On a closed (non-periodic) axis the outer ghost
 planes fall off the grid, exactly like the reference's dropped out-of-grid
 targets, and the outer halos are zero.
 
@@ -111,6 +119,7 @@ class SlabDecomposition:
         self._ops = ops
         self._spread = local_spread or self._device_spread
         self._interp = local_interpolate or self._device_interpolate
+        self.peer = None  # PeerSlab once use_peer_transport() is called
 
     # ---------------------------------------------------------- neighbours
     @property
@@ -184,6 +193,9 @@ class SlabDecomposition:
 
     def spread(self, points, values, out=None):
         """Points homed in this slab -> this rank's owned planes of the field."""
+        if self.peer is not None:
+            self._device_spread(points, values, out=self.peer.spread_buf)
+            return self.peer.ghost_sum()
         return self.ghost_sum(self._spread(points, values))
 
     # -------------------------------------------------------- interpolate
@@ -210,7 +222,25 @@ class SlabDecomposition:
         return L.reshape(-1)
 
     def interpolate(self, owned_field, points, out=None):
+        if self.peer is not None:
+            dst = self.peer.owned_field
+            if owned_field is not None and owned_field.data_ptr() != dst.data_ptr():
+                dst.copy_(owned_field.reshape(-1))
+            return self._device_interpolate(self.peer.halo_fill(), points, out=out)
         return self._interp(self.halo_fill(owned_field), points)
+
+    def use_peer_transport(self, group=None, peers=None) -> "PeerSlab":
+        """Switch this rank to the peer-memory exchange (PeerSlab): IPC over
+        `group`, or the in-process `peers` list (set each rank's
+        `.peer_slab` first, then call with peers=[...] on every rank)."""
+        ps = self.peer_slab if getattr(self, "peer_slab", None) else PeerSlab(self, self._device_ops())
+        self.peer_slab = ps
+        if peers is not None:
+            ps.connect_local(peers)
+        else:
+            ps.connect_ipc(group)
+        self.peer = ps
+        return ps
 
     # ---------------------------------------------------- device operators
     def _device_ops(self):
@@ -283,3 +313,146 @@ def owner_of_planes(planes, nz: int, world: int):
 
     b = torch.tensor(slab_bounds(nz, world)[1:-1], dtype=planes.dtype, device=planes.device)
     return torch.bucketize(planes.contiguous(), b, right=True)
+
+
+# ---------------------------------------------------------------- peer transport
+class _DeviceArray:
+    """__cuda_array_interface__ view of library-allocated device memory."""
+
+    def __init__(self, ptr: int, n: int, typestr: str = "<f8"):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerSlab:
+    """This rank's slab buffers, shared with its ring neighbours over peer
+    memory (include/ibcuda.h ibc_slab_link): `spread_buf` (the local spread
+    output, ghost-summed in place) and `field_buf` (the local interpolation
+    field, halo-filled in place), both nloc + 3 planes, plus a signal block.
+
+    Wire the neighbours with `connect_ipc(group)` (one process per rank:
+    CUDA IPC handles swapped over the process group) or `connect_local(peers)`
+    (ranks in one process).  Every rank then calls `ghost_sum()` /
+    `halo_fill()` in the same order; each is three kernels on the context
+    stream (asynchronous, graph-capturable)."""
+
+    def __init__(self, dec: "SlabDecomposition", ops):
+        import torch
+
+        self.dec, self.ops = dec, ops
+        lay = dec.lay
+        self.count = lay.local_planes * lay.plane
+        lib = load()
+        self._ptrs = []
+        for _ in range(2):
+            ptr = C.c_void_p()
+            check(lib.ibc_device_alloc(ops.context.handle, self.count * 8, C.byref(ptr)))
+            self._ptrs.append(ptr.value)
+        sig = C.c_void_p()
+        check(lib.ibc_slab_signals_create(ops.context.handle, C.byref(sig)))
+        self._sig = sig.value
+        dev = torch.device("cuda", ops.device)
+        self.spread_buf = torch.as_tensor(_DeviceArray(self._ptrs[0], self.count), device=dev)
+        self.field_buf = torch.as_tensor(_DeviceArray(self._ptrs[1], self.count), device=dev)
+        self.field_buf.zero_()
+        self._opened = []
+        self._links = None
+
+    def _link(self, which: int, down, up) -> _capi.IbcSlabLink:
+        lay = self.dec.lay
+        L = _capi.IbcSlabLink()
+        L.nloc = lay.nloc
+        L.nloc_down = down[3]
+        L.plane = lay.plane
+        L.has_down = int(self.dec._has_down())
+        L.has_up = int(self.dec._has_up())
+        L.d_local = self._ptrs[which]
+        L.d_down = down[which]
+        L.d_up = up[which]
+        L.d_sig = self._sig
+        L.d_sig_down = down[2]
+        L.d_sig_up = up[2]
+        return L
+
+    def _wire(self, down, up):
+        """down / up: (spread_ptr, field_ptr, sig_ptr, nloc) of the neighbours."""
+        self._links = [self._link(0, down, up), self._link(1, down, up)]
+
+    def describe(self):
+        return (self._ptrs[0], self._ptrs[1], self._sig, self.dec.lay.nloc)
+
+    def connect_local(self, peers) -> None:
+        """Ranks in one process: peers[r] is rank r's PeerSlab."""
+        self._wire(peers[self.dec.down].describe(), peers[self.dec.up].describe())
+
+    def connect_ipc(self, group=None) -> None:
+        """One process per rank: swap IPC handles over the process group."""
+        import torch.distributed as dist
+
+        lib, h = load(), self.ops.context.handle
+        mine = []
+        for ptr in (*self._ptrs, self._sig):
+            hd = _capi.IbcIpcHandle()
+            check(lib.ibc_ipc_get_handle(h, C.c_void_p(ptr), C.byref(hd)))
+            mine.append(bytes(hd.bytes))
+        allh = [None] * self.dec.lay.world
+        dist.all_gather_object(allh, (mine, self.dec.lay.nloc), group=group)
+        opened = {}
+
+        def peer(r):
+            if r == self.dec.lay.rank:
+                return self.describe()
+            if r not in opened:
+                ptrs = []
+                for raw in allh[r][0]:
+                    hd = _capi.IbcIpcHandle()
+                    C.memmove(hd.bytes, raw, 64)
+                    out = C.c_void_p()
+                    check(lib.ibc_ipc_open_handle(h, C.byref(hd), C.byref(out)))
+                    ptrs.append(out.value)
+                    self._opened.append(out.value)
+                opened[r] = (*ptrs, allh[r][1])
+            return opened[r]
+
+        self._wire(peer(self.dec.down), peer(self.dec.up))
+
+    def _exchange(self, fn, which):
+        if self._links is None:
+            raise RuntimeError("PeerSlab is not connected (connect_ipc / connect_local)")
+        self.ops._sync_stream()
+        # epoch 0: the device-side counter -- correct under CUDA graph replay
+        check(fn(self.ops.context.handle, C.byref(self._links[which]), 0))
+
+    def ghost_sum(self):
+        """spread_buf: local spread output -> its owned planes ghost-summed."""
+        self._exchange(load().ibc_slab_ghost_sum_device, 0)
+        lay = self.dec.lay
+        return self.spread_buf[2 * lay.plane:(lay.nloc + 2) * lay.plane]
+
+    def halo_fill(self):
+        """field_buf: owned planes (written by the caller) -> halos filled."""
+        self._exchange(load().ibc_slab_halo_fill_device, 1)
+        return self.field_buf
+
+    @property
+    def owned_field(self):
+        """The owned planes of field_buf (write the rank's field here)."""
+        lay = self.dec.lay
+        return self.field_buf[2 * lay.plane:(lay.nloc + 2) * lay.plane]
+
+    def timed_out(self) -> bool:
+        flag = C.c_int()
+        check(load().ibc_slab_link_error(self.ops.context.handle, C.byref(self._links[0]),
+                                         C.byref(flag)))
+        return bool(flag.value)
+
+    def close(self) -> None:
+        lib = load()
+        h = getattr(self.ops, "context", None)
+        if h is None or not getattr(self, "_ptrs", None):
+            return
+        for p in self._opened:
+            lib.ibc_ipc_close_handle(h.handle, C.c_void_p(p))
+        for p in (*self._ptrs, self._sig):
+            lib.ibc_device_free(h.handle, C.c_void_p(p))
+        self._ptrs, self._opened = [], []

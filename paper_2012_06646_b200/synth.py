@@ -166,12 +166,14 @@ def survey_config(name: str, seed_offset: int = 0):
                 field=uniform_pm1(N ** 3, 4 + seed_offset))
 
 
-def slab_config(rank: int, world: int):
-    """Weak-scaling multi-GPU workload (BASELINE config 2 per GPU): a global
-    256 x 256 x 256*world periodic grid split in z-slabs of 256 planes; rank r
-    holds 2^20 points homed in its slab (uniform in x, y and in its planes,
-    kept 0.15 h inside the slab so X* = X^n + U[-0.1h, 0.1h] stays homed)."""
-    n, N, edge = 1 << 20, 256, 16e-4
+def slab_config(rank: int, world: int, n: int = 1 << 20):
+    """Weak-scaling multi-GPU workload: a global 256 x 256 x 256*world periodic
+    grid split in z-slabs of 256 planes; rank r holds n points homed in its
+    slab (uniform in x, y and in its planes, kept 0.15 h inside the slab so
+    X* = X^n + U[-0.1h, 0.1h] stays homed).  n = 2^20: BASELINE config 2 per
+    GPU; n = 256^3: config 3's constant-load level, 1 point per cell
+    (SURVEY 8(d) W, 16.8 M cells and points per GPU)."""
+    N, edge = 256, 16e-4
     h = edge / N
     z0, z1 = N * rank, N * (rank + 1)
     u = MT19937_64(1 + 1000 * rank).next_unit(3 * n).reshape(n, 3)

@@ -202,3 +202,119 @@ def test_cpp_multi_rank_peer_exchange():
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "slab ok" in out.stdout
+
+
+def _peer_case(R, periodic, seed):
+    ext, h = (32, 24, 8 * R), 0.5
+    rng = np.random.default_rng(seed)
+    n = 5000
+    zlo, zhi = ((-ext[2] * h, 2 * ext[2] * h) if periodic else (2.0 * h, (ext[2] - 2) * h))
+    pts = np.stack([rng.uniform(0, ext[0] * h, n), rng.uniform(0, ext[1] * h, n),
+                    rng.uniform(zlo, zhi, n)], axis=1)
+    vals = rng.uniform(-1, 1, n)
+    field = rng.uniform(-1, 1, int(np.prod(ext)))
+    per = (True, True, periodic)
+    grid = ib.StaggeredGrid(list(ext), h, [0.5, 0.5, 0.0], list(per))
+    og = O.make_grid(list(ext), h, [0.5, 0.5, 0.0], list(per))
+    return grid, og, pts, vals, field
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("R,periodic", [(1, True), (2, True), (2, False), (3, True), (3, False)])
+def test_peer_transport_in_process(R, periodic):
+    """PeerSlab with ranks in one process (own contexts and streams, peers
+    wired directly): spread + peer ghost sum, halo fill + gather, vs the
+    single-grid oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2012_06646_b200.device import DeviceOperators
+
+    grid, og, pts, vals, field = _peer_case(R, periodic, 40 + R)
+    X = torch.tensor(pts, device="cuda")
+    planes = S.home_planes(grid, X)
+    owner = S.owner_of_planes(planes, grid.extents[-1], R)
+    decs, streams, parts = [], [], []
+    for r in range(R):
+        ops = DeviceOperators(0)
+        decs.append(S.SlabDecomposition(grid, r, R, ops=ops))
+        streams.append(torch.cuda.Stream())
+        m = owner == r
+        parts.append((m.cpu().numpy(), X[m].contiguous(),
+                      torch.tensor(vals, device="cuda")[m].contiguous()))
+    for r in range(R):  # warm-up: size every context's scratch before any handshake
+        with torch.cuda.stream(streams[r]):
+            decs[r]._device_spread(parts[r][1], parts[r][2])
+            decs[r]._device_interpolate(torch.zeros(decs[r].local.point_count(), dtype=torch.float64,
+                                                    device="cuda"), parts[r][1])
+    torch.cuda.synchronize()
+    slabs = []
+    for d in decs:
+        d.peer_slab = S.PeerSlab(d, d._device_ops())
+        slabs.append(d.peer_slab)
+    for d in decs:
+        d.use_peer_transport(peers=slabs)
+    owned, E = [], []
+    for r in range(R):
+        with torch.cuda.stream(streams[r]):
+            owned.append(decs[r].spread(parts[r][1], parts[r][2]))
+    for r in range(R):
+        lay = decs[r].lay
+        with torch.cuda.stream(streams[r]):
+            own_f = torch.tensor(field[lay.z0 * lay.plane:lay.z1 * lay.plane], device="cuda")
+            E.append(decs[r].interpolate(own_f, parts[r][1]))
+    torch.cuda.synchronize()
+    want = O.spread_serial(og, pts, vals)
+    want_e = O.interpolate(og, field, pts)
+    for r in range(R):
+        lay = decs[r].lay
+        assert not slabs[r].timed_out()
+        dev = O.max_rel_deviation(owned[r].cpu().numpy(), want[lay.z0 * lay.plane:lay.z1 * lay.plane])
+        assert dev <= TOL, (r, dev)
+        assert O.max_rel_deviation(E[r].cpu().numpy(), want_e[parts[r][0]]) <= TOL
+    for s_ in slabs:
+        s_.close()
+
+
+def _peer_worker(rank, world, port, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        grid, og, pts, vals, field = _peer_case(world, True, 77)
+        dec = S.SlabDecomposition(grid, rank, world)
+        X = torch.tensor(pts, device="cuda")
+        mine = S.owner_of_planes(S.home_planes(grid, X), grid.extents[-1], world) == rank
+        xm, vm = X[mine].contiguous(), torch.tensor(vals, device="cuda")[mine].contiguous()
+        dec._device_spread(xm, vm)  # warm-up before any handshake
+        dec._device_interpolate(torch.zeros(dec.local.point_count(), dtype=torch.float64,
+                                            device="cuda"), xm)
+        torch.cuda.synchronize()
+        dist.barrier()
+        dec.use_peer_transport()  # CUDA IPC handles swapped over the gloo group
+        dist.barrier()
+        lay = dec.lay
+        own = dec.spread(xm, vm)
+        e = dec.interpolate(torch.tensor(field[lay.z0 * lay.plane:lay.z1 * lay.plane], device="cuda"), xm)
+        torch.cuda.synchronize()
+        assert not dec.peer.timed_out(), "handshake timed out"
+        dev = O.max_rel_deviation(own.cpu().numpy(),
+                                  O.spread_serial(og, pts, vals)[lay.z0 * lay.plane:lay.z1 * lay.plane])
+        assert dev <= TOL, f"rank {rank} spread dev {dev}"
+        dev = O.max_rel_deviation(e.cpu().numpy(), O.interpolate(og, field, pts)[mine.cpu().numpy()])
+        assert dev <= TOL, f"rank {rank} interp dev {dev}"
+        dist.barrier()
+        dec.peer.close()
+        dist.destroy_process_group()
+    except BaseException as exc:  # pragma: no cover
+        errq.put(f"rank {rank}: {exc!r}")
+
+
+@pytest.mark.gpu
+def test_peer_transport_two_processes_ipc():
+    """Two processes, CUDA IPC peer pointers (the multi-GPU setup, here on
+    one device)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    _spawn(_peer_worker, 2)
