@@ -242,6 +242,56 @@ class SlabDecomposition:
         self.peer = ps
         return ps
 
+    # ---------------------------------------------------------- migration
+    def migrate(self, points, *payloads, planes=None):
+        """Per-step point migration between ring neighbours (SURVEY 2 K7,
+        8(e)): points whose home plane left [z0, z1) go to the rank that owns
+        it now -- a neighbour, since IB points move far less than a cell per
+        step.  `planes`: the points' wrapped home planes on the
+        global grid (default: `home_planes` on the device; injectable for CPU
+        checks).  Returns (points, *payloads) of this rank after the move:
+        the staying points in their order, then those from the rank below,
+        then those from the rank above.  Counts go first, then the packed
+        rows, over the same neighbour send/recv as the exchanges."""
+        import torch
+
+        lay = self.lay
+        if planes is None:
+            planes = home_planes(self.grid, points, self._device_ops())
+        owner = owner_of_planes(planes.to(torch.int64), lay.nz, lay.world)
+        stay = owner == lay.rank
+        to_down = (owner == self.down) & ~stay
+        to_up = (owner == self.up) & ~stay & ~to_down
+        if bool((~(stay | to_down | to_up)).any()):
+            raise ValueError("a point moved past a neighbouring slab in one step")
+        cols = [points.reshape(points.shape[0], -1)] + [p.reshape(p.shape[0], -1) for p in payloads]
+        widths = [c.shape[1] for c in cols]
+        rows = torch.cat([c.to(torch.float64) for c in cols], dim=1)
+        send_down, send_up = rows[to_down], rows[to_up]
+        cnt_from_up, cnt_from_down = self._exchange(
+            torch.tensor([send_down.shape[0]], dtype=torch.float64, device=rows.device),
+            torch.tensor([send_up.shape[0]], dtype=torch.float64, device=rows.device), (1,), (1,))
+        W = rows.shape[1]
+        n_up = int(cnt_from_up.item()) if cnt_from_up is not None else 0
+        n_down = int(cnt_from_down.item()) if cnt_from_down is not None else 0
+        # Empty messages still travel (every rank posts the same operations).
+        pad = lambda t: t if t.shape[0] else torch.zeros((1, W), dtype=t.dtype, device=t.device)
+        from_up, from_down = self._exchange(pad(send_down), pad(send_up), (max(n_up, 1), W),
+                                            (max(n_down, 1), W))
+        parts = [rows[stay]]
+        if from_down is not None and n_down:
+            parts.append(from_down[:n_down])
+        if from_up is not None and n_up:
+            parts.append(from_up[:n_up])
+        new = torch.cat(parts, dim=0)
+        out, c0 = [], 0
+        for c, w in zip(cols, widths):
+            out.append(new[:, c0:c0 + w].to(c.dtype).reshape((-1,) + tuple(c.shape[1:]))
+                       if w > 1 else new[:, c0].to(c.dtype))
+            c0 += w
+        out[0] = out[0].reshape(-1, points.shape[1]).contiguous()
+        return tuple(o.contiguous() for o in out)
+
     # ---------------------------------------------------- device operators
     def _device_ops(self):
         if self._ops is None:

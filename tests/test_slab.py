@@ -318,3 +318,43 @@ def test_peer_transport_two_processes_ipc():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     _spawn(_peer_worker, 2)
+
+
+def _migrate_worker(rank, world, port, errq):
+    try:
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        ext, h = (8, 6, 12 * world), 0.5
+        grid = ib.StaggeredGrid(list(ext), h, [0.5, 0.5, 0.0], [True] * 3)
+        og = O.make_grid(list(ext), h, [0.5, 0.5, 0.0], [1, 1, 1])
+        rng = np.random.default_rng(100)
+        n = 3000
+        pts = np.stack([rng.uniform(0, ext[a] * h, n) for a in range(3)], axis=1)
+        moved = pts + rng.uniform(-1.5 * h, 1.5 * h, pts.shape)  # up to 1.5 cells per step
+        ids = np.arange(n, dtype=np.float64)
+        dec = S.SlabDecomposition(grid, rank, world)
+        lay = dec.lay
+        owner0 = S.owner_of_planes(torch.tensor(O.home_cells(og, pts)[:, 2]), ext[2], world)
+        mine = (owner0 == rank).numpy()
+        # this rank's points (old slab), at their new positions
+        X = torch.tensor(moved[mine])
+        planes = torch.tensor(O.home_cells(og, moved[mine])[:, 2])
+        Xn, idn = dec.migrate(X, torch.tensor(ids[mine]), planes=planes)
+        owner1 = S.owner_of_planes(torch.tensor(O.home_cells(og, moved)[:, 2]), ext[2], world).numpy()
+        want = set(np.nonzero(owner1 == rank)[0].tolist())
+        got = idn.numpy().astype(np.int64)
+        assert sorted(got.tolist()) == sorted(want), f"rank {rank}: wrong set after migration"
+        assert np.array_equal(Xn.numpy(), moved[got]), f"rank {rank}: rows scrambled"
+        # the staying points first, in their order
+        stay = [i for i in np.nonzero(mine)[0] if owner1[i] == rank]
+        assert got[:len(stay)].tolist() == stay
+        dist.destroy_process_group()
+    except BaseException as exc:  # pragma: no cover
+        errq.put(f"rank {rank}: {exc!r}")
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_point_migration_between_neighbour_slabs(world):
+    _spawn(_migrate_worker, world)
