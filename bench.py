@@ -94,7 +94,8 @@ def physical_cores() -> int | None:
             with open(base + "core_id") as f:
                 core = f.read().strip()
             cores.add((pkg, core))
-        return len(cores) or None
+        # A VM that exposes no core topology reports every CPU as core 0.
+        return len(cores) if len(cores) > 1 or len(cpus) == 1 else None
     except Exception:
         return None
 
