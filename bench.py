@@ -619,16 +619,18 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            import oracle as O
+        # The reference arm in a child process (its OpenMP team pinned there),
+        # a bounded sample of the same workload.
+        import subprocess
 
-            if O.ref_available():
-                threads = host_threads()
-                t = cpu_reference_steps(data, 2, 1, threads)
-                cpu = {"value": n / float(statistics.median(t)), "unit": UNIT, "cores": threads,
-                       "physical_cores": physical_cores(), "kind": "reference",
-                       "sample": f"2 full {args.workload} steps (ib::spread_fused + ib::interpolate, "
-                                 "oracle/_ref, OpenMP) after 1 warm-up, median"}
+        try:
+            r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference",
+                                "--workload", args.workload, "--steps", "2", "--warmup", "1",
+                                "--no-serial"], capture_output=True, text=True, timeout=900)
+            ref = json.loads(r.stdout.strip().splitlines()[-1])
+            cpu = dict(ref["cpu_baseline"])
+            cpu["sample"] = f"2 full {args.workload} steps (ib::spread_fused + ib::interpolate, " \
+                            "oracle/_ref, OpenMP) after 1 warm-up, median, in a child process"
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "reference",
                    "sample": f"failed: {exc}"}
@@ -667,11 +669,14 @@ def run_ours(args):
 
 
 def main():
-    omp_env()  # before libgomp / torch initialise their thread pools
     args = parse()
     if args.impl == "reference":
+        omp_env()  # before libgomp initialises: the reference's OpenMP team, pinned to cores
         run_reference(args)
     else:
+        # Not pinned: OMP_PROC_BIND would bind this process's main thread (and
+        # every host thread it starts: the e2e callers, the staging copies) to
+        # one core.  The in-run CPU baseline runs in its own process.
         run_ours(args)
 
 

@@ -16,7 +16,7 @@ HEADERS = ["ibc_device.cuh", "ibc_sort.cuh", "ibc_internal.h", "ibc_sweep.cuh", 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-Xcompiler", "-fopenmp", "-shared", "-lgomp",
+    "-Xcompiler", "-fPIC", "-shared",
 ]
 
 

@@ -13,6 +13,10 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <vector>
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -128,15 +132,94 @@ bool is_pinned(const void* p) {
   return a.type != cudaMemoryTypeUnregistered;
 }
 
-// Host memcpy over the OpenMP team (one pageable <-> pinned stage piece).
-void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  constexpr size_t kSlice = size_t{1} << 20;
-  const long slices = (long)((bytes + kSlice - 1) / kSlice);
-#pragma omp parallel for schedule(static)
-  for (long i = 0; i < slices; ++i) {
-    const size_t o = (size_t)i * kSlice, b = bytes - o < kSlice ? bytes - o : kSlice;
-    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, b);
+// Host memcpy split over a small pool of host threads (one pageable <->
+// pinned stage piece).  Plain std::thread: the library does not pull an
+// OpenMP runtime into its callers' processes.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
   }
+  void copy(void* dst, const void* src, size_t bytes) {
+    constexpr size_t kSlice = size_t{1} << 20;
+    const size_t slices = (bytes + kSlice - 1) / kSlice;
+    if (slices <= 1 || workers_.empty()) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::unique_lock<std::mutex> lock(call_mu_);  // one pageable copy at a time uses the pool
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      next_ = 0;
+      slices_ = slices;
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();  // the caller helps
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return done_ == slices_; });
+  }
+
+ private:
+  CopyPool() {
+    unsigned n = std::thread::hardware_concurrency();
+    n = n > 8 ? 8 : n;
+    for (unsigned i = 1; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  void work() {
+    constexpr size_t kSlice = size_t{1} << 20;
+    for (;;) {
+      size_t i;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (next_ >= slices_) return;
+        i = next_++;
+      }
+      const size_t o = i * kSlice, b = bytes_ - o < kSlice ? bytes_ - o : kSlice;
+      std::memcpy(dst_ + o, src_ + o, b);
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (++done_ == slices_) done_cv_.notify_all();
+      }
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0, next_ = 0, slices_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  CopyPool::get().copy(dst, src, bytes);
 }
 
 // Host <-> device copy of a host-buffer call, in 8 MiB pieces.  A copy
