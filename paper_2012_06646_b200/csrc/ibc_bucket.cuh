@@ -385,9 +385,34 @@ __global__ void __launch_bounds__(kThreads) row_sort_kernel(
   if (mode == 0) write_record_from<D>(g, x, gv, a + rk, rec, rcx);
 }
 
-// K4b, long rows: one CTA per listed row, bitonic sort of (key << 32 | index)
-// in shared memory (rows up to kLongSortMax; longer rows rank by counting).
+// Bitonic sort of m (a power of two) 64-bit words in shared memory, one CTA.
 constexpr int kLongThreads = 1024;
+__device__ __forceinline__ void cta_bitonic(unsigned long long* sk, uint32_t m) {
+  for (uint32_t size = 2; size <= m; size <<= 1) {
+    for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
+      for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
+        const uint32_t p = e ^ stride;
+        if (p > e) {
+          const bool up = (e & size) == 0;
+          const unsigned long long x = sk[e], y = sk[p];
+          if ((x > y) == up) {
+            sk[e] = y;
+            sk[p] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// K4b, long rows: one CTA per listed row sorts its (key << 32 | index) pairs
+// (all distinct: the index is unique).  Rows up to kLongSortMax: a bitonic
+// sort in shared memory.  Longer rows (a fibre along x, a cluster in one row):
+// kLongSortMax-chunks sorted the same way, then merged pairwise through
+// global memory (`tmp`, n words) -- each element's place in the merged run is
+// its index in its own run plus its rank in the partner run (binary search),
+// O(len log len) per pass instead of the O(len^2) ranking by counting.
 template <int D>
 __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     const uint32_t* __restrict__ start, const uint32_t* __restrict__ long_rows,
@@ -395,7 +420,8 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
     uint32_t* __restrict__ skey, uint32_t* __restrict__ sidx,
     DevGrid g, const double* __restrict__ X, const double* __restrict__ G,
     double* __restrict__ rec, int* __restrict__ rcx, const uint32_t* __restrict__ maxrow,
-    uint32_t bank_rows, int mode) {
+    uint32_t bank_rows, int mode, unsigned long long* __restrict__ tmp0,
+    unsigned long long* __restrict__ tmp1) {
   pdl_wait();
   extern __shared__ unsigned long long sk[];  // [kLongSortMax] (key << 32 | index)
   if (mode == 0 && bank_mode(maxrow, bank_rows)) return;
@@ -403,46 +429,57 @@ __global__ void __launch_bounds__(kLongThreads) long_row_sort_kernel(
   for (uint32_t li = blockIdx.x; li < count; li += gridDim.x) {
     const uint32_t r = long_rows[li];
     const uint32_t a = start[(size_t)r * kBanks], len = start[(size_t)r * kBanks + kBanks] - a;
+    const unsigned long long* sorted;
     if (len <= (uint32_t)kLongSortMax) {
       uint32_t m = 1;
       while (m < len) m <<= 1;
-      for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
-        sk[e] = e < len ? bpair[a + e] : ~0ull;
-      }
+      for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) sk[e] = e < len ? bpair[a + e] : ~0ull;
       __syncthreads();
-      for (uint32_t size = 2; size <= m; size <<= 1) {
-        for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-          for (uint32_t e = threadIdx.x; e < m; e += kLongThreads) {
-            const uint32_t p = e ^ stride;
-            if (p > e) {
-              const bool up = (e & size) == 0;
-              const unsigned long long x = sk[e], y = sk[p];
-              if ((x > y) == up) {
-                sk[e] = y;
-                sk[p] = x;
-              }
-            }
-          }
-          __syncthreads();
-        }
-      }
-      for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
-        skey[a + e] = (uint32_t)(sk[e] >> 32);
-        sidx[a + e] = (uint32_t)sk[e];
-        if (mode == 0) write_record<D>(g, X, G, (uint32_t)sk[e], a + e, rec, rcx);
-      }
-      __syncthreads();
+      cta_bitonic(sk, m);
+      sorted = sk;
     } else {
-      // Very long row: rank every element by counting (correct, quadratic).
-      for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
-        const unsigned long long ce = bpair[a + e];
-        uint32_t rk = 0;
-        for (uint32_t f = 0; f < len; ++f) rk += bpair[a + f] < ce ? 1u : 0u;
-        skey[a + rk] = (uint32_t)(ce >> 32);
-        sidx[a + rk] = (uint32_t)ce;
-        if (mode == 0) write_record<D>(g, X, G, (uint32_t)ce, a + rk, rec, rcx);
+      // Sorted chunks into tmp0[a ..], then merge passes tmp0 <-> tmp1.
+      for (uint32_t c0 = 0; c0 < len; c0 += kLongSortMax) {
+        const uint32_t cl = min((uint32_t)kLongSortMax, len - c0);
+        for (uint32_t e = threadIdx.x; e < (uint32_t)kLongSortMax; e += kLongThreads)
+          sk[e] = e < cl ? bpair[a + c0 + e] : ~0ull;
+        __syncthreads();
+        cta_bitonic(sk, kLongSortMax);
+        for (uint32_t e = threadIdx.x; e < cl; e += kLongThreads) tmp0[a + c0 + e] = sk[e];
+        __syncthreads();
       }
+      unsigned long long* src = tmp0 + a;
+      unsigned long long* dst = tmp1 + a;
+      for (uint32_t w = kLongSortMax; w < len; w <<= 1) {
+        for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
+          const uint32_t run = e / (2 * w), lo = run * 2 * w, mid = min(lo + w, len),
+                         hi = min(lo + 2 * w, len);
+          const unsigned long long v = src[e];
+          // partner run [plo, phi): elements of it below v
+          const bool left = e < mid;
+          uint32_t plo = left ? mid : lo, phi = left ? hi : mid, lo_b = plo, hi_b = phi;
+          while (lo_b < hi_b) {
+            const uint32_t mm = (lo_b + hi_b) >> 1;
+            if (src[mm] < v) lo_b = mm + 1;
+            else hi_b = mm;
+          }
+          const uint32_t own = e - (left ? lo : mid);
+          dst[lo + own + (lo_b - plo)] = v;
+        }
+        __syncthreads();
+        unsigned long long* t = src;
+        src = dst;
+        dst = t;
+      }
+      sorted = src;
     }
+    for (uint32_t e = threadIdx.x; e < len; e += kLongThreads) {
+      const unsigned long long v = sorted[e];
+      skey[a + e] = (uint32_t)(v >> 32);
+      sidx[a + e] = (uint32_t)v;
+      if (mode == 0) write_record<D>(g, X, G, (uint32_t)v, a + e, rec, rcx);
+    }
+    __syncthreads();
   }
 }
 

@@ -57,6 +57,8 @@ struct PointScratch {
   DevBuf<uint32_t> rowstart;
   DevBuf<uint32_t> rowaux;  // bucket sort: row counts | scan status | ticket | long rows
   DevBuf<unsigned long long> bpair;  // bucket sort: (key << 32 | index) in row buckets
+  DevBuf<unsigned long long> bpair_tmp;  // merge passes of rows longer than kLongSortMax
+  size_t bpair_tmp_half = 0;
   const uint32_t* maxrow = nullptr;  // bucket sort: largest row count (device)
   uint32_t bank_rows = 0;            // spread: bank-mode row threshold (bucket::bank_mode)
   bool obs_pending = false;          // spread: ws.keys / ws.perm not materialised yet

@@ -649,6 +649,7 @@ void PointScratch::release_all() {
   hist.release(); base.release(); counters.release(); rowstart.release();
   rec_cx.release(); rec.release(); run_keys.release(); block_counts.release(); rowaux.release();
   bpair.release();
+  bpair_tmp.release();
   prim_u32.release();
   prim_bytes.release();
   cap = 0;
@@ -930,7 +931,8 @@ void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
     pdl_launch(long_k, (unsigned)ctx.sms, bucket::kLongThreads, lsm, st, s.rowstart.p, long_rows, nlong, s.bpair.p,
                                                    s.keys[0].p, s.vals[0].p, g, d_points,
                                                    d_values, s.rec.p, s.rec_cx.p, maxrow,
-                                                   s.bank_rows, mode);
+                                                   s.bank_rows, mode, s.bpair_tmp.p,
+                                                   s.bpair_tmp.p + s.bpair_tmp_half);
   };
   if (g.dim == 3) sorts(bucket::row_sort_kernel<3>, bucket::long_row_sort_kernel<3>);
   else sorts(bucket::row_sort_kernel<2>, bucket::long_row_sort_kernel<2>);
@@ -1005,6 +1007,9 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
     s.last_n = 0;  // interpolation leaves no observable sort
   } else {
     s.bpair.ensure(n);
+    // merge space of the very long rows (long_row_sort_kernel): 2 x n words
+    s.bpair_tmp.ensure(2 * n);
+    s.bpair_tmp_half = n;
     launch_scatter_spread(ctx, g, n, s);
     // Records: in (row, x bank) buckets (bank mode) or the rows' key order
     // (pull mode, K4b for the long rows; it exits at once in bank mode).

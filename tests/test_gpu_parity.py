@@ -501,3 +501,23 @@ def test_concurrent_host_calls_from_threads_match_serial():
         assert np.array_equal(a, b)
     for a, b in zip(got_i, want_i):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("path", ["auto", "pull"])
+def test_very_long_row_merge_sort(path):
+    # one cell row holding 40000 points (> kLongSortMax = 8192: chunked bitonic
+    # sorts + three merge passes), next to ordinary rows; ws.keys / ws.perm
+    # bit-exact, the spread within 1e-12 (pull mode sorts it inside the spread)
+    rng = np.random.default_rng(19)
+    g = ib.StaggeredGrid([64, 20, 16], 1.0, [0.5, 0.5, 0.0], [True] * 3)
+    row = np.stack([rng.uniform(0, 64, 40000), 7.6 + rng.uniform(-0.3, 0.3, 40000),
+                    4.2 + rng.uniform(-0.3, 0.3, 40000)], axis=1)
+    pts = np.concatenate([row, rand_points(g, 3000, rng)])
+    vals = rng.uniform(-1, 1, len(pts))
+    ctx = ib.Context(0)
+    ctx.set_spread_path(path)
+    ws = ib.SpreadWorkspace(len(pts), g, context=ctx)
+    got = ib.spread_fused(pts, vals, g, K, ws, 8)
+    _, keys, perm, _ = O.spread_fused(og(g), pts, vals)
+    assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm)
+    assert O.max_rel_deviation(got.values, O.spread_serial(og(g), pts, vals)) <= TOL
