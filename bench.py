@@ -313,7 +313,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     from paper_2012_06646_b200 import ib, synth
-    from paper_2012_06646_b200.device import DeviceOperators
+    from paper_2012_06646_b200.device import DeviceOperators, capture_graph
     from paper_2012_06646_b200.slab import SlabDecomposition
 
     world, rank, local = dist_env()
@@ -428,9 +428,7 @@ def run_ours(args):
     # graph and replayed (the pipeline has no host round trip).
     if not args.no_graph:
         for k, f in enumerate(local_ops):
-            graphs[k] = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graphs[k]):
-                f()
+            graphs[k] = capture_graph(f)
         step()
         torch.cuda.synchronize()
     graph = graphs[0]
@@ -592,9 +590,7 @@ def run_ours(args):
         torch.cuda.synchronize()
         mgraph = None
         if not args.no_graph:
-            mgraph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(mgraph):
-                loop.step()
+            mgraph = capture_graph(loop.step)
             mgraph.replay()
             torch.cuda.synchronize()
         mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))

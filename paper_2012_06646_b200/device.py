@@ -14,6 +14,32 @@ from ._capi import InvalidArgument, check, load
 from .ib import Context, CosineKernel, SpreadWorkspace, StaggeredGrid, _kernel_code
 
 
+def capture_graph(fn, graph=None):
+    """Capture fn() into a CUDA graph with Python's garbage collector paused.
+
+    The library's Python objects (contexts, workspaces, binnings) free device
+    memory when collected; a collection that happens to run inside a capture
+    would call cudaFree, which is not capturable, and invalidate the whole
+    capture.  Collect first, then keep the collector off until the capture
+    ends."""
+    import gc
+
+    import torch
+
+    graph = graph if graph is not None else torch.cuda.CUDAGraph()
+    gc.collect()
+    torch.cuda.synchronize()
+    enabled = gc.isenabled()
+    gc.disable()
+    try:
+        with torch.cuda.graph(graph):
+            fn()
+    finally:
+        if enabled:
+            gc.enable()
+    return graph
+
+
 def _ptr(t) -> C.c_void_p:
     return C.c_void_p(int(t.data_ptr()))
 

@@ -368,9 +368,9 @@ def test_cuda_graph_replay_matches_eager():
     step()
     torch.cuda.synchronize()
     ref_ell, ref_E = ell.clone(), E.clone()
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        step()
+    from paper_2012_06646_b200.device import capture_graph
+
+    graph = capture_graph(step)
     ell.zero_()
     E.zero_()
     graph.replay()

@@ -87,9 +87,9 @@ def test_mac_step_loop_graph_replay_matches_eager():
     loop.step()  # warm-up (allocations, kernel attributes) ...
     torch.cuda.synchronize()
     loop.X.copy_(loop.anchors)  # ... then back to the initial state
-    graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
-        loop.step()
+    from paper_2012_06646_b200.device import capture_graph
+
+    graph = capture_graph(loop.step)
     for _ in range(3):
         graph.replay()
     torch.cuda.synchronize()
