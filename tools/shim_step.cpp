@@ -6,7 +6,10 @@
 // host threads (the reference's threading contract allows concurrent calls on
 // disjoint outputs), so the spread's grid copy-out overlaps the
 // interpolation's field copy-in.
-//   shim_step N n reps [concurrent]   -> "step_s_median <s> min <s> ..."
+//   shim_step N n reps [concurrent [heap]]   -> "step_s_median <s> min <s> ..."
+//   heap = 1: glibc keeps large blocks on the heap (mallopt), see main().
+#include <malloc.h>
+
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
@@ -28,6 +31,14 @@ int main(int argc, char** argv) {
     return 77;
   }
   ibc_context_destroy(probe);
+  // Caller-side tuning (glibc): keep large blocks on the heap instead of a
+  // fresh mmap per allocation, so the 134 MB GridField each spread returns
+  // (spread.hpp:180, by value) reuses pages instead of faulting them in
+  // again -- the reference's own callers pay the same construction.
+  if (argc > 5 && std::atoi(argv[5]) != 0) {
+    mallopt(M_MMAP_THRESHOLD, 1 << 30);
+    mallopt(M_TRIM_THRESHOLD, 1 << 30);
+  }
   const int N = std::atoi(argv[1]);
   const std::size_t n = std::strtoull(argv[2], nullptr, 10);
   const int reps = std::atoi(argv[3]);
