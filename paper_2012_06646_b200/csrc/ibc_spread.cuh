@@ -41,6 +41,9 @@ namespace sp {
 
 constexpr int kPadL = 4;  // padded x index xi = x + kPadL
 constexpr uint32_t kPullRow = 64;  // densest row above which batches pull instead of bank mode
+// Bank-mode lists at least this long (per lane and source plane) take the
+// paired loop of plane_banks.
+constexpr uint32_t kPairMin = 12;
 constexpr int kPadR = 2;
 
 struct SweepTiling {
@@ -95,6 +98,82 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
     const int j = (k >= c[0]) + (k >= c[1]) + (k >= c[2]);
     return (j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3]) + k;
   };
+  // y / z weights of a record: phi(sigma_y - t_y)/h for its source row j
+  // (j = 0..3 -> (1-c), (1+s), (1+c), (1-s) over 4h) times the four z weights.
+  auto weights = [&](const double4& gbr, int j, double a[4]) {
+    const double vy = (j & 1) ? gbr.x : gbr.y;
+    const double wq = q * fma((j == 0 || j == 3) ? -q : q, vy, q);  // wy * q
+    if (D == 3) {
+      a[0] = fma(-wq, gbr.w, wq);
+      a[1] = fma(wq, gbr.z, wq);
+      a[2] = fma(wq, gbr.w, wq);
+      a[3] = fma(-wq, gbr.z, wq);
+    } else {
+      a[0] = a[1] = a[3] = 0.0;
+      a[2] = wq / q;
+    }
+  };
+  if (R >= 0 && kmax >= kPairMin) {
+    // Long lists (dense rows): records k and k + 1 of a lane in one pass,
+    // their read-modify-write chains interleaved.  Both sit in the lane's
+    // bank, so their 4-cell x windows are disjoint unless the home cells are
+    // equal -- then the pair is summed in registers and added once.
+    double4 a1 = make_double4(0.0, 0.0, 0.0, 0.0), b1 = a1, a2 = a1, b2 = a1;
+    int x1 = 0, x2 = 0;
+    auto load = [&](uint32_t k, double4& ga_, double4& gb_, int& cx_) {
+      if (k < cnt) {
+        const uint32_t p = pos(k);
+        ga_ = ld_v4_nc(rec + 8 * (size_t)p);
+        gb_ = ld_v4_nc(rec + 8 * (size_t)p + 4);
+        cx_ = __ldg(rcx + p);
+      }
+    };
+    load(0, a1, b1, x1);
+    load(1, a2, b2, x2);
+    for (uint32_t k = 0; k < kmax; k += 2) {
+      const bool v1 = k < cnt;
+      bool v2 = k + 1 < cnt;
+      double4 na1 = a1, nb1 = b1, na2 = a2, nb2 = b2;  // the next pair, in flight
+      int nx1 = x1, nx2 = x2;
+      load(k + 2, na1, nb1, nx1);
+      load(k + 3, na2, nb2, nx2);
+      double w1[4], w2[4];
+      weights(b1, (k >= c[0]) + (k >= c[1]) + (k >= c[2]), w1);
+      weights(b2, (k + 1 >= c[0]) + (k + 1 >= c[1]) + (k + 1 >= c[2]), w2);
+      const double g1[4] = {a1.x, a1.y, a1.z, a1.w};
+      const double g2[4] = {a2.x, a2.y, a2.z, a2.w};
+      const bool merge = v2 && x2 == x1;
+      double* wa1 = W + ES * (x1 + (kPadL - 2));
+      double* wa2 = W + ES * (x2 + (kPadL - 2));
+      if (merge) v2 = false;
+#pragma unroll
+      for (int kx = 0; kx < 4; ++kx) {
+        double l1[4], l2[4];
+#pragma unroll
+        for (int kz = 0; kz < 4; ++kz) {
+          const int o = ((R + kz + 2) & 3) * (ES * RL) + ES * kx;
+          l1[kz] = v1 ? wa1[o] : 0.0;
+          l2[kz] = v2 ? wa2[o] : 0.0;
+        }
+#pragma unroll
+        for (int kz = 0; kz < 4; ++kz) {
+          const int o = ((R + kz + 2) & 3) * (ES * RL) + ES * kx;
+          double t1 = g1[kx] * w1[kz];
+          if (merge) t1 = fma(g2[kx], w2[kz], t1);
+          if (v1) wa1[o] = l1[kz] + t1;
+          if (v2) wa2[o] = l2[kz] + g2[kx] * w2[kz];
+        }
+        __syncwarp();
+      }
+      a1 = na1;
+      b1 = nb1;
+      x1 = nx1;
+      a2 = na2;
+      b2 = nb2;
+      x2 = nx2;
+    }
+    return;
+  }
   // Records are prefetched one iteration ahead (the loop is latency-bound).
   double4 ga = make_double4(0.0, 0.0, 0.0, 0.0), gb4 = ga;
   int cx = 0;
