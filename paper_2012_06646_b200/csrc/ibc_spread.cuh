@@ -71,29 +71,17 @@ __host__ __device__ constexpr int row_len(int nx) {
 // phases of one point: conflict-free, no collision test.  Lane gb + j (j <
 // 4, gb = the group's first lane) holds source row j's length len and row id
 // rid for the group's target row.
+// The paired loop of plane_banks for long lists, kept out of line so the
+// short-list loop of config-2-like densities is compiled as before.
 template <int D, int RL, int R>
-__device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t len,
-                                           uint32_t rid, const uint32_t* __restrict__ bstart,
-                                           const double* __restrict__ rec,
-                                           const int* __restrict__ rcx, double q) {
-  constexpr int GS = bucket::kBanks, ES = 16 / GS;
-  const int lane = threadIdx.x & 31, bank = lane & (GS - 1), gb = lane & ~(GS - 1);
-  uint32_t lo[4], c[4], cnt = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const uint32_t lenj = __shfl_sync(0xffffffffu, len, gb + j);
-    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, gb + j);
-    uint32_t b0 = 0, b1 = 0;  // this lane's (row, bank) bucket of source row j
-    if (lenj) {
-      const uint32_t* t = bstart + (size_t)ridj * GS + bank;
-      b0 = __ldg(t);
-      b1 = __ldg(t + 1);
-    }
-    lo[j] = b0 - cnt;  // record slot of this lane's k-th record = lo[j] + k
-    cnt += b1 - b0;
-    c[j] = cnt;
-  }
-  const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
+__device__ __noinline__ void plane_banks_paired(double* __restrict__ W, uint32_t lo0, uint32_t lo1,
+                                                uint32_t lo2, uint32_t lo3, uint32_t c0, uint32_t c1,
+                                                uint32_t c2, uint32_t cnt, uint32_t kmax,
+                                                const double* __restrict__ rec,
+                                                const int* __restrict__ rcx, double q) {
+  constexpr int ES = 16 / bucket::kBanks;
+  const uint32_t lo[4] = {lo0, lo1, lo2, lo3};
+  const uint32_t c[3] = {c0, c1, c2};
   auto pos = [&](uint32_t k) {
     const int j = (k >= c[0]) + (k >= c[1]) + (k >= c[2]);
     return (j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3]) + k;
@@ -113,7 +101,7 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
       a[2] = wq / q;
     }
   };
-  if (R >= 0 && kmax >= kPairMin) {
+  {
     // Long lists (dense rows): records k and k + 1 of a lane in one pass,
     // their read-modify-write chains interleaved.  Both sit in the lane's
     // bank, so their 4-cell x windows are disjoint unless the home cells are
@@ -172,6 +160,40 @@ __device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so
       b2 = nb2;
       x2 = nx2;
     }
+    return;
+  }
+}
+
+template <int D, int RL, int R>
+__device__ __forceinline__ void plane_banks(double* __restrict__ W, const int so[4], uint32_t len,
+                                           uint32_t rid, const uint32_t* __restrict__ bstart,
+                                           const double* __restrict__ rec,
+                                           const int* __restrict__ rcx, double q) {
+  constexpr int GS = bucket::kBanks, ES = 16 / GS;
+  const int lane = threadIdx.x & 31, bank = lane & (GS - 1), gb = lane & ~(GS - 1);
+  uint32_t lo[4], c[4], cnt = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t lenj = __shfl_sync(0xffffffffu, len, gb + j);
+    const uint32_t ridj = __shfl_sync(0xffffffffu, rid, gb + j);
+    uint32_t b0 = 0, b1 = 0;  // this lane's (row, bank) bucket of source row j
+    if (lenj) {
+      const uint32_t* t = bstart + (size_t)ridj * GS + bank;
+      b0 = __ldg(t);
+      b1 = __ldg(t + 1);
+    }
+    lo[j] = b0 - cnt;  // record slot of this lane's k-th record = lo[j] + k
+    cnt += b1 - b0;
+    c[j] = cnt;
+  }
+  const uint32_t kmax = __reduce_max_sync(0xffffffffu, cnt);
+  auto pos = [&](uint32_t k) {
+    const int j = (k >= c[0]) + (k >= c[1]) + (k >= c[2]);
+    return (j == 0 ? lo[0] : j == 1 ? lo[1] : j == 2 ? lo[2] : lo[3]) + k;
+  };
+  if (R >= 0 && kmax >= kPairMin) {
+    plane_banks_paired<D, RL, R>(W, lo[0], lo[1], lo[2], lo[3], c[0], c[1], c[2], cnt, kmax, rec, rcx,
+                                 q);
     return;
   }
   // Records are prefetched one iteration ahead (the loop is latency-bound).
