@@ -1,6 +1,6 @@
 """Dev: time + spot-check the BASELINE configs on one GPU.
-usage: config_time.py [c1|c2|w128|w256|rbc|clustered|severe ...]"""
-import sys, time
+usage: [IBC_DEV_PATH=auto|bank|pull|radix|walk] config_time.py [c1|c2|w128|w256|rbc|clustered|severe ...]"""
+import os, sys, time
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np, torch
@@ -20,6 +20,7 @@ def cfg(name):
     return N, pts
 
 ops = DeviceOperators(0)
+ops.context.set_spread_path(os.environ.get("IBC_DEV_PATH", "auto"))
 flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
 for name in sys.argv[1:] or ["c1", "c2", "w128", "rbc", "clustered"]:
     N, pts = cfg(name)
