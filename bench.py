@@ -71,21 +71,30 @@ def dist_env():
     return world, rank, local
 
 
+def _affinity() -> set:
+    try:
+        return set(os.sched_getaffinity(0))
+    except Exception:
+        return set(range(os.cpu_count() or 1))
+
+
+# Read once at import, before libgomp (the reference arm) binds the main
+# thread to one place and shrinks the mask.
+_CPUS = _affinity()
+
+
 def host_threads() -> int:
     """Host threads available to this process: the reference's OpenMP team
     (workers = nproc), one thread per logical CPU of the
     affinity mask."""
-    try:
-        return max(1, len(os.sched_getaffinity(0)))
-    except Exception:
-        return os.cpu_count() or 1
+    return max(1, len(_CPUS))
 
 
 def physical_cores() -> int | None:
     """Distinct physical cores behind the affinity mask (sysfs topology), or
     None when the topology is not readable."""
     try:
-        cpus = os.sched_getaffinity(0)
+        cpus = _CPUS
         cores = set()
         for c in cpus:
             base = f"/sys/devices/system/cpu/cpu{c}/topology/"
