@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-graph", action="store_true", help="time eager launches, not a CUDA graph")
     ap.add_argument("--mac-steps", type=int, default=5, help="MAC vector step timing (0: skip)")
+    ap.add_argument("--f32-steps", type=int, default=10,
+                    help="FP32 storage-mode step timing, a secondary figure (0: skip)")
     ap.add_argument("--no-serial", action="store_true", help="reference arm: skip the spread_serial timing")
     ap.add_argument("--transport", default="peer", choices=["peer", "collective"],
                     help="N > 1: slab exchange over peer memory (C ABI, one CUDA graph per step) "
@@ -626,6 +628,36 @@ def run_ours(args):
                            "updates per step, same 2^20 points, FP64, CUDA graph"}
         del loop
 
+    # Secondary figure: the same step in the FP32 storage mode (ibc_*_f32:
+    # float points / values / fields / results, FP64 arithmetic inside).
+    f32 = None
+    if world == 1 and args.f32_steps > 0 and dec is None:
+        xs32, gv32, fe32, xn32 = xs.float(), gv.float(), fe.float(), xn.float()
+        ell32 = torch.empty(n_omega, dtype=torch.float32, device=dev)
+        E32 = torch.empty(n, dtype=torch.float32, device=dev)
+        f32_op = lambda: (ops.spread(xs32, gv32, grid, out=ell32), ops.interpolate(fe32, xn32, grid, out=E32))
+        for _ in range(3):
+            f32_op()
+        torch.cuda.synchronize()
+        fgraph = None if args.no_graph else capture_graph(f32_op)
+        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.f32_steps)]
+        for i in range(args.f32_steps):
+            flush.fill_(float(i))
+            fev[i][0].record()
+            fgraph.replay() if fgraph is not None else f32_op()
+            fev[i][1].record()
+        torch.cuda.synchronize()
+        f32_ms = sum(a.elapsed_time(b) for a, b in fev) / args.f32_steps
+        f32_bytes = 32 * n + 8 * n_omega
+        f32 = {"value": n / (f32_ms * 1e-3), "unit": UNIT, "ms_per_step": f32_ms,
+               "steps": args.f32_steps, "dtype": "f32 storage, f64 arithmetic",
+               "step_roofline": {"alg_bytes": f32_bytes,
+                                 "frac": f32_bytes / (f32_ms * 1e-3) / 1e9 / peak},
+               "workload": "the headline step with float points, values, field and results "
+                           "(ibc_spread_device_f32 / ibc_interpolate_device_f32), CUDA graph"}
+        del xs32, gv32, fe32, xn32, ell32, E32
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         # The reference arm in a child process (its OpenMP team pinned there),
@@ -669,6 +701,7 @@ def run_ours(args):
             "breakdown_us": {k: round(v, 2) for k, v in per_launch.items()},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "mac_vector_step": mac,
+            "f32_storage_step": f32,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

@@ -184,6 +184,27 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
                                   const double* d_field, const double* d_points, size_t n,
                                   double* d_out);
 
+/* FP32 storage mode (the SURVEY 8(b) precision F32; the reference itself is
+ * FP64-only): points, values, fields and results are float in memory.  The
+ * inputs are widened exactly to double on the device, cells / weights / sums
+ * are the FP64 operator above, and each result is rounded once when stored
+ * -- so a result differs from the FP64 operator on the same (float-valued)
+ * inputs by that one rounding.  Same arguments, checks and errors as the
+ * FP64 entry points; multi-GPU slabs and binned points stay FP64. */
+ibc_status ibc_spread_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                          ibc_spread_algorithm algorithm, const float* points,
+                          const float* values, size_t n_points, size_t n_values,
+                          int sweep_width, ibc_workspace* ws, int workers, float* out);
+ibc_status ibc_interpolate_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                               const float* field, const float* points, size_t n_points,
+                               int workers, float* out);
+ibc_status ibc_spread_device_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                 const float* d_points, const float* d_values, size_t n,
+                                 ibc_workspace* ws, float* d_out);
+ibc_status ibc_interpolate_device_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                      const float* d_field, const float* d_points, size_t n,
+                                      float* d_out);
+
 /* Binned points: the field-independent half of an interpolation (cell keys,
  * row bucket sort, per-point weight records), kept so several fields can be
  * interpolated at the same points -- the reference's step interpolates the

@@ -379,6 +379,7 @@ void Context::release_resources() {
   interp_scratch.release_all();
   prim_scratch.release_all();
   for (auto& b : h_stage) b.release();
+  for (auto& b : wide) b.release();
   for (auto& p : pending) {
     cudaEventDestroy(p.second.first);
     cudaEventDestroy(p.second.second);
@@ -643,37 +644,146 @@ static void spread_checks(const ibc_grid* grid, ibc_kernel kernel, ibc_spread_al
   }
 }
 
+// Host-buffer and device-resident operators, FP64 or the FP32 storage mode
+// (T = float: inputs widened exactly to FP64 on the device, FP64 arithmetic,
+// one rounding per stored result).
+}  // extern "C"
+namespace {
+const double* as_f64(ibc::Context& c, const double* d, size_t, int) { (void)c; return d; }
+const double* as_f64(ibc::Context& c, const float* d, size_t m, int slot) {
+  return ibc::widen(c, d, m, c.wide[slot]);
+}
+
+template <class T>
+void spread_host(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                 ibc_spread_algorithm algorithm, const T* points, const T* values, size_t n_points,
+                 size_t n_values, int sweep_width, ibc_workspace* ws, T* out) {
+  if (!ctx) invalid("context is null");
+  spread_checks(grid, kernel, algorithm, n_points, n_values, sweep_width, ws);
+  if ((!points || !values) && n_points) invalid("null input buffer");
+  if (!out) invalid("null output buffer");
+  use_device(ctx->c);
+  ibc::Lane lane(ctx->c);
+  auto& c = *lane;
+  const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
+  // Serial/otf own no caller workspace: they run on the context's scratch.
+  ibc_workspace* use_ws =
+      (algorithm == IBC_SPREAD_FUSED || algorithm == IBC_SPREAD_BUFFERED) ? ws : nullptr;
+  ibc::PointScratch& s = spread_scratch_for(c, use_ws, n_points, g);
+  const size_t np = grid_points(grid);
+  c.h_stage[0].ensure(n_points * grid->dim);
+  c.h_stage[1].ensure(n_points);
+  c.h_stage[2].ensure(np);
+  T* d_pts = reinterpret_cast<T*>(c.h_stage[0].p);
+  T* d_val = reinterpret_cast<T*>(c.h_stage[1].p);
+  T* d_out = reinterpret_cast<T*>(c.h_stage[2].p);
+  if (n_points) {
+    host_copy(c, d_pts, points, n_points * grid->dim * sizeof(T), cudaMemcpyHostToDevice, c.stream);
+    host_copy(c, d_val, values, n_points * sizeof(T), cudaMemcpyHostToDevice, c.stream);
+  }
+  ibc::spread_pipeline(c, g, as_f64(c, d_pts, n_points * grid->dim, 0), as_f64(c, d_val, n_points, 1),
+                       n_points, s, d_out);
+  host_copy(c, out, d_out, np * sizeof(T), cudaMemcpyDeviceToHost, c.stream);
+  IBC_CUDA(cudaStreamSynchronize(c.stream));
+  g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
+}
+
+template <class T>
+void interp_host(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel, const T* field,
+                 const T* points, size_t n_points, T* out) {
+  if (!ctx) invalid("context is null");
+  check_grid(grid);
+  check_kernel(kernel);
+  check_points(n_points);
+  if (!field) invalid("null field");
+  if (n_points && (!points || !out)) invalid("null point buffer");
+  use_device(ctx->c);
+  ibc::Lane lane(ctx->c);
+  auto& c = *lane;
+  const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
+  const size_t np = grid_points(grid);
+  c.interp_scratch.reserve_points(n_points, false);
+  c.interp_scratch.reserve_rows(g.nrows);
+  c.h_stage[2].ensure(np);
+  c.h_stage[0].ensure(n_points * grid->dim);
+  c.h_stage[3].ensure(n_points);
+  T* d_pts = reinterpret_cast<T*>(c.h_stage[0].p);
+  T* d_field = reinterpret_cast<T*>(c.h_stage[2].p);
+  T* d_out = reinterpret_cast<T*>(c.h_stage[3].p);
+  // Points first: their binning (keys, row sort, records) runs while the
+  // field is still arriving on the lane's copy stream.
+  if (n_points)
+    host_copy(c, d_pts, points, n_points * grid->dim * sizeof(T), cudaMemcpyHostToDevice, c.stream);
+  cudaEvent_t field_in = c.acquire_event();
+  host_copy(c, d_field, field, np * sizeof(T), cudaMemcpyHostToDevice, c.copy_stream);
+  IBC_CUDA(cudaEventRecord(field_in, c.copy_stream));
+  const double* pts = as_f64(c, d_pts, n_points * grid->dim, 0);
+  const ibc::InterpPlan P = ibc::interp_bin(c, g, pts, n_points, c.interp_scratch, true);
+  IBC_CUDA(cudaStreamWaitEvent(c.stream, field_in, 0));
+  c.event_pool.push_back(field_in);
+  ibc::interp_gather(c, g, P, (const T*)d_field, pts, n_points, c.interp_scratch, d_out);
+  if (n_points) host_copy(c, out, d_out, n_points * sizeof(T), cudaMemcpyDeviceToHost, c.stream);
+  IBC_CUDA(cudaStreamSynchronize(c.stream));
+  g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
+}
+
+template <class T>
+void spread_dev(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel, const T* d_points,
+                const T* d_values, size_t n, ibc_workspace* ws, T* d_out) {
+  if (!ctx) invalid("context is null");
+  check_grid(grid);
+  check_kernel(kernel);
+  check_points(n);
+  if (ws) {
+    if (ws->w.point_count != n) invalid("workspace sized for a different point count");
+    if (ws->w.grid_points != grid_points(grid)) invalid("workspace sized for a different grid");
+  }
+  if (!d_out) invalid("null output buffer");
+  auto& c = ctx->c;
+  use_device(c);
+  const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
+  ibc::PointScratch& s = spread_scratch_for(c, ws, n, g);
+  ibc::spread_pipeline(c, g, as_f64(c, d_points, n * grid->dim, 0), as_f64(c, d_values, n, 1), n, s,
+                       d_out);
+  g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
+}
+
+template <class T>
+void interp_dev(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel, const T* d_field,
+                const T* d_points, size_t n, T* d_out) {
+  if (!ctx) invalid("context is null");
+  check_grid(grid);
+  check_kernel(kernel);
+  check_points(n);
+  auto& c = ctx->c;
+  use_device(c);
+  const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
+  c.interp_scratch.reserve_points(n, false);
+  c.interp_scratch.reserve_rows(g.nrows);
+  ibc::interp_pipeline(c, g, d_field, as_f64(c, d_points, n * grid->dim, 0), n, c.interp_scratch,
+                       d_out);
+  g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
+}
+}  // namespace
+extern "C" {
+
 ibc_status ibc_spread(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
                       ibc_spread_algorithm algorithm, const double* points, const double* values,
                       size_t n_points, size_t n_values, int sweep_width, ibc_workspace* ws,
                       int workers, double* out) {
   (void)workers;
   return guarded([&] {
-    if (!ctx) invalid("context is null");
-    spread_checks(grid, kernel, algorithm, n_points, n_values, sweep_width, ws);
-    if ((!points || !values) && n_points) invalid("null input buffer");
-    if (!out) invalid("null output buffer");
-    use_device(ctx->c);
-    ibc::Lane lane(ctx->c);
-    auto& c = *lane;
-    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
-    // Serial/otf own no caller workspace: they run on the context's scratch.
-    ibc_workspace* use_ws =
-        (algorithm == IBC_SPREAD_FUSED || algorithm == IBC_SPREAD_BUFFERED) ? ws : nullptr;
-    ibc::PointScratch& s = spread_scratch_for(c, use_ws, n_points, g);
-    const size_t np = grid_points(grid);
-    c.h_stage[0].ensure(n_points * grid->dim);
-    c.h_stage[1].ensure(n_points);
-    c.h_stage[2].ensure(np);
-    if (n_points) {
-      host_copy(c, c.h_stage[0].p, points, n_points * grid->dim * 8, cudaMemcpyHostToDevice,
-                c.stream);
-      host_copy(c, c.h_stage[1].p, values, n_points * 8, cudaMemcpyHostToDevice, c.stream);
-    }
-    ibc::spread_pipeline(c, g, c.h_stage[0].p, c.h_stage[1].p, n_points, s, c.h_stage[2].p);
-    host_copy(c, out, c.h_stage[2].p, np * 8, cudaMemcpyDeviceToHost, c.stream);
-    IBC_CUDA(cudaStreamSynchronize(c.stream));
-    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
+    spread_host(ctx, grid, kernel, algorithm, points, values, n_points, n_values, sweep_width, ws, out);
+  });
+}
+
+ibc_status ibc_spread_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                          ibc_spread_algorithm algorithm, const float* points, const float* values,
+                          size_t n_points, size_t n_values, int sweep_width, ibc_workspace* ws,
+                          int workers, float* out) {
+  (void)workers;
+  return guarded([&] {
+    spread_host(ctx, grid, kernel, algorithm, points, values, n_points, n_values, sweep_width, ws, out);
   });
 }
 
@@ -681,80 +791,38 @@ ibc_status ibc_interpolate(ibc_context* ctx, const ibc_grid* grid, ibc_kernel ke
                            const double* field, const double* points, size_t n_points,
                            int workers, double* out) {
   (void)workers;
-  return guarded([&] {
-    if (!ctx) invalid("context is null");
-    check_grid(grid);
-    check_kernel(kernel);
-    check_points(n_points);
-    if (!field) invalid("null field");
-    if (n_points && (!points || !out)) invalid("null point buffer");
-    use_device(ctx->c);
-    ibc::Lane lane(ctx->c);
-    auto& c = *lane;
-    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
-    const size_t np = grid_points(grid);
-    c.interp_scratch.reserve_points(n_points, false);
-    c.interp_scratch.reserve_rows(g.nrows);
-    c.h_stage[2].ensure(np);
-    c.h_stage[0].ensure(n_points * grid->dim);
-    c.h_stage[3].ensure(n_points);
-    // Points first: their binning (keys, row sort, records) runs while the
-    // field is still arriving on the lane's copy stream.
-    if (n_points)
-      host_copy(c, c.h_stage[0].p, points, n_points * grid->dim * 8, cudaMemcpyHostToDevice,
-                c.stream);
-    cudaEvent_t field_in = c.acquire_event();
-    host_copy(c, c.h_stage[2].p, field, np * 8, cudaMemcpyHostToDevice, c.copy_stream);
-    IBC_CUDA(cudaEventRecord(field_in, c.copy_stream));
-    const ibc::InterpPlan P = ibc::interp_bin(c, g, c.h_stage[0].p, n_points, c.interp_scratch, true);
-    IBC_CUDA(cudaStreamWaitEvent(c.stream, field_in, 0));
-    c.event_pool.push_back(field_in);
-    ibc::interp_gather(c, g, P, c.h_stage[2].p, c.h_stage[0].p, n_points, c.interp_scratch,
-                       c.h_stage[3].p);
-    if (n_points) host_copy(c, out, c.h_stage[3].p, n_points * 8, cudaMemcpyDeviceToHost, c.stream);
-    IBC_CUDA(cudaStreamSynchronize(c.stream));
-    g_delta_evaluations.fetch_add(n_points * shift_count(grid->dim, kernel), std::memory_order_relaxed);
-  });
+  return guarded([&] { interp_host(ctx, grid, kernel, field, points, n_points, out); });
+}
+
+ibc_status ibc_interpolate_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                               const float* field, const float* points, size_t n_points,
+                               int workers, float* out) {
+  (void)workers;
+  return guarded([&] { interp_host(ctx, grid, kernel, field, points, n_points, out); });
 }
 
 ibc_status ibc_spread_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
                              const double* d_points, const double* d_values, size_t n,
                              ibc_workspace* ws, double* d_out) {
-  return guarded([&] {
-    if (!ctx) invalid("context is null");
-    check_grid(grid);
-    check_kernel(kernel);
-    check_points(n);
-    if (ws) {
-      if (ws->w.point_count != n) invalid("workspace sized for a different point count");
-      if (ws->w.grid_points != grid_points(grid)) invalid("workspace sized for a different grid");
-    }
-    if (!d_out) invalid("null output buffer");
-    auto& c = ctx->c;
-    use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
-    ibc::PointScratch& s = spread_scratch_for(c, ws, n, g);
-    ibc::spread_pipeline(c, g, d_points, d_values, n, s, d_out);
-    g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
-  });
+  return guarded([&] { spread_dev(ctx, grid, kernel, d_points, d_values, n, ws, d_out); });
+}
+
+ibc_status ibc_spread_device_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                 const float* d_points, const float* d_values, size_t n,
+                                 ibc_workspace* ws, float* d_out) {
+  return guarded([&] { spread_dev(ctx, grid, kernel, d_points, d_values, n, ws, d_out); });
 }
 
 ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
                                   const double* d_field, const double* d_points, size_t n,
                                   double* d_out) {
-  return guarded([&] {
-    if (!ctx) invalid("context is null");
-    check_grid(grid);
-    check_kernel(kernel);
-    check_points(n);
-    auto& c = ctx->c;
-    use_device(c);
-    const ibc::DevGrid g = ibc::make_devgrid(*grid, (int)kernel);
-    c.interp_scratch.reserve_points(n, false);
-    c.interp_scratch.reserve_rows(g.nrows);
-    ibc::interp_pipeline(c, g, d_field, d_points, n, c.interp_scratch, d_out);
-    g_delta_evaluations.fetch_add(n * shift_count(grid->dim, kernel), std::memory_order_relaxed);
-  });
+  return guarded([&] { interp_dev(ctx, grid, kernel, d_field, d_points, n, d_out); });
+}
+
+ibc_status ibc_interpolate_device_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
+                                      const float* d_field, const float* d_points, size_t n,
+                                      float* d_out) {
+  return guarded([&] { interp_dev(ctx, grid, kernel, d_field, d_points, n, d_out); });
 }
 
 static void check_slab(const ibc_grid* grid, const ibc_slab* slab, ibc_kernel kernel) {

@@ -94,6 +94,7 @@ struct Context {
   PointScratch interp_scratch;  // interpolation
   PointScratch prim_scratch;    // sort / reduce primitives
   DevBuf<double> h_stage[4];    // device staging for host-buffer calls
+  DevBuf<double> wide[2];       // FP32 storage mode: points / values widened to FP64
   cudaEvent_t acquire_event();
   void prof_begin(int cls, cudaEvent_t* ev);
   void prof_end(int cls, cudaEvent_t ev);
@@ -157,8 +158,12 @@ inline int kernel_support(int k) {
 }
 // Wrapped home cell along the last axis of every point (slab binning key).
 void home_planes(Context& ctx, const DevGrid& g, const double* d_points, size_t n, int* d_planes);
+// TO / TF: the grid value type in memory (double; float in the FP32 storage
+// mode -- points and values are widened to double before the pipeline, all
+// arithmetic is FP64, one rounding at the store).
+template <typename TO>
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points,
-                     const double* d_values, size_t n, PointScratch& s, double* d_out);
+                     const double* d_values, size_t n, PointScratch& s, TO* d_out);
 // Interpolation split into a field-independent binning and the gather.
 struct InterpPlan {
   bool tma = false;
@@ -166,10 +171,14 @@ struct InterpPlan {
 };
 InterpPlan interp_bin(Context& ctx, const DevGrid& g, const double* d_points, size_t n,
                       PointScratch& s, bool allow_tma);
-void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const double* d_field,
-                   const double* d_points, size_t n, PointScratch& s, double* d_out);
-void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field,
-                     const double* d_points, size_t n, PointScratch& s, double* d_out);
+template <typename TF>
+void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const TF* d_field,
+                   const double* d_points, size_t n, PointScratch& s, TF* d_out);
+template <typename TF>
+void interp_pipeline(Context& ctx, const DevGrid& g, const TF* d_field,
+                     const double* d_points, size_t n, PointScratch& s, TF* d_out);
+// FP32 storage mode: m floats widened (exactly) to doubles in buf, on ctx.stream.
+const double* widen(Context& ctx, const float* d_in, size_t m, DevBuf<double>& buf);
 // ws.run_keys on the device; returns q (synchronizes).
 size_t compute_run_keys(Context& ctx, PointScratch& s);
 // The stable (key, index) order of the last spread (ws.keys / ws.perm), on request.

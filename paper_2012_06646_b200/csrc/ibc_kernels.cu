@@ -211,10 +211,11 @@ struct SpreadTiling {
 // cell, so shared-memory accumulation needs no atomics and the summation
 // order is fixed (results are bitwise reproducible).  Each grid value is
 // written to HBM exactly once, with coalesced stores.
+template <typename TO>
 __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
     DevGrid g, SpreadTiling T, const uint32_t* __restrict__ rowstart,
     const int* __restrict__ rec_cx, const double* __restrict__ rec, uint32_t n,
-    double* __restrict__ out) {
+    TO* __restrict__ out) {
   extern __shared__ double s_acc[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   int b = blockIdx.x;
@@ -299,7 +300,7 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
   for (int i = tid; i < cells; i += blockDim.x) {
     const int tr = i / T.tx, xx = i - tr * T.tx;
     const int ty = y0 + tr % T.ty, tz = z0 + tr / T.ty, x = x0 + xx;
-    if (ty < g.n[1] && tz < g.n[2] && x < g.n[0]) out[tz * sz_ + ty * sy_ + x] = s_acc[i];
+    if (ty < g.n[1] && tz < g.n[2] && x < g.n[0]) out[tz * sz_ + ty * sy_ + x] = (TO)s_acc[i];
   }
 }
 
@@ -308,10 +309,11 @@ __global__ void __launch_bounds__(kSpreadThreads) spread_tiles_kernel(
 // threads gather neighbouring grid values; result stored at the point's
 // input slot.  Summation order over the 4^d support is the reference's
 // colexicographic shift order (interpolate.hpp:42-52).
-__global__ void __launch_bounds__(kBlock) interp_kernel(DevGrid g, const double* __restrict__ field,
+template <typename TF>
+__global__ void __launch_bounds__(kBlock) interp_kernel(DevGrid g, const TF* __restrict__ field,
                                                         const double* __restrict__ X,
                                                         const uint32_t* __restrict__ perm, uint32_t n,
-                                                        double* __restrict__ out) {
+                                                        TF* __restrict__ out) {
   const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r >= n) return;
   const uint32_t i = perm ? __ldg(perm + r) : r;
@@ -356,12 +358,12 @@ __global__ void __launch_bounds__(kBlock) interp_kernel(DevGrid g, const double*
         const int64_t o = off[0][kx] + oyz;
         if (kx <= s1 && o >= 0) {
           const double wt = (w[0][kx] * w[1][ky]) * w[2][kz];
-          acc += wt * __ldg(field + o);
+          acc += wt * (double)__ldg(field + o);
         }
       }
     }
   }
-  out[i] = acc * g.hd;
+  out[i] = (TF)(acc * g.hd);
 }
 
 // ---------------------------------------------------------------- run keys
@@ -707,8 +709,9 @@ bool sweep_tiling(const DevGrid& g, int sms, uint32_t pull_row, sp::SweepTiling&
 }
 }  // namespace
 
+template <typename TO>
 void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, const double* d_values,
-                     size_t n, PointScratch& s, double* d_out) {
+                     size_t n, PointScratch& s, TO* d_out) {
   cudaStream_t st = ctx.stream;
   sp::SweepTiling W, WB;  // pull mode, bank mode
   // Bank-mode row threshold: AUTO -- rows up to kPullRow (and crowded
@@ -747,19 +750,19 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
   cudaEvent_t ev = nullptr;
   static bool attr_set[64] = {};
   if (!attr_set[ctx.device & 63]) {
-    IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    IBC_CUDA(cudaFuncSetAttribute(spread_tiles_kernel<TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   160 * 1024));
     for (const void* k :
-         {(const void*)sp::spread_sweep_kernel<2, 0>, (const void*)sp::spread_banks_kernel<2, 0>,
-          (const void*)sp::spread_sweep_kernel<3, 0>, (const void*)sp::spread_banks_kernel<3, 0>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64)>,
-          (const void*)sp::spread_banks_kernel<3, sp::row_len(64)>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128)>,
-          (const void*)sp::spread_banks_kernel<3, sp::row_len(128)>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256)>,
-          (const void*)sp::spread_banks_kernel<3, sp::row_len(256)>,
-          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512)>,
-          (const void*)sp::spread_banks_kernel<3, sp::row_len(512)>})
+         {(const void*)sp::spread_sweep_kernel<2, 0, TO>, (const void*)sp::spread_banks_kernel<2, 0, TO>,
+          (const void*)sp::spread_sweep_kernel<3, 0, TO>, (const void*)sp::spread_banks_kernel<3, 0, TO>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(64), TO>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(64), TO>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(128), TO>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(128), TO>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(256), TO>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(256), TO>,
+          (const void*)sp::spread_sweep_kernel<3, sp::row_len(512), TO>,
+          (const void*)sp::spread_banks_kernel<3, sp::row_len(512), TO>})
       IBC_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_set[ctx.device & 63] = true;
   }
@@ -782,7 +785,7 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
                                                s.rec_cx.p, d_out);
     };
     const int nx = g.n[0];
-#define IBC_SWEEP(D, RL) launch(sp::spread_banks_kernel<D, RL>, sp::spread_sweep_kernel<D, RL>)
+#define IBC_SWEEP(D, RL) launch(sp::spread_banks_kernel<D, RL, TO>, sp::spread_sweep_kernel<D, RL, TO>)
     if (g.dim == 3) {
       if (nx == 64) IBC_SWEEP(3, sp::row_len(64));
       else if (nx == 128) IBC_SWEEP(3, sp::row_len(128));
@@ -807,23 +810,47 @@ void spread_pipeline(Context& ctx, const DevGrid& g, const double* d_points, con
     const size_t smem = (size_t)T.tx * T.ty * T.tz * sizeof(double);
     ctx.prof_begin(kProfSpread, &ev);
     const unsigned blocks = (unsigned)((size_t)T.ntx * T.nty * T.ntz);
-    spread_tiles_kernel<<<blocks, kSpreadThreads, smem, st>>>(g, T, s.rowstart.p, s.rec_cx.p,
-                                                              s.rec.p, (uint32_t)n, d_out);
+    spread_tiles_kernel<TO><<<blocks, kSpreadThreads, smem, st>>>(g, T, s.rowstart.p, s.rec_cx.p,
+                                                                  s.rec.p, (uint32_t)n, d_out);
     ++ctx.launches;
     ctx.prof_end(kProfSpread, ev);
   }
   IBC_CUDA(cudaGetLastError());
   ++ctx.spread_calls;
 }
+namespace {
+__global__ void __launch_bounds__(kBlock) widen_kernel(const float* __restrict__ in, size_t m,
+                                                       double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)kBlock + threadIdx.x; i < m; i += (size_t)gridDim.x * kBlock)
+    out[i] = (double)__ldg(in + i);
+}
+}  // namespace
+
+const double* widen(Context& ctx, const float* d_in, size_t m, DevBuf<double>& buf) {
+  buf.ensure(m);
+  if (m) {
+    const unsigned blocks = (unsigned)std::min<size_t>((m + kBlock - 1) / kBlock, (size_t)ctx.sms * 8);
+    widen_kernel<<<blocks, kBlock, 0, ctx.stream>>>(d_in, m, buf.p);
+    ++ctx.launches;
+    IBC_CUDA(cudaGetLastError());
+  }
+  return buf.p;
+}
+
+template void spread_pipeline<double>(Context&, const DevGrid&, const double*, const double*, size_t,
+                                      PointScratch&, double*);
+template void spread_pipeline<float>(Context&, const DevGrid&, const double*, const double*, size_t,
+                                     PointScratch&, float*);
 
 namespace {
 
 // Tiling of the TMA interpolation sweep (3-D, nx % 16 == 0, nx <= 4096).
-bool interp_tma_tiling(const DevGrid& g, size_t n, int sms, sw::InterpTiling& T) {
+// elem: bytes per field value (8, or 4 in the FP32 storage mode).
+bool interp_tma_tiling(const DevGrid& g, size_t n, int sms, sw::InterpTiling& T, int elem = 8) {
   if (g.dim != 3) return false;
   const int nx = g.n[0], ny = g.n[1], nz = g.n[2];
   if (nx % 16 != 0 || nx > 4096) return false;
-  const uint32_t pitch = (uint32_t)((nx * 8 + 1023) & ~1023);
+  const uint32_t pitch = (uint32_t)((nx * elem + 1023) & ~1023);
   // Pick TY (home rows per CTA) minimising the bytes one SM streams, with at
   // least 3 planes in flight (slots >= 7) when possible and one CTA per SM.
   double best = 1e300;
@@ -867,7 +894,7 @@ bool interp_tma_tiling(const DevGrid& g, size_t n, int sms, sw::InterpTiling& T)
   if (!found) return false;
   T.pitch = pitch;
   T.slot_bytes = (uint32_t)T.frmax * pitch;
-  T.box_ok = nx % 128 == 0 ? 1 : 0;  // box rows land at the slot pitch (1024-byte multiple)
+  T.box_ok = (nx * elem) % 1024 == 0 ? 1 : 0;  // box rows land at the slot pitch (1024-byte multiple)
   return true;
 }
 
@@ -878,7 +905,8 @@ size_t interp_tma_smem(const sw::InterpTiling& T) {
 }  // namespace
 
 namespace tma {
-bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz, int box_rows) {
+bool encode_rows_map(CUtensorMap* map, const void* field, int elem, int nx, int ny, int nz,
+                     int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
     void* p = nullptr;
@@ -889,11 +917,13 @@ bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int 
     fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
   }
   if (reinterpret_cast<uintptr_t>(field) % 16 != 0) return false;
+  const cuuint64_t e = (cuuint64_t)elem;
   const cuuint64_t dims[4] = {16, (cuuint64_t)(nx / 16), (cuuint64_t)ny, (cuuint64_t)nz};
-  const cuuint64_t strides[3] = {128, (cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+  const cuuint64_t strides[3] = {16 * e, (cuuint64_t)nx * e, (cuuint64_t)nx * ny * e};
   const cuuint32_t box[4] = {16, (cuuint32_t)(nx / 16), (cuuint32_t)box_rows, 1};
   const cuuint32_t es[4] = {1, 1, 1, 1};
-  return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(field), dims, strides, box,
+  return fn(map, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4,
+            const_cast<void*>(field), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1045,33 +1075,38 @@ InterpPlan interp_bin(Context& ctx, const DevGrid& g, const double* d_points, si
 }
 
 // The gather over a binning (d_points is read again on the generic path).
-void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const double* d_field,
-                   const double* d_points, size_t n, PointScratch& s, double* d_out) {
+// The binning plans the TMA tiling for 8-byte values; FP32 fields retile
+// (half the plane bytes: a 4-byte tiling exists whenever the 8-byte one does).
+template <typename TF>
+void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const TF* d_field,
+                   const double* d_points, size_t n, PointScratch& s, TF* d_out) {
   if (n == 0) return;
   cudaStream_t st = ctx.stream;
   cudaEvent_t ev = nullptr;
   if (P.tma) {
-    const sw::InterpTiling& T = P.T;
+    sw::InterpTiling T = P.T;
+    if (sizeof(TF) != 8 && !interp_tma_tiling(g, n, ctx.sms, T, (int)sizeof(TF)))
+      throw ArgError{"no shared-memory tiling for this field"};
     CUtensorMap map, map_box;
-    if (!tma::encode_rows_map(&map, d_field, g.n[0], g.n[1], g.n[2]) ||
-        !tma::encode_rows_map(&map_box, d_field, g.n[0], g.n[1], g.n[2], T.frmax))
+    if (!tma::encode_rows_map(&map, d_field, (int)sizeof(TF), g.n[0], g.n[1], g.n[2]) ||
+        !tma::encode_rows_map(&map_box, d_field, (int)sizeof(TF), g.n[0], g.n[1], g.n[2], T.frmax))
       throw ArgError{"field must be 16-byte aligned device memory"};
     const size_t smem = interp_tma_smem(T);
     static bool attr_set[64] = {};
     if (!attr_set[ctx.device & 63]) {
-      IBC_CUDA(cudaFuncSetAttribute(sw::interp_tma_kernel,
+      IBC_CUDA(cudaFuncSetAttribute(sw::interp_tma_kernel<TF>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
       attr_set[ctx.device & 63] = true;
     }
     ctx.prof_begin(kProfInterp, &ev);
-    pdl_launch(sw::interp_tma_kernel, (unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st, g, T, map,
-               map_box, s.rowstart.p, s.rec.p, d_out);
+    pdl_launch(sw::interp_tma_kernel<TF>, (unsigned)(T.nty * T.nzc), sw::kIThreads, smem, st, g, T,
+               map, map_box, (const uint32_t*)s.rowstart.p, (const double*)s.rec.p, d_out);
   } else {
     // Generic gather (1-D/2-D grids, x extents the TMA rows do not take,
     // other supports): one thread per point in sorted order.
     ctx.prof_begin(kProfInterp, &ev);
-    interp_kernel<<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
-                                                          (uint32_t)n, d_out);
+    interp_kernel<TF><<<grid_for(n, kBlock), kBlock, 0, st>>>(g, d_field, d_points, s.sorted_perm,
+                                                              (uint32_t)n, d_out);
   }
   ++ctx.launches;
   ctx.prof_end(kProfInterp, ev);
@@ -1079,14 +1114,23 @@ void interp_gather(Context& ctx, const DevGrid& g, const InterpPlan& P, const do
   ++ctx.interp_calls;
 }
 
-void interp_pipeline(Context& ctx, const DevGrid& g, const double* d_field, const double* d_points,
-                     size_t n, PointScratch& s, double* d_out) {
+template <typename TF>
+void interp_pipeline(Context& ctx, const DevGrid& g, const TF* d_field, const double* d_points,
+                     size_t n, PointScratch& s, TF* d_out) {
   if (n == 0) return;
   // The TMA tensor maps need a 16-byte aligned field.
   const bool aligned = reinterpret_cast<uintptr_t>(d_field) % 16 == 0;
   const InterpPlan P = interp_bin(ctx, g, d_points, n, s, aligned);
   interp_gather(ctx, g, P, d_field, d_points, n, s, d_out);
 }
+template void interp_gather<double>(Context&, const DevGrid&, const InterpPlan&, const double*,
+                                    const double*, size_t, PointScratch&, double*);
+template void interp_gather<float>(Context&, const DevGrid&, const InterpPlan&, const float*,
+                                   const double*, size_t, PointScratch&, float*);
+template void interp_pipeline<double>(Context&, const DevGrid&, const double*, const double*, size_t,
+                                      PointScratch&, double*);
+template void interp_pipeline<float>(Context&, const DevGrid&, const float*, const double*, size_t,
+                                     PointScratch&, float*);
 
 // ws.run_keys and ws.run_count (= q) on the device, computed on demand from
 // the sorted keys (reduce.hpp:36-69); cached until the next sort.

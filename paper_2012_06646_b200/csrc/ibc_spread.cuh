@@ -29,6 +29,8 @@
 //    records per batch; lanes with the same home cx are summed into their
 //    group's lowest lane by shuffles, which adds alone.
 // Either way the summation order is fixed by the data: bitwise reproducible.
+// Sums are FP64 throughout; TO (double, or float for the FP32 storage mode)
+// is only the type of the single store per grid value.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -345,13 +347,13 @@ __device__ __forceinline__ void plane_batches_pull(double* __restrict__ W, const
 // lanes with the same home cx are summed into their group leader by shuffles.
 // Launched next to the bank-mode kernel; the one that does not match the
 // densest row seen by the row scan (*maxrow) returns at once.
-template <int D, int RL>
+template <int D, int RL, typename TO>
 __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTiling T,
                                                            const uint32_t* __restrict__ maxrow,
                                                            const uint32_t* __restrict__ rowstart,
                                                            const double* __restrict__ rec,
                                                            const int* __restrict__ rcx,
-                                                           double* __restrict__ out) {
+                                                           TO* __restrict__ out) {
   pdl_wait();
   extern __shared__ __align__(16) double win[];
   if (maxrow && bucket::bank_mode(maxrow, T.pull_row)) return;  // bank mode
@@ -436,13 +438,13 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
     const int t = D == 3 ? s - 2 : 0;
     if (t >= z0 && t < z1) {
       double* Wr = W + (D == 3 ? (t & 3) * rl : 0);
-      double* orow = out + ((size_t)t * ny + ty) * nx;
+      TO* orow = out + ((size_t)t * ny + ty) * nx;
       if (px && nx < 8) {
         for (int x = lane; x < nx; x += 32) {
           double v = Wr[(x + kPadL)];
           for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[(qx + kPadL)];
           for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[(qx + kPadL)];
-          orow[x] = v;
+          orow[x] = (TO)v;
         }
       } else {
         for (int x = lane; x < nx; x += 32) {
@@ -451,7 +453,7 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
             if (x >= nx - kPadL) v += Wr[(x - nx + kPadL)];
             if (x < kPadR) v += Wr[(x + nx + kPadL)];
           }
-          orow[x] = v;
+          orow[x] = (TO)v;
         }
       }
       __syncwarp();
@@ -466,13 +468,13 @@ __global__ void __launch_bounds__(256, 3) spread_sweep_kernel(DevGrid g, SweepTi
 // Bank mode (bucket::bank_mode): one warp per kRowsPerWarp target rows of a
 // z-chunk, z-sweep as above, plane_banks per source plane.  Window per
 // half-warp: its 16 / kBanks rows interleaved, four slots.
-template <int D, int RL>
+template <int D, int RL, typename TO>
 __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling T,
                                                           const uint32_t* __restrict__ maxrow,
                                                           const uint32_t* __restrict__ bstart,
                                                           const double* __restrict__ rec,
                                                           const int* __restrict__ rcx,
-                                                          double* __restrict__ out) {
+                                                          TO* __restrict__ out) {
   pdl_wait();
   extern __shared__ __align__(16) double win[];
   if (!bucket::bank_mode(maxrow, T.pull_row)) return;  // pull mode
@@ -547,13 +549,13 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
       const size_t slot = D == 3 ? (size_t)(t & 3) * ES * rl : 0;
       const double* Wr = W + slot;
       if (row_ok) {
-        double* orow = out + ((size_t)t * ny + ty) * nx;
+        TO* orow = out + ((size_t)t * ny + ty) * nx;
         if (px && nx < 8) {
           for (int x = bank; x < nx; x += GS) {
             double v = Wr[ES * (x + kPadL)];
             for (int qx = x - nx; qx >= -kPadL; qx -= nx) v += Wr[ES * (qx + kPadL)];
             for (int qx = x + nx; qx < nx + kPadR; qx += nx) v += Wr[ES * (qx + kPadL)];
-            orow[x] = v;
+            orow[x] = (TO)v;
           }
         } else {
           for (int x = bank; x < nx; x += GS) {
@@ -562,7 +564,7 @@ __global__ void __launch_bounds__(32) spread_banks_kernel(DevGrid g, SweepTiling
               if (x >= nx - kPadL) v += Wr[ES * (x - nx + kPadL)];
               if (x < kPadR) v += Wr[ES * (x + nx + kPadL)];
             }
-            orow[x] = v;
+            orow[x] = (TO)v;
           }
         }
       }

@@ -46,10 +46,13 @@ __device__ __forceinline__ double shfl_d(double v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
 
+// TF: the field / output element type (double, or float for the FP32
+// storage mode: planes half the size in shared memory, FP64 arithmetic).
+template <typename TF>
 __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
     DevGrid g, InterpTiling T, const __grid_constant__ CUtensorMap tmap_row,
     const __grid_constant__ CUtensorMap tmap_box, const uint32_t* __restrict__ rowstart,
-    const double* __restrict__ rec, double* __restrict__ out) {
+    const double* __restrict__ rec, TF* __restrict__ out) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // Layout: full[kMaxSlots] | empty[kMaxSlots] | step table [3][hmax] |
@@ -77,7 +80,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
   const int H = hz1 - hz0;            // home planes (steps)
   // One box load per plane unless the rows wrap around a periodic y edge.
   const bool box = T.box_ok && (!g.periodic[1] || (hy0 - 2 >= 0 && hy1 < ny));
-  const uint32_t plane_bytes = (uint32_t)(box ? T.frmax : fr) * (uint32_t)nx * 8u;
+  const uint32_t plane_bytes = (uint32_t)(box ? T.frmax : fr) * (uint32_t)nx * (uint32_t)sizeof(TF);
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
@@ -109,7 +112,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
   {
     const uint32_t o0 = __ldg(rowstart + g.nrows), o1 = __ldg(rowstart + g.nrows + 1);
     for (uint32_t r = o0 + blockIdx.x * kIThreads + tid; r < o1; r += gridDim.x * kIThreads)
-      out[(uint32_t)__double_as_longlong(rec[8 * (size_t)r + 6])] = 0.0;
+      out[(uint32_t)__double_as_longlong(rec[8 * (size_t)r + 6])] = TF(0);
   }
 
   if (warp == kIConsumers) {
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
         wxk = 0.0;  // off the closed grid: the reference skips the term
         x = 0;
       }
-      const uint32_t xo = (uint32_t)x * 8u + (uint32_t)(valid ? cy - hy0 : 0) * T.pitch;
+      const uint32_t xo = (uint32_t)x * (uint32_t)sizeof(TF) + (uint32_t)(valid ? cy - hy0 : 0) * T.pitch;
       double acc = 0.0;
       if (valid) {
         // Pairwise sums (dependency depth 6 instead of 20 fused multiply-adds).
@@ -215,14 +218,14 @@ __global__ void __launch_bounds__(kIThreads, 1) interp_tma_kernel(
           double v[4];
 #pragma unroll
           for (int ky = 0; ky < 4; ++ky)
-            v[ky] = *reinterpret_cast<const double*>(p + (uint32_t)ky * T.pitch);
+            v[ky] = (double)*reinterpret_cast<const TF*>(p + (uint32_t)ky * T.pitch);
           az[kz] = fma(wy[1], v[1], wy[0] * v[0]) + fma(wy[3], v[3], wy[2] * v[2]);
         }
         acc = (fma(wz[1], az[1], wz[0] * az[0]) + fma(wz[3], az[3], wz[2] * az[2])) * wxk;
       }
       acc += __shfl_xor_sync(0xffffffffu, acc, 1);
       acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (valid && kx == 0) out[idx] = acc * g.hd;
+      if (valid && kx == 0) out[idx] = (TF)(acc * g.hd);
     }
     // Plane j is not read by any later step.
     __syncwarp();

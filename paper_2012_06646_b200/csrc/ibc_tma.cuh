@@ -92,7 +92,8 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 // (16, nx/16, ny, nz) with a box of box_rows rows (16, nx/16, box_rows, 1), no
 // swizzle (the gather's bank pattern depends on x only either way; measured
 // a little faster unswizzled), zero fill out of bounds.  Requires nx % 16 == 0, nx <= 4096.
-bool encode_rows_map(CUtensorMap* map, const double* field, int nx, int ny, int nz, int box_rows = 1);
+bool encode_rows_map(CUtensorMap* map, const void* field, int elem, int nx, int ny, int nz,
+                     int box_rows = 1);
 
 }  // namespace tma
 }  // namespace ibc

@@ -44,15 +44,26 @@ def _ptr(t) -> C.c_void_p:
     return C.c_void_p(int(t.data_ptr()))
 
 
-def _require(t, name, numel=None):
+def _require(t, name, numel=None, dtype=None):
     import torch
 
+    dtype = dtype or torch.float64
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise InvalidArgument(f"{name} must be a CUDA tensor")
-    if t.dtype != torch.float64 or not t.is_contiguous():
-        raise InvalidArgument(f"{name} must be contiguous float64")
+    if t.dtype != dtype or not t.is_contiguous():
+        raise InvalidArgument(f"{name} must be contiguous {str(dtype).split('.')[-1]}")
     if numel is not None and t.numel() != numel:
         raise InvalidArgument(f"{name} has {t.numel()} elements, expected {numel}")
+
+
+def _precision(t):
+    """float64 tensors run the FP64 operators, float32 ones the FP32 storage
+    mode (ibc_*_device_f32: float in memory, FP64 arithmetic)."""
+    import torch
+
+    if isinstance(t, torch.Tensor) and t.dtype == torch.float32:
+        return torch.float32, "_f32"
+    return torch.float64, ""
 
 
 class BinnedPoints:
@@ -98,37 +109,41 @@ class DeviceOperators:
 
     def spread(self, points, values, grid: StaggeredGrid, out=None, workspace=None,
                kernel=CosineKernel):
-        """points (n, D) float64 cuda, values (n,) -> out (prod(extent),) float64 cuda."""
+        """points (n, D), values (n,) -> out (prod(extent),), cuda, all float64 --
+        or all float32 (the FP32 storage mode, ibc_spread_device_f32)."""
         import torch
 
         n = points.shape[0] if points.dim() == 2 else points.numel() // grid.dim
-        _require(points, "points", n * grid.dim)
-        _require(values, "values", n)
+        dt, sfx = _precision(points)
+        _require(points, "points", n * grid.dim, dt)
+        _require(values, "values", n, dt)
         if out is None:
-            out = torch.empty(grid.point_count(), dtype=torch.float64, device=points.device)
-        _require(out, "out", grid.point_count())
+            out = torch.empty(grid.point_count(), dtype=dt, device=points.device)
+        _require(out, "out", grid.point_count(), dt)
         ws = workspace if workspace is not None else self.workspace(n, grid)
         self._sync_stream()
-        check(load().ibc_spread_device(self.context.handle, C.byref(grid.c_grid),
-                                       _kernel_code(kernel), _ptr(points), _ptr(values), n,
-                                       ws.handle, _ptr(out)))
+        check(getattr(load(), "ibc_spread_device" + sfx)(
+            self.context.handle, C.byref(grid.c_grid), _kernel_code(kernel), _ptr(points),
+            _ptr(values), n, ws.handle, _ptr(out)))
         ws._mark(n)
         return out
 
     def interpolate(self, field, points, grid: StaggeredGrid, out=None, kernel=CosineKernel):
-        """field (prod(extent),) + points (n, D) -> out (n,), all float64 cuda."""
+        """field (prod(extent),) + points (n, D) -> out (n,), cuda, all float64 --
+        or all float32 (the FP32 storage mode, ibc_interpolate_device_f32)."""
         import torch
 
         n = points.shape[0] if points.dim() == 2 else points.numel() // grid.dim
-        _require(field, "field", grid.point_count())
-        _require(points, "points", n * grid.dim)
+        dt, sfx = _precision(field)
+        _require(field, "field", grid.point_count(), dt)
+        _require(points, "points", n * grid.dim, dt)
         if out is None:
-            out = torch.empty(n, dtype=torch.float64, device=points.device)
-        _require(out, "out", n)
+            out = torch.empty(n, dtype=dt, device=points.device)
+        _require(out, "out", n, dt)
         self._sync_stream()
-        check(load().ibc_interpolate_device(self.context.handle, C.byref(grid.c_grid),
-                                            _kernel_code(kernel), _ptr(field), _ptr(points),
-                                            n, _ptr(out)))
+        check(getattr(load(), "ibc_interpolate_device" + sfx)(
+            self.context.handle, C.byref(grid.c_grid), _kernel_code(kernel), _ptr(field),
+            _ptr(points), n, _ptr(out)))
         return out
 
     def bin_points(self, points, grid: StaggeredGrid, kernel=CosineKernel, binned=None):
