@@ -7,3 +7,4 @@ timeout -s KILL 600 compute-sanitizer --tool memcheck --print-limit 10 python -m
 timeout -s KILL 600 compute-sanitizer --tool memcheck --print-limit 10 tests/cpp/build/slab_test 2>&1 | tail -2
 timeout -s KILL 600 compute-sanitizer --tool memcheck --print-limit 10 tests/cpp/build/overlay_test verify 2>&1 | tail -2
 timeout -s KILL 1200 compute-sanitizer --tool memcheck --print-limit 5 --target-processes all python -m pytest tests/test_modes.py -m gpu -x -q --timeout 1100 2>&1 | tail -2
+timeout -s KILL 600 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_f32.py -m gpu -x -q --timeout 500 -k "not config2" 2>&1 | tail -2
