@@ -46,19 +46,28 @@ constexpr int kBanks = 32 / kRowsPerWarp;
 constexpr int kShortRow = 256;      // rows up to this length are sorted by one warp
 
 // Spread batching mode, decided on the device from the row scan's statistics
-// stats[0] = densest row, stats[1] = fullest (row, x bank) bucket: bank mode
-// (lanes own x banks, ibc_spread.cuh) for sparse rows, and for crowded
-// buckets (>= kClusterBucket points), where the pull mode's same-cell shuffle
-// groups serialise.  Measured spreads, bank vs pull: W 256^3 (fullest bucket
-// 40) 3.75 vs 5.49 ms, severe clustering (293) 13.9 vs 26.9 ms; clustered
-// (32) 2.08 vs 2.04 ms, W 128^3 (24) 0.52 vs 0.49 ms, RBC (17) 0.45 vs
-// 0.29 ms.
+// stats[0] = densest row, stats[1] = fullest (row, x bank) bucket, and over
+// the rows of >= kBalanceRow points stats[2] = sum of their fullest buckets,
+// stats[3] = sum of their lengths: bank mode (lanes own x banks,
+// ibc_spread.cuh) for sparse rows; for crowded buckets (>= kClusterBucket
+// points), where the pull mode's same-cell shuffle groups serialise; and for
+// dense rows whose points spread evenly over the x banks (fullest bucket of a
+// row <= kBalance x its mean bucket, summed over the dense rows) -- a lane's
+// list is then close to the row's mean, the bank sweep's lanes stay full.
+// Measured spreads, bank vs pull (round 2, paired bank loop): W 128^3
+// (balance 1.67) 437 vs 460 us, clustered (1.79) 1.91 vs 2.03 ms, severe
+// clustering (fullest bucket 297) 10.4 vs 26.9 ms, RBC surfaces (balance
+// 2.32: a membrane crossing a row fills a few banks) 422 vs 265 us.
 constexpr uint32_t kClusterBucket = 36;
+constexpr uint32_t kBalanceRow = 32;
+constexpr uint32_t kBalance = 2;  // stats[2] * 16 <= kBalance * stats[3]
 // pull_row == kNoBankMode: the bank window does not fit (very long x rows).
 constexpr uint32_t kNoBankMode = 0xffffffffu;
 __host__ __device__ __forceinline__ bool bank_mode(const uint32_t* stats, uint32_t pull_row) {
   if (pull_row == kNoBankMode) return false;
-  return stats[0] <= pull_row || stats[1] >= kClusterBucket;
+  if (pull_row == 0xfffffffeu) return true;  // forced (IBC_SPREAD_PATH_BANK)
+  return stats[0] <= pull_row || stats[1] >= kClusterBucket ||
+         (stats[3] > 0 && (uint64_t)stats[2] * 16u <= (uint64_t)kBalance * stats[3]);
 }
 constexpr int kLongSortMax = 8192;  // longest row the shared-memory bitonic sort takes
 constexpr uint32_t kOutside = 0x80000000u;  // rank flag: home cell outside the grid (K1)
@@ -123,6 +132,7 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
                                                                 uint32_t* nlong, uint32_t* maxrow) {
   pdl_wait();
   __shared__ uint32_t s_warp[kScanThreads / 32], s_vmax[kScanThreads / 32], s_bmax[kScanThreads / 32];
+  __shared__ uint32_t s_balb[kScanThreads / 32], s_baln[kScanThreads / 32];
   __shared__ uint32_t s_chunk, s_prefix;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_chunk = atomicAdd(ticket, 1u);  // chunks start in ticket order
@@ -151,19 +161,27 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
       if (long_rows && v[q] > (uint32_t)kShortRow) long_rows[atomicAdd(nlong, 1u)] = r0 + q;
     }
   }
-  uint32_t bmax = 0;
+  uint32_t bmax = 0, bal_b = 0, bal_n = 0;
   if (group > 1) {  // the thread's ITEMS == group buckets are one grid row
 #pragma unroll
     for (int q = 0; q < ITEMS; ++q) bmax = max(bmax, v[q]);
     vmax = sum;
     if (long_rows && sum > (uint32_t)kShortRow && r0 < nrows)
       long_rows[atomicAdd(nlong, 1u)] = r0 / (uint32_t)group;
+    if (sum >= kBalanceRow) {  // dense row: its fullest bucket vs its length
+      bal_b = bmax;
+      bal_n = sum;
+    }
   }
   vmax = __reduce_max_sync(0xffffffffu, vmax);
   bmax = __reduce_max_sync(0xffffffffu, bmax);
+  bal_b = __reduce_add_sync(0xffffffffu, bal_b);
+  bal_n = __reduce_add_sync(0xffffffffu, bal_n);
   if (lane == 0) {  // per-CTA maxima: one atomic per CTA, not per warp
     s_vmax[warp] = vmax;
     s_bmax[warp] = bmax;
+    s_balb[warp] = bal_b;
+    s_baln[warp] = bal_n;
   }
   // Block scan of the per-thread sums.
   uint32_t x = sum;
@@ -186,9 +204,17 @@ __global__ void __launch_bounds__(kScanThreads) row_scan_kernel(const uint32_t* 
     if (maxrow) {  // densest row, fullest bucket (spread batching mode)
       const uint32_t cm = __reduce_max_sync(0xffffffffu, s_vmax[lane]);
       const uint32_t cb = __reduce_max_sync(0xffffffffu, s_bmax[lane]);
+      const uint32_t sb = __reduce_add_sync(0xffffffffu, s_balb[lane]);
+      const uint32_t sn = __reduce_add_sync(0xffffffffu, s_baln[lane]);
       if (lane == 0) {
         atomicMax(maxrow, cm);
-        if (group > 1) atomicMax(maxrow + 1, cb);
+        if (group > 1) {
+          atomicMax(maxrow + 1, cb);
+          if (sn) {
+            atomicAdd(maxrow + 2, sb);
+            atomicAdd(maxrow + 3, sn);
+          }
+        }
       }
     }
     // Publish the aggregate, then look back 32 chunks per round trip.

@@ -944,7 +944,7 @@ void launch_row_sorts(Context& ctx, const DevGrid& g, const double* d_points,
   cudaStream_t st = ctx.stream;
   const uint32_t* maxrow = s.maxrow;
   uint32_t* nlong = const_cast<uint32_t*>(maxrow) - 1;
-  const uint32_t* long_rows = maxrow + 2;
+  const uint32_t* long_rows = maxrow + 4;
   static bool attr_set[64] = {};
   const size_t lsm = (size_t)bucket::kLongSortMax * 8;
   if (!attr_set[ctx.device & 63]) {
@@ -989,8 +989,8 @@ void bucket_points(Context& ctx, const DevGrid& g, const double* d_points, const
   uint32_t* ticket = status + nchunks;
   uint32_t* nlong = ticket + 1;
   uint32_t* maxrow = nlong + 1;     // [densest row, fullest bucket]
-  uint32_t* long_rows = maxrow + 2;
-  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nb + nchunks + 4) * 4, st));
+  uint32_t* long_rows = maxrow + 4;
+  IBC_CUDA(cudaMemsetAsync(count, 0, ((size_t)nb + nchunks + 6) * 4, st));
   s.maxrow = spread ? maxrow : nullptr;  // (zeroed above; set by the row scan)
   if (n == 0) {
     IBC_CUDA(cudaMemsetAsync(s.rowstart.p, 0, ((size_t)nb + 1) * 4, st));
