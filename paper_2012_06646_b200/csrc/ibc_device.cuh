@@ -302,7 +302,7 @@ struct InterpTiling {
   int slots;             // ring depth (>= 5)
   uint32_t pitch;        // bytes per field row in shared memory (multiple of 1024)
   uint32_t slot_bytes;   // frmax * pitch
-  int rec_cap;           // point records staged per step (32 B each)
+  int rec_cap;           // point records staged per step (64 B each)
   int hmax;              // max home planes per CTA (row-range table entries)
   uint32_t slot_stride;  // slot_bytes + rec_cap * 64, rounded up to 1024
   int box_ok;            // one TMA per plane allowed (nx % 128 == 0)
