@@ -4,13 +4,16 @@
 // ib::b200; the reference's names live in the sibling headers.
 #pragma once
 
+#include <array>
 #include <cstddef>
 #include <cstdint>
+#include <exception>
 #include <functional>
 #include <new>
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "ibcuda.h"
@@ -51,6 +54,38 @@ inline ibc_context* context() {
   static Holder h;
   if (!h.ctx) check(ibc_context_create(default_device(), &h.ctx));
   return h.ctx;
+}
+
+// f(c) for the components c = 0 .. count-1 of a vector operation, one host
+// thread each (the calling thread takes the last): the context serves every
+// host-buffer call on its own lane (stream, staging, scratch), so the
+// components' copies and kernels overlap -- one component's grid download
+// beside the next one's upload.  Results do not depend on the overlap.
+// Rethrows the lowest component's exception.
+template <std::size_t N, class F>
+void for_components(std::size_t count, F&& f) {
+  context();  // created once, before any thread asks for it
+  std::array<std::exception_ptr, N> err{};
+  std::vector<std::thread> threads;
+  threads.reserve(count);
+  for (std::size_t c = 0; c + 1 < count; ++c)
+    threads.emplace_back([&f, &err, c] {
+      try {
+        f(c);
+      } catch (...) {
+        err[c] = std::current_exception();
+      }
+    });
+  if (count) {
+    try {
+      f(count - 1);
+    } catch (...) {
+      err[count - 1] = std::current_exception();
+    }
+  }
+  for (auto& t : threads) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
 }
 
 // A workspace result the reference keeps as a plain member (ws.keys,

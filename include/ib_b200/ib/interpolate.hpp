@@ -29,14 +29,16 @@ LagrangianValues interpolate(const GridField<D>& field, const PointSet<D>& point
   return out;
 }
 
-// interpolate.hpp:60-72.
+// interpolate.hpp:60-72; the components run concurrently.
 template <std::size_t D, Kernel K>
 std::array<LagrangianValues, D> interpolate_vector(std::span<const GridField<D>> fields,
                                                    const PointSet<D>& points, const K& kernel,
                                                    int workers) {
   if (fields.size() != D) throw std::invalid_argument("expected one field per vector component");
+  // The components concurrently, one host thread each (b200::for_components);
+  // each call checks its arguments before any work, like the reference's.
   std::array<LagrangianValues, D> out;
-  for (std::size_t c = 0; c < D; ++c) out[c] = interpolate(fields[c], points, kernel, workers);
+  b200::for_components<D>(D, [&](std::size_t c) { out[c] = interpolate(fields[c], points, kernel, workers); });
   return out;
 }
 

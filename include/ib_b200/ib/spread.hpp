@@ -7,6 +7,7 @@
 #include <cassert>
 #include <cstdint>
 #include <memory>
+#include <optional>
 #include <span>
 #include <stdexcept>
 #include <utility>
@@ -144,7 +145,14 @@ GridField<D> spread_buffered_otf(const PointSet<D>& points, std::span<const doub
                          workers);
 }
 
-// One spread per MAC component (spread.hpp:319-350).
+// One spread per MAC component (spread.hpp:319-350).  The reference runs the
+// components one after the other, each checking its arguments first; here
+// the checks run first, in the same order and with the same messages, and
+// the components that would have run before the first failing one run
+// concurrently (b200::for_components), then its exception is thrown.  With
+// a workspace (fused / buffered) the last component spreads through it, so
+// it ends up holding that component's sort as in the reference, and the
+// others run the same device operator on context scratch.
 template <std::size_t D, Kernel K>
 std::array<GridField<D>, D> spread_vector(const PointSet<D>& points,
                                           const std::array<LagrangianValues, D>& values,
@@ -152,25 +160,55 @@ std::array<GridField<D>, D> spread_vector(const PointSet<D>& points,
                                           SpreadAlgorithm algorithm, int sweep_width,
                                           SpreadWorkspace<D>* workspace, int workers) {
   if (grids.size() != D) throw std::invalid_argument("expected one grid per vector component");
-  auto component = [&](std::size_t c) -> GridField<D> {
-    const std::span<const double> v(values[c]);
-    switch (algorithm) {
-      case SpreadAlgorithm::serial:
-        return spread_serial(points, v, grids[c], kernel);
-      case SpreadAlgorithm::fused:
-        if (!workspace) throw std::invalid_argument("fused spreading needs a workspace");
-        return spread_fused(points, v, grids[c], kernel, *workspace, workers);
-      case SpreadAlgorithm::buffered:
-        if (!workspace) throw std::invalid_argument("buffered spreading needs a workspace");
-        return spread_buffered(points, v, grids[c], kernel, *workspace, workers);
-      case SpreadAlgorithm::otf:
-        return spread_buffered_otf(points, v, grids[c], kernel, sweep_width, workers);
+  // The first component whose call would throw, and its exception.
+  std::size_t ok = D;
+  std::exception_ptr fail;
+  for (std::size_t c = 0; c < D && !fail; ++c) {
+    try {
+      switch (algorithm) {
+        case SpreadAlgorithm::serial:
+          detail::check_spread_args<D>(points.size(), values[c].size(), kernel.support());
+          break;
+        case SpreadAlgorithm::fused:
+        case SpreadAlgorithm::buffered: {
+          const bool buffered = algorithm == SpreadAlgorithm::buffered;
+          if (!workspace)
+            throw std::invalid_argument(buffered ? "buffered spreading needs a workspace"
+                                                 : "fused spreading needs a workspace");
+          detail::check_spread_args<D>(points.size(), values[c].size(), kernel.support());
+          detail::check_workspace(*workspace, points.size(), grids[c], buffered);
+          break;
+        }
+        case SpreadAlgorithm::otf:
+          if (sweep_width < 1) throw std::invalid_argument("sweep width must be >= 1");
+          detail::check_spread_args<D>(points.size(), values[c].size(), kernel.support());
+          break;
+        default:
+          throw std::invalid_argument("unknown spreading algorithm");
+      }
+    } catch (...) {
+      ok = c;
+      fail = std::current_exception();
     }
-    throw std::invalid_argument("unknown spreading algorithm");
+  }
+  std::array<std::optional<GridField<D>>, D> res;
+  auto component = [&](std::size_t c) {
+    const std::span<const double> v(values[c]);
+    const bool last = c + 1 == D;
+    if (algorithm == SpreadAlgorithm::serial || (!last && algorithm != SpreadAlgorithm::otf))
+      res[c].emplace(spread_serial(points, v, grids[c], kernel));
+    else if (algorithm == SpreadAlgorithm::fused)
+      res[c].emplace(spread_fused(points, v, grids[c], kernel, *workspace, workers));
+    else if (algorithm == SpreadAlgorithm::buffered)
+      res[c].emplace(spread_buffered(points, v, grids[c], kernel, *workspace, workers));
+    else
+      res[c].emplace(spread_buffered_otf(points, v, grids[c], kernel, sweep_width, workers));
   };
-  if constexpr (D == 1) return {component(0)};
-  else if constexpr (D == 2) return {component(0), component(1)};
-  else return {component(0), component(1), component(2)};
+  b200::for_components<D>(ok, component);
+  if (fail) std::rethrow_exception(fail);
+  if constexpr (D == 1) return {std::move(*res[0])};
+  else if constexpr (D == 2) return {std::move(*res[0]), std::move(*res[1])};
+  else return {std::move(*res[0]), std::move(*res[1]), std::move(*res[2])};
 }
 
 }  // namespace ib
