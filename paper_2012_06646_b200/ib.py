@@ -356,10 +356,10 @@ class SpreadWorkspace:
 
 
 def _spread(points, values, grid: StaggeredGrid, kernel, algorithm: int, sweep_width: int,
-            ws: SpreadWorkspace | None, workers: int) -> GridField:
+            ws: SpreadWorkspace | None, workers: int, context: Context | None = None) -> GridField:
     p = _points(points, grid.dim)
     v = np.ascontiguousarray(values, dtype=np.float64).reshape(-1)
-    ctx = ws.context if ws is not None else default_context()
+    ctx = ws.context if ws is not None else (context or default_context())
     out = np.empty(grid.point_count(), np.float64)
     check(load().ibc_spread(ctx.handle, C.byref(grid.c_grid), _kernel_code(kernel), int(algorithm),
                             p.ctypes.data_as(C.c_void_p), v.ctypes.data_as(C.c_void_p),
@@ -399,30 +399,90 @@ def spread_buffered_otf(points, values, grid: StaggeredGrid, kernel, sweep_width
     return _spread(points, values, grid, kernel, SpreadAlgorithm.otf, sweep_width, None, workers)
 
 
+def _for_components(count: int, fn) -> list:
+    """fn(c) for c < count on one host thread each (ctypes releases the GIL; the
+    context serves each host-buffer call on its own lane, so the components'
+    copies and kernels overlap).  Raises the lowest component's exception."""
+    if count <= 1:
+        return [fn(c) for c in range(count)]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=count - 1) as pool:
+        futs = [pool.submit(fn, c) for c in range(count - 1)]
+        out, err = [None] * count, [None] * count
+        try:
+            out[count - 1] = fn(count - 1)
+        except Exception as e:  # noqa: BLE001 -- re-raised in component order below
+            err[count - 1] = e
+        for c, f in enumerate(futs):
+            try:
+                out[c] = f.result()
+            except Exception as e:  # noqa: BLE001
+                err[c] = e
+    for e in err:
+        if e is not None:
+            raise e
+    return out
+
+
 def spread_vector(points, values, grids, kernel, algorithm, sweep_width: int,
                   workspace: SpreadWorkspace | None, workers: int = 1):
-    """ib::spread_vector (spread.hpp:321-350): one spread per MAC component."""
+    """ib::spread_vector (spread.hpp:321-350): one spread per MAC component.
+
+    The reference's per-component argument checks run first, in its order; the
+    components before the first failing one then run concurrently
+    (_for_components) and its error is raised.  With a workspace the last
+    component spreads through it (so it holds that component's sort, as in the
+    reference); the others run the same device operator on its context."""
     grids = list(grids)
     dim = grids[0].dim if grids else 0
     if len(grids) != dim:
         raise InvalidArgument("expected one grid per vector component")
-    out = []
+    n = _points(points, dim).shape[0] if dim else 0
+    ok, fail = dim, None
     for c in range(dim):
-        if algorithm == SpreadAlgorithm.serial:
-            out.append(spread_serial(points, values[c], grids[c], kernel))
-        elif algorithm == SpreadAlgorithm.fused:
-            if workspace is None:
-                raise InvalidArgument("fused spreading needs a workspace")
-            out.append(spread_fused(points, values[c], grids[c], kernel, workspace, workers))
-        elif algorithm == SpreadAlgorithm.buffered:
-            if workspace is None:
-                raise InvalidArgument("buffered spreading needs a workspace")
-            out.append(spread_buffered(points, values[c], grids[c], kernel, workspace, workers))
-        elif algorithm == SpreadAlgorithm.otf:
-            out.append(spread_buffered_otf(points, values[c], grids[c], kernel, sweep_width,
-                                           workers))
-        else:
-            raise InvalidArgument("unknown spreading algorithm")
+        try:
+            nv = np.asarray(values[c]).size
+            if algorithm in (SpreadAlgorithm.fused, SpreadAlgorithm.buffered):
+                if workspace is None:
+                    raise InvalidArgument("fused spreading needs a workspace"
+                                          if algorithm == SpreadAlgorithm.fused
+                                          else "buffered spreading needs a workspace")
+            elif algorithm == SpreadAlgorithm.otf:
+                if sweep_width < 1:
+                    raise InvalidArgument("sweep width must be >= 1")
+            elif algorithm != SpreadAlgorithm.serial:
+                raise InvalidArgument("unknown spreading algorithm")
+            if nv != n:
+                raise InvalidArgument("one value per point required")
+            if not 1 <= kernel.support() <= 8:
+                raise InvalidArgument("unsupported kernel support size")
+            if workspace is not None and algorithm in (SpreadAlgorithm.fused, SpreadAlgorithm.buffered):
+                if workspace.point_count != n:
+                    raise InvalidArgument("workspace sized for a different point count")
+                if workspace.grid_points != grids[c].point_count():
+                    raise InvalidArgument("workspace sized for a different grid")
+                if algorithm == SpreadAlgorithm.buffered and workspace.sweep_width < 1:
+                    raise InvalidArgument("workspace has no sweep buffers")
+        except InvalidArgument as e:
+            ok, fail = c, e
+            break
+    ctx = workspace.context if workspace is not None else None
+
+    def component(c):
+        last = c == dim - 1
+        if algorithm == SpreadAlgorithm.serial or (not last and algorithm != SpreadAlgorithm.otf):
+            return _spread(points, values[c], grids[c], kernel, SpreadAlgorithm.serial, 0, None, 1,
+                           context=ctx)
+        if algorithm == SpreadAlgorithm.fused:
+            return spread_fused(points, values[c], grids[c], kernel, workspace, workers)
+        if algorithm == SpreadAlgorithm.buffered:
+            return spread_buffered(points, values[c], grids[c], kernel, workspace, workers)
+        return spread_buffered_otf(points, values[c], grids[c], kernel, sweep_width, workers)
+
+    out = _for_components(ok, component)
+    if fail is not None:
+        raise fail
     return out
 
 
@@ -445,7 +505,9 @@ def interpolate_vector(fields, points, kernel, workers: int = 1):
     dim = fields[0].grid.dim if fields else 0
     if len(fields) != dim:
         raise InvalidArgument("expected one field per vector component")
-    return [interpolate(f, points, kernel, workers) for f in fields]
+    # the components concurrently (_for_components); each call checks its
+    # arguments before any work, like the reference's
+    return _for_components(dim, lambda c: interpolate(fields[c], points, kernel, workers))
 
 
 class stats:

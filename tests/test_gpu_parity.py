@@ -272,6 +272,39 @@ def test_vector_components_match_scalar_oracle():
         assert O.max_rel_deviation(sp[c].values, O.spread_serial(og(grids[c]), pts, values[c])) <= TOL
 
 
+def test_vector_components_concurrent_equal_sequential():
+    # spread_vector / interpolate_vector run their components on concurrent
+    # host threads: bit-identical to the scalar calls one after the other,
+    # the workspace holds the last component's sort (as in the reference),
+    # the operation count is the sequential one, and a component whose
+    # arguments fail raises after exactly the components before it ran
+    grids = [ib.StaggeredGrid([32] * 3, 0.5, a, [True] * 3)
+             for a in ([0.0, 0.5, 0.5], [0.5, 0.0, 0.5], [0.5, 0.5, 0.0])]
+    rng = np.random.default_rng(98)
+    n = 20000
+    pts = rand_points(grids[0], n, rng)
+    values = [rng.uniform(-1, 1, n) for _ in range(3)]
+    fields = [ib.GridField(g, rng.uniform(-1, 1, g.point_count())) for g in grids]
+    for algo in (ib.SpreadAlgorithm.fused, ib.SpreadAlgorithm.serial, ib.SpreadAlgorithm.otf):
+        ws = ib.SpreadWorkspace(n, grids[0]) if algo == ib.SpreadAlgorithm.fused else None
+        ib.stats.reset_delta_evaluations()
+        vec = ib.spread_vector(pts, values, grids, K, algo, 2, ws, 4)
+        assert ib.stats.delta_evaluations() == 3 * n * 64
+        for c in range(3):
+            assert np.array_equal(vec[c].values, ib.spread_serial(pts, values[c], grids[c], K).values)
+        if ws is not None:
+            keys, perm, _ = O.prepare_keys(og(grids[2]), pts)
+            assert np.array_equal(ws.keys, keys) and np.array_equal(ws.perm, perm)
+    E = ib.interpolate_vector(fields, pts, K, 4)
+    for c in range(3):
+        assert np.array_equal(E[c], ib.interpolate(fields[c], pts, K, 4))
+    ib.stats.reset_delta_evaluations()
+    with pytest.raises(ib.InvalidArgument, match="one value per point"):
+        ib.spread_vector(pts, [values[0], values[1][:10], values[2]], grids, K,
+                         ib.SpreadAlgorithm.serial, 0, None, 1)
+    assert ib.stats.delta_evaluations() == n * 64  # component 0 ran, as in the reference
+
+
 def test_workspace_errors():
     g = ib.StaggeredGrid([8, 8], 0.5, [0.0, 0.0], [True, True])
     other = ib.StaggeredGrid([10, 10], 0.5, [0.0, 0.0], [True, True])
