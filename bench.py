@@ -124,12 +124,10 @@ def bench_config(workload: str, n: int, grid) -> dict:
 
 
 def lib_build_id() -> str:
-    """sha256 (16 hex) of the loaded libibcuda.so: stamps measured ncu traffic."""
-    import hashlib
+    """Source hash of libibcuda.so (_build.source_id): stamps measured ncu traffic."""
+    from paper_2012_06646_b200 import _build
 
-    from paper_2012_06646_b200 import _capi
-
-    return hashlib.sha256(_capi.LIB_PATH.read_bytes()).hexdigest()[:16]
+    return _build.source_id()
 
 
 def peaks():

@@ -20,6 +20,20 @@ NVCC_FLAGS = [
 ]
 
 
+def source_id() -> str:
+    """sha256 (16 hex) of what libibcuda.so is built from: its sources, the C
+    ABI header and the nvcc flags.  Stamps measured ncu traffic
+    (profiles/traffic.json); unlike the binary's hash (nvcc output is not
+    byte-reproducible) it survives a rebuild of the same code."""
+    import hashlib
+
+    h = hashlib.sha256(" ".join(NVCC_FLAGS).encode())
+    for f in [CSRC / s for s in SOURCES + HEADERS] + [ROOT / "include" / "ibcuda.h"]:
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
+
+
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and Path(cand).exists():

@@ -3,9 +3,10 @@
 active).  Also writes profiles/traffic.json (DRAM bytes per launch per
 operator kernel) for bench.py's roofline.traffic field.
 usage: ncu_summary.py report.ncu-rep out.txt [workload]
-traffic.json is stamped with the sha256 of the libibcuda.so the capture ran
-(copy that build into the repo before summarising) and the bench workload,
-so bench.py only reports it for the same build."""
+traffic.json is stamped with the source hash of libibcuda.so
+(_build.source_id: sources, C ABI header, nvcc flags -- summarise before
+editing them) and the bench workload, so bench.py only reports it for the
+same code."""
 import csv, json, subprocess, sys
 from pathlib import Path
 rep, outp = sys.argv[1], sys.argv[2]
@@ -49,9 +50,9 @@ for row in r[2:]:
             traffic[tag] = int(total)
 Path(outp).write_text("\n".join(lines) + "\n")
 if traffic:
-    import hashlib
-    lib = Path(__file__).resolve().parents[1] / "paper_2012_06646_b200" / "_lib" / "libibcuda.so"
-    traffic["build"] = hashlib.sha256(lib.read_bytes()).hexdigest()[:16]
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_2012_06646_b200 import _build
+    traffic["build"] = _build.source_id()  # the sources the capture's build came from
     traffic["workload"] = sys.argv[3] if len(sys.argv) > 3 else "c2"
     Path("profiles/traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
 print("\n".join(lines))
