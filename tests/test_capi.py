@@ -3,6 +3,7 @@
 import re
 from pathlib import Path
 
+import numpy as np
 import pytest
 
 from paper_2012_06646_b200 import _capi
@@ -58,3 +59,27 @@ def test_grid_accessors():
     assert g.axis_length(1) == 3.0
     assert g.is_periodic(0) and not g.is_periodic(1)
     assert g.staggering(1) == 0.5 and g.spacing() == 0.5
+
+
+def test_vector_spread_checks_run_before_any_device_work():
+    # ib.spread_vector checks every component's arguments first, in the
+    # reference's order (spread.hpp:321-350 -> :60-77, :314); these cases fail
+    # at component 0, so no library call (and no GPU) is needed
+    g = [ib.StaggeredGrid([8, 8], 0.5, a, [True, True]) for a in ([0.0, 0.5], [0.5, 0.0])]
+    pts = np.array([[1.0, 1.0], [2.0, 2.0]])
+    vals = [np.ones(2), np.ones(2)]
+    K = ib.CosineKernel()
+    with pytest.raises(ib.InvalidArgument, match="one grid per vector component"):
+        ib.spread_vector(pts, vals, g[:1], K, ib.SpreadAlgorithm.serial, 0, None, 1)
+    with pytest.raises(ib.InvalidArgument, match="fused spreading needs a workspace"):
+        ib.spread_vector(pts, vals, g, K, ib.SpreadAlgorithm.fused, 0, None, 1)
+    with pytest.raises(ib.InvalidArgument, match="buffered spreading needs a workspace"):
+        ib.spread_vector(pts, vals, g, K, ib.SpreadAlgorithm.buffered, 0, None, 1)
+    with pytest.raises(ib.InvalidArgument, match="sweep width must be >= 1"):
+        ib.spread_vector(pts, vals, g, K, ib.SpreadAlgorithm.otf, 0, None, 1)
+    with pytest.raises(ib.InvalidArgument, match="one value per point"):
+        ib.spread_vector(pts, [np.ones(3), np.ones(2)], g, K, ib.SpreadAlgorithm.serial, 0, None, 1)
+    with pytest.raises(ib.InvalidArgument, match="unknown spreading algorithm"):
+        ib.spread_vector(pts, vals, g, K, 7, 0, None, 1)
+    with pytest.raises(ib.InvalidArgument, match="expected one field per vector component"):
+        ib.interpolate_vector([ib.GridField(g[0])], pts, K, 1)
