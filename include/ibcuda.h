@@ -190,7 +190,8 @@ ibc_status ibc_interpolate_device(ibc_context* ctx, const ibc_grid* grid, ibc_ke
  * are the FP64 operator above, and each result is rounded once when stored
  * -- so a result differs from the FP64 operator on the same (float-valued)
  * inputs by that one rounding.  Same arguments, checks and errors as the
- * FP64 entry points; multi-GPU slabs and binned points stay FP64. */
+ * FP64 entry points (binned points: ibc_bin_points_device_f32 below);
+ * multi-GPU slabs stay FP64. */
 ibc_status ibc_spread_f32(ibc_context* ctx, const ibc_grid* grid, ibc_kernel kernel,
                           ibc_spread_algorithm algorithm, const float* points,
                           const float* values, size_t n_points, size_t n_values,
@@ -222,6 +223,12 @@ ibc_status ibc_bin_points_device(ibc_context* ctx, ibc_binned* b, const ibc_grid
                                  ibc_kernel kernel, const double* d_points, size_t n);
 ibc_status ibc_interpolate_binned_device(ibc_context* ctx, const ibc_binned* b,
                                          const double* d_field, double* d_out);
+/* The FP32 storage mode of the two (float points / fields / results, FP64
+ * arithmetic; the binning keeps its own widened copy of the points). */
+ibc_status ibc_bin_points_device_f32(ibc_context* ctx, ibc_binned* b, const ibc_grid* grid,
+                                     ibc_kernel kernel, const float* d_points, size_t n);
+ibc_status ibc_interpolate_binned_device_f32(ibc_context* ctx, const ibc_binned* b,
+                                             const float* d_field, float* d_out);
 
 /* Multi-GPU z-slab decomposition (no reference analog: the
  * paper defers multi-device runs).  A rank owns home planes

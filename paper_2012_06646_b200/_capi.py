@@ -120,6 +120,8 @@ SIGNATURES = {
     "ibc_interpolate_f32": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, C.c_int, _vp]),
     "ibc_spread_device_f32": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, _vp, _vp]),
     "ibc_interpolate_device_f32": (_st, [_vp, _G, C.c_int, _vp, _vp, _sz, _vp]),
+    "ibc_bin_points_device_f32": (_st, [_vp, _vp, _G, C.c_int, _vp, _sz]),
+    "ibc_interpolate_binned_device_f32": (_st, [_vp, _vp, _vp, _vp]),
     "ibc_spread_slab_device": (_st, [_vp, _G, C.POINTER(IbcSlab), C.c_int, _vp, _vp, _sz, _vp, _vp]),
     "ibc_interpolate_slab_device": (_st, [_vp, _G, C.POINTER(IbcSlab), C.c_int, _vp, _vp, _sz, _vp]),
     "ibc_home_planes_device": (_st, [_vp, _G, C.c_int, _vp, _sz, _vp]),

@@ -11,6 +11,8 @@
 //   interpolate               interpolate.hpp:27-28
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include <algorithm>
 #include <atomic>
 #include <condition_variable>
@@ -35,6 +37,7 @@ struct ibc_binned {
   ibc::PointScratch s;
   ibc::DevGrid g{};
   ibc::InterpPlan P;
+  ibc::DevBuf<double> wide;  // FP32 storage mode: the points widened to FP64
   const double* d_points = nullptr;
   size_t n = 0;
   size_t grid_points = 0;
@@ -910,45 +913,70 @@ ibc_status ibc_binned_destroy(ibc_binned* b) {
     if (!b) return;
     cudaSetDevice(b->device);
     b->s.release_all();
+    b->wide.release();
     delete b;
   });
 }
 
+}  // extern "C"
+namespace {
+template <class T>
+void bin_points_dev(ibc_context* ctx, ibc_binned* b, const ibc_grid* grid, ibc_kernel kernel,
+                    const T* d_points, size_t n) {
+  if (!ctx || !b) invalid("null argument");
+  check_grid(grid);
+  check_kernel(kernel);
+  check_points(n);
+  if (n && !d_points) invalid("null point buffer");
+  auto& c = ctx->c;
+  use_device(c);
+  b->ready = false;
+  b->g = ibc::make_devgrid(*grid, (int)kernel);
+  b->s.reserve_points(n, false);
+  b->s.reserve_rows(b->g.nrows);
+  const double* pts = nullptr;
+  if constexpr (std::is_same_v<T, float>) pts = ibc::widen(c, d_points, n * grid->dim, b->wide);
+  else pts = d_points;
+  b->P = ibc::interp_bin(c, b->g, pts, n, b->s, true);
+  b->d_points = pts;
+  b->n = n;
+  b->grid_points = grid_points(grid);
+  b->ready = true;
+}
+
+template <class T>
+void interp_binned_dev(ibc_context* ctx, const ibc_binned* b, const T* d_field, T* d_out) {
+  if (!ctx || !b) invalid("null argument");
+  if (!b->ready) invalid("points have not been binned");
+  if (b->n && (!d_field || !d_out)) invalid("null buffer");
+  auto& c = ctx->c;
+  use_device(c);
+  ibc::interp_gather(c, b->g, b->P, d_field, b->d_points, b->n, const_cast<ibc::PointScratch&>(b->s),
+                     d_out);
+  g_delta_evaluations.fetch_add(b->n * (uint64_t)std::pow(b->g.support, b->g.dim),
+                                std::memory_order_relaxed);
+}
+}  // namespace
+extern "C" {
+
 ibc_status ibc_bin_points_device(ibc_context* ctx, ibc_binned* b, const ibc_grid* grid,
                                  ibc_kernel kernel, const double* d_points, size_t n) {
-  return guarded([&] {
-    if (!ctx || !b) invalid("null argument");
-    check_grid(grid);
-    check_kernel(kernel);
-    check_points(n);
-    if (n && !d_points) invalid("null point buffer");
-    auto& c = ctx->c;
-    use_device(c);
-    b->ready = false;
-    b->g = ibc::make_devgrid(*grid, (int)kernel);
-    b->s.reserve_points(n, false);
-    b->s.reserve_rows(b->g.nrows);
-    b->P = ibc::interp_bin(c, b->g, d_points, n, b->s, true);
-    b->d_points = d_points;
-    b->n = n;
-    b->grid_points = grid_points(grid);
-    b->ready = true;
-  });
+  return guarded([&] { bin_points_dev(ctx, b, grid, kernel, d_points, n); });
+}
+
+ibc_status ibc_bin_points_device_f32(ibc_context* ctx, ibc_binned* b, const ibc_grid* grid,
+                                     ibc_kernel kernel, const float* d_points, size_t n) {
+  return guarded([&] { bin_points_dev(ctx, b, grid, kernel, d_points, n); });
 }
 
 ibc_status ibc_interpolate_binned_device(ibc_context* ctx, const ibc_binned* b,
                                          const double* d_field, double* d_out) {
-  return guarded([&] {
-    if (!ctx || !b) invalid("null argument");
-    if (!b->ready) invalid("points have not been binned");
-    if (b->n && (!d_field || !d_out)) invalid("null buffer");
-    auto& c = ctx->c;
-    use_device(c);
-    ibc::interp_gather(c, b->g, b->P, d_field, b->d_points, b->n,
-                       const_cast<ibc::PointScratch&>(b->s), d_out);
-    g_delta_evaluations.fetch_add(b->n * (uint64_t)std::pow(b->g.support, b->g.dim),
-                                  std::memory_order_relaxed);
-  });
+  return guarded([&] { interp_binned_dev(ctx, b, d_field, d_out); });
+}
+
+ibc_status ibc_interpolate_binned_device_f32(ibc_context* ctx, const ibc_binned* b,
+                                             const float* d_field, float* d_out) {
+  return guarded([&] { interp_binned_dev(ctx, b, d_field, d_out); });
 }
 
 // ---------------------------------------------------------------- Primitives

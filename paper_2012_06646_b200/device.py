@@ -151,11 +151,14 @@ class DeviceOperators:
         the field-independent half of `interpolate`, reusable for any number
         of fields at the same points.  `points` must stay unchanged."""
         n = points.shape[0] if points.dim() == 2 else points.numel() // grid.dim
-        _require(points, "points", n * grid.dim)
+        dt, sfx = _precision(points)
+        _require(points, "points", n * grid.dim, dt)
         b = binned if binned is not None else BinnedPoints(self.context)
         self._sync_stream()
-        check(load().ibc_bin_points_device(self.context.handle, b.handle, C.byref(grid.c_grid),
-                                           _kernel_code(kernel), _ptr(points), n))
+        check(getattr(load(), "ibc_bin_points_device" + sfx)(
+            self.context.handle, b.handle, C.byref(grid.c_grid), _kernel_code(kernel),
+            _ptr(points), n))
+        b.dtype = dt
         b.n, b.grid = n, grid
         b._points = points  # keep the binned tensor alive
         return b
@@ -164,13 +167,15 @@ class DeviceOperators:
         """Interpolate `field` at binned points (ibc_interpolate_binned_device)."""
         import torch
 
-        _require(field, "field", binned.grid.point_count())
+        dt = getattr(binned, "dtype", torch.float64)  # the binned points' precision
+        sfx = "_f32" if dt == torch.float32 else ""
+        _require(field, "field", binned.grid.point_count(), dt)
         if out is None:
-            out = torch.empty(binned.n, dtype=torch.float64, device=field.device)
-        _require(out, "out", binned.n)
+            out = torch.empty(binned.n, dtype=dt, device=field.device)
+        _require(out, "out", binned.n, dt)
         self._sync_stream()
-        check(load().ibc_interpolate_binned_device(self.context.handle, binned.handle,
-                                                   _ptr(field), _ptr(out)))
+        check(getattr(load(), "ibc_interpolate_binned_device" + sfx)(
+            self.context.handle, binned.handle, _ptr(field), _ptr(out)))
         return out
 
     @property

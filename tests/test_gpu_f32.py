@@ -144,3 +144,18 @@ def test_f32_rejects_mixed_precision(torch_cuda):
     with pytest.raises(ib.InvalidArgument):
         ops.interpolate(torch.zeros(g.point_count(), dtype=torch.float32, device="cuda"),
                         p.double(), g)
+
+
+def test_f32_binned_equals_unbinned(torch_cuda):
+    # ibc_bin_points_device_f32 / ibc_interpolate_binned_device_f32: the same
+    # results as ibc_interpolate_device_f32, bit for bit, for several fields
+    torch = torch_cuda
+    rng = np.random.default_rng(9)
+    for ext, per in (([64, 48, 40], [True] * 3), ([40, 36, 24], [False, True, True])):
+        g = ib.StaggeredGrid(ext, 0.25, [0.5, 0.5, 0.0], per)
+        pts = torch.from_numpy(rand32(g, 20000, rng)).cuda()
+        ops = DeviceOperators(0)
+        b = ops.bin_points(pts, g)
+        for s in range(3):
+            f = torch.from_numpy(rng.uniform(-1, 1, g.point_count()).astype(np.float32)).cuda()
+            assert torch.equal(ops.interpolate_binned(f, b), ops.interpolate(f, pts, g))
